@@ -1,0 +1,142 @@
+/*
+ * sbd_b200.h -- C ABI of the B200-native Sparse Bessel Decomposition apply path.
+ *
+ * Drop-in boundary for the reference C++ library's online path (reference:
+ * /root/reference/proj/include/sbd/conv_operator.hpp and nufft.hpp). Plain
+ * pointers and sizes only; complex arrays are interleaved (re, im) float64
+ * exactly like std::complex<double> (reference vec2.hpp:8), points are (x, y)
+ * float64 pairs exactly like sbd::Vec2 (vec2.hpp:10-23).
+ *
+ * Every entry point returns an int status (SBD_OK = 0). On failure the
+ * thread-local message is available from sbd_last_error(). The C++ wrapper in
+ * sbd_b200.hpp maps the codes back onto the exception types the reference
+ * throws (conv_operator.cpp:246-247, 265, 303; nufft.cpp:158-160, 387-388).
+ *
+ * Entry point                     replaces (reference file:line)
+ * ------------------------------  -----------------------------------------------
+ * sbd_op_assemble                 CompressedOperator::assemble  conv_operator.cpp:244-294
+ * sbd_op_load / sbd_op_save       CompressedOperator::load/save conv_operator.cpp:449-490 / 357-397
+ * sbd_op_apply                    CompressedOperator::apply     conv_operator.cpp:301-309
+ * sbd_op_apply_adjoint            CompressedOperator::apply_adjoint conv_operator.cpp:311-324
+ * sbd_op_apply_device[_adjoint]   (same, device buffers on a caller stream; no reference analogue)
+ * sbd_op_info / sbd_op_get        accessors + bytes()           conv_operator.hpp:56-70
+ * sbd_nufft_create/apply/...      NufftPlan ctor/apply/apply_transpose nufft.cpp:369-398
+ * sbd_ndft_direct                 ndft_direct                   nufft.cpp:76-93
+ * sbd_choose_parameters           choose_parameters             conv_operator.cpp:121-133
+ */
+#ifndef SBD_B200_H
+#define SBD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum sbd_status {
+    SBD_OK = 0,
+    SBD_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+    SBD_ERR_DOMAIN = 2,           /* std::domain_error */
+    SBD_ERR_RUNTIME = 3,          /* std::runtime_error */
+    SBD_ERR_CUDA = 4,             /* CUDA / cuFFT failure (no reference analogue) */
+    SBD_ERR_CONVERGENCE = 5       /* SbdConvergenceError (sbd.hpp:31-38) */
+};
+
+enum sbd_kernel_kind { SBD_KERNEL_LAPLACE = 0, SBD_KERNEL_HELMHOLTZ = 1 };
+
+typedef struct sbd_op sbd_op;
+typedef struct sbd_nufft sbd_nufft;
+
+/* AssembleOptions (conv_operator.hpp:24-31) plus the device ordinal. */
+typedef struct sbd_assemble_options {
+    double eps;                      /* 1e-6 */
+    double alpha;                    /* 0 */
+    double a_override;               /* 0: N-based rule (conv_operator.cpp:263-269) */
+    double small_k_factor;           /* 0.5 */
+    uint64_t nufft_direct_threshold; /* 2^20 */
+    uint64_t max_grid_bytes;         /* 4 GiB */
+    int device;                      /* CUDA ordinal */
+} sbd_assemble_options;
+
+typedef struct sbd_op_info_t {
+    uint64_t n_src, n_tgt, n_xi, nnz;
+    int single_cloud, kind;
+    double k, eps, alpha, a, delta_min, delta_max, nufft_tol;
+    int P;                           /* SBD order */
+    int w;                           /* NUFFT kernel width (both plans) */
+    double beta;                     /* KB shape parameter */
+    int n1_in, n2_in, n1_out, n2_out; /* oversampled grids (0 on the direct path) */
+    int fast_in, fast_out;           /* fast (gridded) vs direct path per plan */
+    uint64_t bytes;                  /* CompressedOperator::bytes() (conv_operator.cpp:338-353) */
+    uint64_t device_bytes;           /* HBM actually held by this operator */
+} sbd_op_info_t;
+
+const char* sbd_last_error(void);
+const char* sbd_version(void);
+
+void sbd_assemble_options_default(sbd_assemble_options* o);
+
+/* ---- operator lifecycle ---- */
+int sbd_op_assemble(int kind, double k, const double* src_xy, uint64_t n_src,
+                    const double* tgt_xy /* NULL: single cloud */, uint64_t n_tgt,
+                    const sbd_assemble_options* opts, sbd_op** out);
+int sbd_op_load(const char* path, int device, uint64_t max_grid_bytes /* 0: 4 GiB */,
+                sbd_op** out);
+int sbd_op_save(const sbd_op* op, const char* path);
+int sbd_op_destroy(sbd_op* op);
+int sbd_op_info(const sbd_op* op, sbd_op_info_t* info);
+
+/* Copies an operator array to host memory. which: 0 src points (2*n_src),
+ * 1 tgt points (2*n_tgt), 2 freqs (2*n_xi), 3 weights (2*n_xi),
+ * 4 D row_offsets (u64, n_tgt+1), 5 D cols (u32, nnz), 6 D values (2*nnz),
+ * 7 ring_offsets (i32), 8 SBD coeffs, 9 SBD roots, 10 SBD norm constants.
+ * With dst == NULL only *count (elements of the natural type) is written. */
+int sbd_op_get(const sbd_op* op, int which, void* dst, uint64_t* count);
+
+/* ---- the hot path ---- */
+/* q = A f for nrhs right-hand sides stored back to back (f: nrhs x n_src,
+ * q: nrhs x n_tgt, interleaved complex). Host buffers; copies are inside. */
+int sbd_op_apply(sbd_op* op, const double* f, double* q, int nrhs);
+int sbd_op_apply_adjoint(sbd_op* op, const double* u, double* q, int nrhs);
+/* Same on device buffers, enqueued on `stream` (cudaStream_t; NULL = the
+ * operator's own stream). Returns without synchronising. */
+int sbd_op_apply_device(sbd_op* op, const double* d_f, double* d_q, int nrhs, void* stream);
+int sbd_op_apply_adjoint_device(sbd_op* op, const double* d_u, double* d_q, int nrhs,
+                                void* stream);
+
+/* Per-stage CUDA-event timing of the most recent apply (profiling must be
+ * enabled first). names: "spread_src", "fft_in", "interp_xi", "spread_xi",
+ * "fft_out", "interp_tgt", "spmv", ... ms[i] in milliseconds. Returns count. */
+int sbd_op_set_profiling(sbd_op* op, int enable);
+int sbd_op_stage_times(sbd_op* op, double* ms, const char** names, int cap);
+
+/* ---- standalone type-III NUFFT (NufftPlan) ---- */
+/* mode: 0 Auto, 1 Direct, 2 Fast (nufft.hpp:18-24). */
+int sbd_nufft_create(const double* points, uint64_t np, const double* freqs, uint64_t nf, int sign,
+                     double tol, int mode, uint64_t direct_threshold, uint64_t max_grid_bytes,
+                     int device, sbd_nufft** out);
+int sbd_nufft_apply(sbd_nufft* p, const double* coeffs, double* out);
+int sbd_nufft_apply_transpose(sbd_nufft* p, const double* values, double* out);
+/* fast, w, n1, n2 (n1 = n2 = 0 on the direct path) */
+int sbd_nufft_info(const sbd_nufft* p, int* fast, int* w, int* n1, int* n2);
+int sbd_nufft_destroy(sbd_nufft* p);
+
+int sbd_ndft_direct(const double* points, uint64_t np, const double* freqs, uint64_t nf,
+                    const double* coeffs, int sign, int device, double* out);
+
+/* choose_parameters (conv_operator.cpp:121-133). */
+int sbd_choose_parameters(uint64_t n, double eps, double alpha, double* a, int* p_hint);
+
+/* Number of CUDA kernels this library launched since load (process-wide). */
+uint64_t sbd_kernel_launch_count(void);
+
+/* Diagnostics: sup-norm error of the device Kaiser-Bessel window polynomials
+ * for width w and shape beta, relative to the window peak I0(beta). */
+double sbd_window_fit_error(int w, double beta);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,464 @@
+// kernels.cu -- sm_100a kernels of the SBD apply path (first correct version).
+//
+// Stage map (reference file:line -> kernel):
+//   plan geometry per point/output  nufft.cpp:163-192     -> k_plan_points / k_plan_outputs
+//   SPREAD                          nufft.cpp:229-250     -> k_spread<W>
+//   DECONV + INTERP                 nufft.cpp:254-283     -> k_interp<W> (deconv folded into taps)
+//   transpose spread/deconv/gather  nufft.cpp:308-361     -> k_spread<W>(deconv) / k_interp<W>
+//   direct sum                      nufft.cpp:76-93       -> k_ndft
+//   omega-hat multiply              conv_operator.cpp:305 -> fused into k_interp (mult)
+//   CSR SpMV q += D f               point_cloud.cpp:116-123 -> k_spmv
+//   adjoint q += D^H u              point_cloud.cpp:125-132 -> k_spmv_adjoint
+#include <cub/cub.cuh>
+
+#include "sbd_internal.h"
+
+namespace sbdgpu {
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// kb_window_hat (nufft.cpp:34-45), arguments formed without FMA contraction so
+// they round exactly like the reference's host code.
+__device__ double kb_hat(double beta, double w) {
+    const double s2 = __dsub_rn(__dmul_rn(beta, beta), __dmul_rn(w, w));
+    if (s2 > 1e-12) {
+        const double s = sqrt(s2);
+        return __ddiv_rn(2.0 * sinh(s), s);
+    }
+    if (s2 < -1e-12) {
+        const double s = sqrt(-s2);
+        return __ddiv_rn(2.0 * sin(s), s);
+    }
+    return __dmul_rn(2.0, __dadd_rn(1.0, __ddiv_rn(s2, 6.0)));
+}
+
+// Per-point plan arrays (nufft.cpp:163-177).
+__global__ void k_plan_points(const double2* __restrict__ pts, uint64_t n, Axis ax, Axis ay,
+                              double beta, double2* __restrict__ t, double2* __restrict__ pre) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double2 p = pts[k];
+    const double px = __dsub_rn(p.x, ax.center);
+    const double py = __dsub_rn(p.y, ay.center);
+    const double ux = __ddiv_rn(px, ax.gamma);
+    const double uy = __ddiv_rn(py, ay.gamma);
+    const double two_pi = 2.0 * kPi;
+    t[k] = make_double2(__ddiv_rn(__dmul_rn(__dadd_rn(ux, kPi), (double)ax.n), two_pi),
+                        __ddiv_rn(__dmul_rn(__dadd_rn(uy, kPi), (double)ay.n), two_pi));
+    const double phase = __dadd_rn(__dmul_rn(px, ax.fcenter), __dmul_rn(py, ay.fcenter));
+    const double dec = __dmul_rn(__dmul_rn(ax.alpha2, kb_hat(beta, __dmul_rn(ax.alpha2, px))),
+                                 __dmul_rn(ay.alpha2, kb_hat(beta, __dmul_rn(ay.alpha2, py))));
+    double sn, cs;
+    sincos(phase, &sn, &cs);
+    pre[k] = make_double2(__ddiv_rn(cs, dec), __ddiv_rn(sn, dec));
+}
+
+// Per-output plan arrays (nufft.cpp:179-192). sgn = sign of the plan.
+__global__ void k_plan_outputs(const double2* __restrict__ frq, uint64_t n, Axis ax, Axis ay,
+                               double sgn, double cxy, double2* __restrict__ s,
+                               double2* __restrict__ post) {
+    const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const double2 f = frq[v];
+    const double fx = __dmul_rn(sgn, f.x), fy = __dmul_rn(sgn, f.y);
+    s[v] = make_double2(__dmul_rn(ax.gamma, __dsub_rn(fx, ax.fcenter)),
+                        __dmul_rn(ay.gamma, __dsub_rn(fy, ay.fcenter)));
+    const double phase = __dadd_rn(__dmul_rn(ax.center, fx), __dmul_rn(ay.center, fy));
+    double sn, cs;
+    sincos(phase, &sn, &cs);
+    post[v] = make_double2(__dmul_rn(cs, cxy), __dmul_rn(sn, cxy));
+}
+
+__global__ void k_bin_keys(const double2* __restrict__ pos, uint64_t n, GridGeom g, int tile,
+                           uint32_t* __restrict__ keys) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double2 p = pos[k];
+    int ix = (int)ceil(p.x - g.half), iy = (int)ceil(p.y - g.half);
+    ix = ((ix % g.n1) + g.n1) % g.n1;
+    iy = ((iy % g.n2) + g.n2) % g.n2;
+    const uint32_t ntx = (uint32_t)((g.n2 + tile - 1) / tile);
+    keys[k] = (uint32_t)(ix / tile) * ntx + (uint32_t)(iy / tile);
+}
+
+__global__ void k_iota(uint32_t* v, uint64_t n) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k < n) v[k] = (uint32_t)k;
+}
+
+template <typename T>
+__global__ void k_gather(const T* __restrict__ src, const uint32_t* __restrict__ perm,
+                         T* __restrict__ dst, uint64_t n) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k < n) dst[k] = src[perm[k]];
+}
+
+// Window taps at sub-cell offset u in [0,1): w[i] = phi((u - w/2 + i)/(w/2)).
+template <int W>
+__device__ __forceinline__ void kb_taps(double u, const WindowPoly& P, double (&wt)[W]) {
+    const double v = 2.0 * u - 1.0;
+    const double v2 = v * v;
+#pragma unroll
+    for (int i = 0; i < W / 2; ++i) {
+        double e = P.e[i][kHorner - 1], o = P.o[i][kHorner - 1];
+#pragma unroll
+        for (int h = kHorner - 2; h >= 0; --h) {
+            e = fma(e, v2, P.e[i][h]);
+            o = fma(o, v2, P.o[i][h]);
+        }
+        wt[i] = fma(v, o, e);
+        wt[W - 1 - i] = fma(-v, o, e);
+    }
+    if (W & 1) {
+        constexpr int m = W / 2;
+        double e = P.e[m][kHorner - 1];
+#pragma unroll
+        for (int h = kHorner - 2; h >= 0; --h) e = fma(e, v2, P.e[m][h]);
+        wt[m] = e;
+    }
+}
+
+__device__ __forceinline__ int wrap_base(int i, int n) {
+    int r = i % n;
+    return r < 0 ? r + n : r;
+}
+
+// Spread (nufft.cpp:229-250): one thread per point, fp64 reductions into the
+// full grid. b = in * phase (* mult); taps optionally carry deconv factors
+// (transpose path, nufft.cpp:328-335).
+template <int W>
+__global__ void __launch_bounds__(256) k_spread(WindowPoly P, GridGeom g, uint64_t n,
+                                                const uint32_t* __restrict__ perm,
+                                                const double2* __restrict__ in,
+                                                const double2* __restrict__ pos,
+                                                const double2* __restrict__ phase,
+                                                const double2* __restrict__ mult,
+                                                const double* __restrict__ dxt,
+                                                const double* __restrict__ dyt,
+                                                double2* __restrict__ grid, int conj_in) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double2 c = in[perm ? perm[k] : k];
+    if (conj_in) c.y = -c.y;
+    double2 b = cmul(c, phase[k]);
+    if (mult) b = cmul(b, mult[k]);
+    if (b.x == 0.0 && b.y == 0.0) return;
+    const double2 t = pos[k];
+    const int ix0 = (int)ceil(t.x - g.half), iy0 = (int)ceil(t.y - g.half);
+    double wx[W], wy[W];
+    kb_taps<W>((ix0 - t.x) + g.half, P, wx);
+    kb_taps<W>((iy0 - t.y) + g.half, P, wy);
+    const int mx0 = wrap_base(ix0, g.n1), my0 = wrap_base(iy0, g.n2);
+    if (dyt) {
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            int my = my0 + j;
+            if (my >= g.n2) my -= g.n2;
+            wy[j] *= dyt[my];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        int mx = mx0 + i;
+        if (mx >= g.n1) mx -= g.n1;
+        double wxi = wx[i];
+        if (dxt) wxi *= dxt[mx];
+        const double bxr = b.x * wxi, bxi = b.y * wxi;
+        double* row = reinterpret_cast<double*>(grid + (size_t)mx * g.n2);
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            int my = my0 + j;
+            if (my >= g.n2) my -= g.n2;
+            atomicAdd(row + 2 * my, bxr * wy[j]);
+            atomicAdd(row + 2 * my + 1, bxi * wy[j]);
+        }
+    }
+}
+
+// Interp (nufft.cpp:254-283): one thread per output; deconvolution folded
+// into the taps (exact: stencils never leave the band).
+template <int W>
+__global__ void __launch_bounds__(256) k_interp(WindowPoly P, GridGeom g, uint64_t n,
+                                                const double2* __restrict__ pos,
+                                                const double2* __restrict__ phase,
+                                                const double2* __restrict__ mult,
+                                                const double* __restrict__ dxt,
+                                                const double* __restrict__ dyt,
+                                                const double2* __restrict__ grid,
+                                                const uint32_t* __restrict__ perm,
+                                                double2* __restrict__ out, int accumulate,
+                                                int conj_out) {
+    const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const double2 s = pos[v];
+    const int jx0 = (int)ceil(s.x - g.half), jy0 = (int)ceil(s.y - g.half);
+    double wx[W], wy[W];
+    kb_taps<W>((jx0 - s.x) + g.half, P, wx);
+    kb_taps<W>((jy0 - s.y) + g.half, P, wy);
+    const int mx0 = wrap_base(jx0, g.n1), my0 = wrap_base(jy0, g.n2);
+    int myj[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        int my = my0 + j;
+        if (my >= g.n2) my -= g.n2;
+        myj[j] = my;
+        if (dyt) wy[j] *= dyt[my];
+    }
+    double ar = 0.0, ai = 0.0;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        int mx = mx0 + i;
+        if (mx >= g.n1) mx -= g.n1;
+        const double2* row = grid + (size_t)mx * g.n2;
+        double rr = 0.0, ri = 0.0;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            const double2 gv = __ldg(row + myj[j]);
+            rr = fma(gv.x, wy[j], rr);
+            ri = fma(gv.y, wy[j], ri);
+        }
+        const double wxi = dxt ? wx[i] * dxt[mx] : wx[i];
+        ar = fma(rr, wxi, ar);
+        ai = fma(ri, wxi, ai);
+    }
+    double2 o = cmul(make_double2(ar, ai), phase[v]);
+    if (mult) o = cmul(o, mult[v]);
+    if (conj_out) o.y = -o.y;
+    const uint64_t dst = perm ? perm[v] : v;
+    if (accumulate) {
+        double2 q = out[dst];
+        q.x += o.x;
+        q.y += o.y;
+        out[dst] = q;
+    } else {
+        out[dst] = o;
+    }
+}
+
+// Direct sum (nufft.cpp:76-93): thread per output, sequential over points in
+// the caller's order (same summation order as the reference).
+__global__ void k_ndft(const double2* __restrict__ pts, uint64_t np,
+                       const double2* __restrict__ frq, uint64_t nf,
+                       const double2* __restrict__ c, double sgn, double2* __restrict__ out) {
+    const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (v >= nf) return;
+    const double fx = __dmul_rn(sgn, frq[v].x), fy = __dmul_rn(sgn, frq[v].y);
+    double ar = 0.0, ai = 0.0;
+    for (uint64_t k = 0; k < np; ++k) {
+        const double2 z = pts[k];
+        const double phase = __dadd_rn(__dmul_rn(z.x, fx), __dmul_rn(z.y, fy));
+        double sn, cs;
+        sincos(phase, &sn, &cs);
+        const double2 ck = c[k];
+        ar = __dadd_rn(ar, __dsub_rn(__dmul_rn(ck.x, cs), __dmul_rn(ck.y, sn)));
+        ai = __dadd_rn(ai, __dadd_rn(__dmul_rn(ck.x, sn), __dmul_rn(ck.y, cs)));
+    }
+    out[v] = make_double2(ar, ai);
+}
+
+__global__ void k_mul(double2* x, const double2* __restrict__ m, uint64_t n) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k < n) x[k] = cmul(x[k], m[k]);
+}
+
+__global__ void k_conj(const double2* __restrict__ in, double2* out, uint64_t n) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k < n) out[k] = make_double2(in[k].x, -in[k].y);
+}
+
+// q_k += sum_{i in row k} D_i f_{col i}, sequential in CSR order like
+// point_cloud.cpp:116-123.
+__global__ void k_spmv(uint64_t rows, const uint64_t* __restrict__ ro,
+                       const uint32_t* __restrict__ cols, const double2* __restrict__ vals,
+                       const double2* __restrict__ f, double2* __restrict__ q) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= rows) return;
+    double ar = 0.0, ai = 0.0;
+    for (uint64_t i = ro[k]; i < ro[k + 1]; ++i) {
+        const double2 v = vals[i];
+        const double2 x = f[cols[i]];
+        ar += v.x * x.x - v.y * x.y;
+        ai += v.x * x.y + v.y * x.x;
+    }
+    double2 o = q[k];
+    o.x += ar;
+    o.y += ai;
+    q[k] = o;
+}
+
+// q_{col} += conj(D_i) u_k (point_cloud.cpp:125-132), fp64 reductions.
+__global__ void k_spmv_adjoint(uint64_t rows, const uint64_t* __restrict__ ro,
+                               const uint32_t* __restrict__ cols,
+                               const double2* __restrict__ vals,
+                               const double2* __restrict__ u, double2* q) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= rows) return;
+    const double2 uk = u[k];
+    for (uint64_t i = ro[k]; i < ro[k + 1]; ++i) {
+        const double2 v = vals[i];
+        double* dst = reinterpret_cast<double*>(q + cols[i]);
+        atomicAdd(dst, v.x * uk.x + v.y * uk.y);
+        atomicAdd(dst + 1, v.x * uk.y - v.y * uk.x);
+    }
+}
+
+inline unsigned blocks(uint64_t n, unsigned t) { return (unsigned)((n + t - 1) / t); }
+
+template <template <int> class F, typename... Args>
+void dispatch_w(int w, Args&&... args) {
+    switch (w) {
+#define SBD_W(N) \
+    case N: F<N>::run(args...); break;
+        SBD_W(4) SBD_W(5) SBD_W(6) SBD_W(7) SBD_W(8) SBD_W(9) SBD_W(10) SBD_W(11) SBD_W(12)
+        SBD_W(13) SBD_W(14) SBD_W(15) SBD_W(16) SBD_W(17)
+#undef SBD_W
+        default: throw Error(3, "unsupported kernel width");
+    }
+}
+
+template <int W>
+struct SpreadRun {
+    static void run(const WindowPoly& P, GridGeom g, uint64_t n, const uint32_t* perm,
+                    const double2* in, const double2* pos, const double2* phase,
+                    const double2* mult, const double* dx, const double* dy, double2* grid,
+                    int conj_in, cudaStream_t st) {
+        k_spread<W><<<blocks(n, 256), 256, 0, st>>>(P, g, n, perm, in, pos, phase, mult, dx, dy,
+                                                    grid, conj_in);
+    }
+};
+
+template <int W>
+struct InterpRun {
+    static void run(const WindowPoly& P, GridGeom g, uint64_t n, const double2* pos,
+                    const double2* phase, const double2* mult, const double* dx, const double* dy,
+                    const double2* grid, const uint32_t* perm, double2* out, int acc, int cj,
+                    cudaStream_t st) {
+        k_interp<W><<<blocks(n, 256), 256, 0, st>>>(P, g, n, pos, phase, mult, dx, dy, grid, perm,
+                                                    out, acc, cj);
+    }
+};
+
+} // namespace
+
+void launch_plan_points(const double2* pts, uint64_t n, Axis ax, Axis ay, double beta,
+                        double2* t, double2* pre, cudaStream_t st) {
+    if (!n) return;
+    k_plan_points<<<blocks(n, 256), 256, 0, st>>>(pts, n, ax, ay, beta, t, pre);
+    count_launch();
+    ck(cudaGetLastError(), "k_plan_points");
+}
+
+void launch_plan_outputs(const double2* frq, uint64_t n, Axis ax, Axis ay, double sgn,
+                         double2* s, double2* post, cudaStream_t st) {
+    if (!n) return;
+    const double cx = 2.0 * kPi / (ax.n * ax.gamma);
+    const double cy = 2.0 * kPi / (ay.n * ay.gamma);
+    k_plan_outputs<<<blocks(n, 256), 256, 0, st>>>(frq, n, ax, ay, sgn, cx * cy, s, post);
+    count_launch();
+    ck(cudaGetLastError(), "k_plan_outputs");
+}
+
+void launch_bin_keys(const double2* pos, uint64_t n, GridGeom g, int tile, uint32_t* keys,
+                     cudaStream_t st) {
+    if (!n) return;
+    k_bin_keys<<<blocks(n, 256), 256, 0, st>>>(pos, n, g, tile, keys);
+    count_launch();
+    ck(cudaGetLastError(), "k_bin_keys");
+}
+
+void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st) {
+    if (!n) return;
+    k_iota<<<blocks(n, 256), 256, 0, st>>>(v, n);
+    count_launch();
+}
+
+void sort_by_key(uint32_t* keys, uint32_t* vals, uint64_t n, cudaStream_t st) {
+    if (n < 2) return;
+    DevBuf<uint32_t> k2(n), v2(n);
+    size_t tmp = 0;
+    ck(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, k2.p, vals, v2.p, (int)n, 0, 32, st),
+       "cub sort (size)");
+    DevBuf<unsigned char> t(tmp);
+    ck(cub::DeviceRadixSort::SortPairs(t.p, tmp, keys, k2.p, vals, v2.p, (int)n, 0, 32, st),
+       "cub sort");
+    count_launch(4);
+    ck(cudaMemcpyAsync(keys, k2.p, n * 4, cudaMemcpyDeviceToDevice, st), "sort copy");
+    ck(cudaMemcpyAsync(vals, v2.p, n * 4, cudaMemcpyDeviceToDevice, st), "sort copy");
+    ck(cudaStreamSynchronize(st), "sort sync");
+}
+
+template <typename T>
+void launch_gather(const T* src, const uint32_t* perm, T* dst, uint64_t n, cudaStream_t st) {
+    if (!n) return;
+    k_gather<T><<<blocks(n, 256), 256, 0, st>>>(src, perm, dst, n);
+    count_launch();
+}
+template void launch_gather<double2>(const double2*, const uint32_t*, double2*, uint64_t,
+                                     cudaStream_t);
+template void launch_gather<uint32_t>(const uint32_t*, const uint32_t*, uint32_t*, uint64_t,
+                                      cudaStream_t);
+
+void launch_spread(int w, const WindowPoly& win, GridGeom g, uint64_t n, const uint32_t* perm,
+                   const double2* in, const double2* pos, const double2* phase,
+                   const double2* mult, const double* dx, const double* dy, double2* grid,
+                   int conj_in, cudaStream_t st) {
+    if (!n) return;
+    dispatch_w<SpreadRun>(w, win, g, n, perm, in, pos, phase, mult, dx, dy, grid, conj_in, st);
+    count_launch();
+    ck(cudaGetLastError(), "k_spread");
+}
+
+void launch_interp(int w, const WindowPoly& win, GridGeom g, uint64_t n, const double2* pos,
+                   const double2* phase, const double2* mult, const double* dx, const double* dy,
+                   const double2* grid, const uint32_t* perm, double2* out, int accumulate,
+                   int conj_out, cudaStream_t st) {
+    if (!n) return;
+    dispatch_w<InterpRun>(w, win, g, n, pos, phase, mult, dx, dy, grid, perm, out, accumulate,
+                          conj_out, st);
+    count_launch();
+    ck(cudaGetLastError(), "k_interp");
+}
+
+void launch_ndft(const double2* pts, uint64_t np, const double2* frq, uint64_t nf,
+                 const double2* c, int sign, double2* out, cudaStream_t st) {
+    if (!nf) return;
+    k_ndft<<<blocks(nf, 128), 128, 0, st>>>(pts, np, frq, nf, c, sign > 0 ? 1.0 : -1.0, out);
+    count_launch();
+    ck(cudaGetLastError(), "k_ndft");
+}
+
+void launch_mul(double2* x, const double2* m, uint64_t n, cudaStream_t st) {
+    if (!n) return;
+    k_mul<<<blocks(n, 256), 256, 0, st>>>(x, m, n);
+    count_launch();
+}
+
+void launch_conj(const double2* in, double2* out, uint64_t n, cudaStream_t st) {
+    if (!n) return;
+    k_conj<<<blocks(n, 256), 256, 0, st>>>(in, out, n);
+    count_launch();
+}
+
+void launch_spmv(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double2* vals,
+                 const double2* f, double2* q, cudaStream_t st) {
+    if (!rows) return;
+    k_spmv<<<blocks(rows, 256), 256, 0, st>>>(rows, ro, cols, vals, f, q);
+    count_launch();
+    ck(cudaGetLastError(), "k_spmv");
+}
+
+void launch_spmv_adjoint(uint64_t rows, const uint64_t* ro, const uint32_t* cols,
+                         const double2* vals, const double2* u, double2* q, cudaStream_t st) {
+    if (!rows) return;
+    k_spmv_adjoint<<<blocks(rows, 256), 256, 0, st>>>(rows, ro, cols, vals, u, q);
+    count_launch();
+    ck(cudaGetLastError(), "k_spmv_adjoint");
+}
+
+} // namespace sbdgpu

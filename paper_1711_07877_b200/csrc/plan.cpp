@@ -1,0 +1,259 @@
+// plan.cpp -- host side of the device type-III NUFFT plan (reference
+// NufftPlan, /root/reference/proj/src/nufft.cpp:97-216, 369-398).
+//
+// The plan geometry (w, beta, centers, gamma, n, alpha1, alpha2) is restated
+// exactly on the host from the coordinate extrema (nufft.cpp:127-160), so the
+// device path uses the same grid, stencil starts and window as the reference;
+// per-point arrays are computed on the device (k_plan_points/k_plan_outputs)
+// with the same operation order. Points and outputs are stored sorted by grid
+// tile for locality.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "sbd_internal.h"
+
+namespace sbdgpu {
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kSigma = 2.0; // nufft.cpp:19
+constexpr int kBinTile = 32;
+
+void span(const double* v, uint64_t n, int comp, double s, double& lo, double& hi) {
+    lo = 1e300;
+    hi = -1e300;
+    for (uint64_t i = 0; i < n; ++i) {
+        const double x = s * v[2 * i + comp];
+        lo = std::min(lo, x);
+        hi = std::max(hi, x);
+    }
+    if (n == 0) lo = hi = 0.0;
+}
+
+std::vector<double> make_deconv(const Axis& a, double beta) {
+    std::vector<double> d(a.n, 0.0);
+    const int band = a.n / (int)(2.0 * kSigma);
+    for (int m = 0; m < a.n; ++m) {
+        const int j = m <= a.n / 2 ? m : m - a.n;
+        if (std::abs(j) > band) continue;
+        const double psi1 = a.alpha1 * kb_window_hat_host(beta, a.alpha1 * j);
+        d[m] = ((j & 1) ? -1.0 : 1.0) / psi1;
+    }
+    return d;
+}
+
+} // namespace
+
+Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf_, int sign_,
+           const NufftOpts& o, int dev, bool sort_points, bool sort_outputs, cudaStream_t st)
+    : sign(sign_ > 0 ? 1 : -1), device(dev), np(np_), nf(nf_), opts(o) {
+    const uint64_t work = np * nf;
+    const bool direct = o.mode == 1 || (o.mode == 0 && work <= o.direct_threshold);
+    pts.upload(reinterpret_cast<const double2*>(pts_xy), np, st);
+    frq.upload(reinterpret_cast<const double2*>(frq_xy), nf, st);
+    if (direct) {
+        fast = false;
+        ck(cudaStreamSynchronize(st), "plan upload");
+        return;
+    }
+
+    // ---- geometry, nufft.cpp:127-160
+    w = width_for_tol(o.tol);
+    beta = 2.3562 * w;
+    const double sg = (double)sign;
+    auto setup_axis = [&](Axis& a, int comp) {
+        double plo, phi, flo, fhi;
+        span(pts_xy, np, comp, 1.0, plo, phi);
+        span(frq_xy, nf, comp, sg, flo, fhi);
+        a.center = 0.5 * (plo + phi);
+        a.fcenter = 0.5 * (flo + fhi);
+        const double X = std::max(0.5 * (phi - plo), 1e-8 * (1.0 + std::fabs(a.center)));
+        const double S = std::max(0.5 * (fhi - flo), 1e-8 * (1.0 + std::fabs(a.fcenter)));
+        a.gamma = kSigma * X / kPi;
+        a.n = next_fast_even((int)std::ceil(2.0 * kSigma * (a.gamma * S + 0.5 * w + 1.0)));
+        a.alpha1 = kPi * w / a.n;
+        a.alpha2 = 0.5 * w / a.gamma;
+    };
+    setup_axis(ax, 0);
+    setup_axis(ay, 1);
+    const uint64_t ncell = (uint64_t)ax.n * (uint64_t)ay.n;
+    if (ncell * 16u > o.max_grid_bytes)
+        throw Error(3, "nufft: oversampled grid exceeds the memory limit");
+    win = fit_window(w, beta);
+    fast = true;
+
+    // ---- per point / per output arrays (nufft.cpp:163-192), caller order
+    t.alloc(np);
+    pre.alloc(np);
+    this->s.alloc(nf);
+    post.alloc(nf);
+    launch_plan_points(pts.p, np, ax, ay, beta, t.p, pre.p, st);
+    launch_plan_outputs(frq.p, nf, ax, ay, sg, this->s.p, post.p, st);
+
+    // ---- deconvolution tables (nufft.cpp:194-205), host exact
+    const std::vector<double> hx = make_deconv(ax, beta), hy = make_deconv(ay, beta);
+    dx.upload(hx.data(), hx.size(), st);
+    dy.upload(hy.data(), hy.size(), st);
+
+    // ---- sort both sides by grid tile of the stencil start
+    const GridGeom g{ax.n, ay.n, 0.5 * w};
+    auto sort_side = [&](DevBuf<double2>& pos, DevBuf<double2>& ph, DevBuf<uint32_t>& perm,
+                         uint64_t n) {
+        if (n < 2) return;
+        DevBuf<uint32_t> keys(n);
+        perm.alloc(n);
+        launch_bin_keys(pos.p, n, g, kBinTile, keys.p, st);
+        launch_iota(perm.p, n, st);
+        sort_by_key(keys.p, perm.p, n, st);
+        DevBuf<double2> a(n), b(n);
+        launch_gather(pos.p, perm.p, a.p, n, st);
+        launch_gather(ph.p, perm.p, b.p, n, st);
+        pos = std::move(a);
+        ph = std::move(b);
+    };
+    if (sort_points) sort_side(t, pre, perm_t, np);
+    if (sort_outputs) sort_side(this->s, post, perm_s, nf);
+
+    // ---- cuFFT: unnormalised e^{+2 pi i jm/n} (FFTW_BACKWARD), row-major
+    // n1 x n2 with the second index fastest (nufft.cpp:207-213, 244).
+    ckfft(cufftPlan2d(&fft, ax.n, ay.n, CUFFT_Z2Z), "cufftPlan2d");
+    ck(cudaStreamSynchronize(st), "plan build");
+}
+
+Plan::~Plan() {
+    if (fft) cufftDestroy(fft);
+}
+
+size_t Plan::device_bytes() const {
+    return pts.bytes() + frq.bytes() + perm_t.bytes() + perm_s.bytes() + t.bytes() + pre.bytes() +
+           s.bytes() + post.bytes() + dx.bytes() + dy.bytes();
+}
+
+// nufft.cpp:218-290
+void Plan::apply(const double2* in, double2* out, double2* grid, cudaStream_t st,
+                 StageTimer* tm, const double2* mult, const char* tag_spread,
+                 const char* tag_fft, const char* tag_interp) const {
+    if (!fast) {
+        if (tm) tm->start(tag_interp);
+        launch_ndft(pts.p, np, frq.p, nf, in, sign, out, st);
+        if (mult) launch_mul(out, mult, nf, st);
+        if (tm) tm->stop();
+        return;
+    }
+    const GridGeom g{ax.n, ay.n, 0.5 * w};
+    if (tm) tm->start(tag_spread);
+    ck(cudaMemsetAsync(grid, 0, cells() * sizeof(double2), st), "grid zero");
+    launch_spread(w, win, g, np, perm_t.n ? perm_t.p : nullptr, in, t.p, pre.p, nullptr, nullptr,
+                  nullptr, grid, 0, st);
+    if (tm) tm->stop();
+    if (tm) tm->start(tag_fft);
+    ckfft(cufftSetStream(fft, st), "cufftSetStream");
+    ckfft(cufftExecZ2Z(fft, reinterpret_cast<cufftDoubleComplex*>(grid),
+                       reinterpret_cast<cufftDoubleComplex*>(grid), CUFFT_INVERSE),
+          "cufftExecZ2Z");
+    count_launch();
+    if (tm) tm->stop();
+    if (tm) tm->start(tag_interp);
+    launch_interp(w, win, g, nf, s.p, post.p, mult, dx.p, dy.p, grid,
+                  perm_s.n ? perm_s.p : nullptr, out, 0, 0, st);
+    if (tm) tm->stop();
+}
+
+// nufft.cpp:295-367
+void Plan::apply_transpose(const double2* in, double2* out, double2* grid, cudaStream_t st,
+                           StageTimer* tm, const double2* mult, int conj_in,
+                           int conj_out) const {
+    if (!fast) {
+        if (tm) tm->start("ndft_T");
+        const double2* src = in;
+        DevBuf<double2> tmp;
+        if (conj_in) {
+            tmp.alloc(nf);
+            launch_conj(in, tmp.p, nf, st);
+            src = tmp.p;
+        }
+        launch_ndft(frq.p, nf, pts.p, np, src, sign, out, st);
+        if (mult) launch_mul(out, mult, np, st);
+        if (conj_out) launch_conj(out, out, np, st);
+        if (tm) tm->stop();
+        if (conj_in) ck(cudaStreamSynchronize(st), "ndft_T tmp");
+        return;
+    }
+    const GridGeom g{ax.n, ay.n, 0.5 * w};
+    if (tm) tm->start("spread_T");
+    ck(cudaMemsetAsync(grid, 0, cells() * sizeof(double2), st), "grid zero");
+    // spread at the frequency stencils with postphase, deconv folded in
+    launch_spread(w, win, g, nf, perm_s.n ? perm_s.p : nullptr, in, s.p, post.p, nullptr, dx.p,
+                  dy.p, grid, conj_in, st);
+    if (tm) tm->stop();
+    if (tm) tm->start("fft_T");
+    ckfft(cufftSetStream(fft, st), "cufftSetStream");
+    ckfft(cufftExecZ2Z(fft, reinterpret_cast<cufftDoubleComplex*>(grid),
+                       reinterpret_cast<cufftDoubleComplex*>(grid), CUFFT_INVERSE),
+          "cufftExecZ2Z");
+    count_launch();
+    if (tm) tm->stop();
+    if (tm) tm->start("interp_T");
+    launch_interp(w, win, g, np, t.p, pre.p, mult, nullptr, nullptr, grid,
+                  perm_t.n ? perm_t.p : nullptr, out, 0, conj_out, st);
+    if (tm) tm->stop();
+}
+
+std::vector<uint32_t> Plan::adopt_point_order(cudaStream_t st) {
+    std::vector<uint32_t> h(np);
+    if (perm_t.n) {
+        ck(cudaMemcpyAsync(h.data(), perm_t.p, np * 4, cudaMemcpyDeviceToHost, st), "perm D2H");
+        ck(cudaStreamSynchronize(st), "perm D2H");
+        perm_t.release();
+    } else {
+        for (uint64_t i = 0; i < np; ++i) h[i] = (uint32_t)i;
+    }
+    if (!fast) {
+        // direct path keeps raw points; reorder them to match
+        std::vector<double2> raw(np), sorted(np);
+        ck(cudaMemcpy(raw.data(), pts.p, np * 16, cudaMemcpyDeviceToHost), "pts D2H");
+        for (uint64_t i = 0; i < np; ++i) sorted[i] = raw[h[i]];
+        pts.upload(sorted.data(), np, st);
+        ck(cudaStreamSynchronize(st), "pts H2D");
+    }
+    return h;
+}
+
+// ------------------------------------------------------------ StageTimer
+void StageTimer::reset() {
+    for (auto e : begin) cudaEventDestroy(e);
+    for (auto e : end) cudaEventDestroy(e);
+    begin.clear();
+    end.clear();
+    names.clear();
+}
+void StageTimer::start(const char* name) {
+    if (!on) return;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, stream);
+    begin.push_back(a);
+    end.push_back(b);
+    names.emplace_back(name);
+}
+void StageTimer::stop() {
+    if (!on || end.empty()) return;
+    cudaEventRecord(end.back(), stream);
+}
+int StageTimer::read(double* ms, const char** nm, int cap) {
+    const int n = (int)names.size();
+    for (int i = 0; i < n && i < cap; ++i) {
+        float f = 0.f;
+        cudaEventSynchronize(end[i]);
+        cudaEventElapsedTime(&f, begin[i], end[i]);
+        if (ms) ms[i] = f;
+        if (nm) nm[i] = names[i].c_str();
+    }
+    return n;
+}
+StageTimer::~StageTimer() { reset(); }
+
+} // namespace sbdgpu

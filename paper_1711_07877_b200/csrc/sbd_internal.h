@@ -1,0 +1,208 @@
+// sbd_internal.h -- internal types shared by the host C++ and the sm_100a
+// kernels of the B200 SBD apply path. Not part of the public ABI
+// (include/sbd_b200.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace sbdgpu {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what);
+[[noreturn]] void throw_cufft(cufftResult r, const char* what);
+inline void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw_cuda(e, what);
+}
+inline void ckfft(cufftResult r, const char* what) {
+    if (r != CUFFT_SUCCESS) throw_cufft(r, what);
+}
+void count_launch(int n = 1);
+
+// ---------------------------------------------------------------- buffers
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p; n = o.n; o.p = nullptr; o.n = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) ck(cudaMalloc(&p, count * sizeof(T) + 64), "cudaMalloc");
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+    void upload(const T* h, size_t count, cudaStream_t s) {
+        if (count > n) alloc(count);
+        if (count) ck(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s), "H2D");
+    }
+};
+
+// ---------------------------------------------------------------- window
+// Kaiser-Bessel window phi(z) = I0(beta sqrt(1 - z^2)) (reference
+// nufft.cpp:28-32) restated per tap as a polynomial in v = 2u - 1 where
+// u = ix0 - t + w/2 in [0, 1) is the (exactly computed) sub-cell offset.
+// Tap i and tap w-1-i share one even/odd split: P_i(v) = E_i(v^2) + v O_i(v^2),
+// P_{w-1-i}(v) = E_i(v^2) - v O_i(v^2). Degree 15 (8 + 8 coefficients) keeps
+// the sup-norm error ~1e-16 of the window peak for every w the reference can
+// choose (4..17); see window.cpp.
+constexpr int kMaxW = 17;
+constexpr int kPairs = (kMaxW + 1) / 2;
+constexpr int kHorner = 8;
+struct WindowPoly {
+    double e[kPairs][kHorner];
+    double o[kPairs][kHorner];
+};
+WindowPoly fit_window(int w, double beta, double* max_rel_err = nullptr);
+double kb_window_host(double beta, double z);     // exact reference formula (long double I0)
+double kb_window_hat_host(double beta, double w); // nufft.cpp:34-45
+
+// ---------------------------------------------------------------- geometry
+// Per-axis plan geometry, restated from nufft.cpp:65-72 / 139-155.
+struct Axis {
+    double center = 0.0, fcenter = 0.0, gamma = 1.0;
+    int n = 0;
+    double alpha1 = 0.0, alpha2 = 0.0;
+};
+
+struct NufftOpts {
+    double tol = 1e-9;
+    int mode = 0; // 0 auto, 1 direct, 2 fast
+    uint64_t direct_threshold = uint64_t(1) << 20;
+    uint64_t max_grid_bytes = uint64_t(4) << 30;
+};
+
+int width_for_tol(double tol);  // nufft.cpp:47-52
+int next_fast_even(int n);      // nufft.cpp:55-63
+
+// Timing of the apply stages with CUDA events (only when profiling).
+struct StageTimer {
+    bool on = false;
+    cudaStream_t stream = nullptr;
+    std::vector<std::string> names;
+    std::vector<cudaEvent_t> begin, end;
+    void reset();
+    void start(const char* name);
+    void stop();
+    int read(double* ms, const char** nm, int cap);
+    ~StageTimer();
+};
+
+// A type-III NUFFT plan on one device (reference NufftPlan, nufft.hpp:30-56).
+// Point side ("t": spread in apply, gather in apply_transpose) and output side
+// ("s": gather in apply, spread in apply_transpose) are stored in a sorted
+// order chosen for locality; perm_* map sorted position -> caller index (empty
+// when the caller's order is kept).
+class Plan {
+  public:
+    Plan(const double* pts_xy, uint64_t np, const double* frq_xy, uint64_t nf, int sign,
+         const NufftOpts& opts, int device, bool sort_points, bool sort_outputs, cudaStream_t st);
+    ~Plan();
+    Plan(const Plan&) = delete;
+    Plan& operator=(const Plan&) = delete;
+
+    bool fast = false;
+    int sign = 1;
+    int device = 0;
+    int w = 0;
+    double beta = 0.0;
+    Axis ax, ay;
+    uint64_t np = 0, nf = 0;
+    WindowPoly win{};
+    NufftOpts opts;
+
+    // direct path (and point/freq sets kept for it)
+    DevBuf<double2> pts, frq;
+    // fast path, sorted
+    DevBuf<uint32_t> perm_t, perm_s;
+    DevBuf<double2> t, pre;  // point side: grid coords (cells), prephase
+    DevBuf<double2> s, post; // output side: mode coords, postphase
+    DevBuf<double> dx, dy;   // deconvolution per FFT index (nufft.cpp:194-205)
+    cufftHandle fft = 0;
+
+    uint64_t cells() const { return fast ? (uint64_t)ax.n * (uint64_t)ay.n : 0; }
+    size_t device_bytes() const;
+
+    // Enqueue apply / apply_transpose on stream `st`. in/out in caller order.
+    // `grid` must hold cells() complex values. `extra` (optional) multiplies
+    // the outputs elementwise in SORTED output order (used for omega-hat).
+    void apply(const double2* in, double2* out, double2* grid, cudaStream_t st,
+               StageTimer* tm, const double2* mult = nullptr, const char* tag_spread = "spread",
+               const char* tag_fft = "fft", const char* tag_interp = "interp") const;
+    void apply_transpose(const double2* in, double2* out, double2* grid, cudaStream_t st,
+                         StageTimer* tm, const double2* mult = nullptr, int conj_in = 0,
+                         int conj_out = 0) const;
+    // Drop the point-side permutation: the caller promises to pass point-side
+    // data in this plan's sorted order from now on. Returns the permutation
+    // (sorted position -> caller index) on the host.
+    std::vector<uint32_t> adopt_point_order(cudaStream_t st);
+};
+
+// ---------------------------------------------------------------- kernels
+// Launchers (kernels.cu). n1/n2 grid sizes, half = w/2.
+struct GridGeom {
+    int n1, n2;
+    double half;
+};
+
+void launch_plan_points(const double2* pts, uint64_t n, Axis ax, Axis ay, double beta,
+                        double2* t, double2* pre, cudaStream_t st);
+void launch_plan_outputs(const double2* frq, uint64_t n, Axis ax, Axis ay, double sgn,
+                         double2* s, double2* post, cudaStream_t st);
+void launch_deconv_tables(Axis a, double beta, double* d, cudaStream_t st);
+void launch_bin_keys(const double2* pos, uint64_t n, GridGeom g, int tile, uint32_t* keys,
+                     cudaStream_t st);
+void sort_by_key(uint32_t* keys, uint32_t* vals, uint64_t n, cudaStream_t st);
+void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st);
+template <typename T>
+void launch_gather(const T* src, const uint32_t* perm, T* dst, uint64_t n, cudaStream_t st);
+
+// spread: grid[...] += (in[perm?perm[k]:k] * phase[k] (* mult[k])) * taps,
+// with optional deconv factors folded into the taps.
+void launch_spread(int w, const WindowPoly& win, GridGeom g, uint64_t n, const uint32_t* perm,
+                   const double2* in, const double2* pos, const double2* phase,
+                   const double2* mult, const double* dx, const double* dy, double2* grid,
+                   int conj_in, cudaStream_t st);
+// interp: out[perm?perm[k]:k] (+)= sum taps * (dx dy) * grid * phase[k] (* mult[k])
+void launch_interp(int w, const WindowPoly& win, GridGeom g, uint64_t n, const double2* pos,
+                   const double2* phase, const double2* mult, const double* dx, const double* dy,
+                   const double2* grid, const uint32_t* perm, double2* out, int accumulate,
+                   int conj_out, cudaStream_t st);
+// direct sum out[v] = sum_k c_k e^{i sign z_k . f_v}
+void launch_ndft(const double2* pts, uint64_t np, const double2* frq, uint64_t nf,
+                 const double2* c, int sign, double2* out, cudaStream_t st);
+void launch_mul(double2* x, const double2* m, uint64_t n, cudaStream_t st);
+void launch_conj(const double2* in, double2* out, uint64_t n, cudaStream_t st);
+void launch_spmv(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double2* vals,
+                 const double2* f, double2* q, cudaStream_t st);
+void launch_spmv_adjoint(uint64_t rows, const uint64_t* ro, const uint32_t* cols,
+                         const double2* vals, const double2* u, double2* q, cudaStream_t st);
+
+} // namespace sbdgpu

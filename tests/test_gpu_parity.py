@@ -1,0 +1,184 @@
+"""GPU parity: the B200 path (through the C ABI) against the reference.
+
+Tolerances (north_star): apply() output matches the reference's on identical
+inputs and parameters to relative l2 <= 1e-9; the direct O(N^2) sum to
+<= eps * sum|f| (the reference's own contract, conv_operator.hpp:50-51).
+Checkers: golden fixtures from the unmodified reference (tests/golden/), the
+compiled reference (oracle/_ref, when present) and the C restatement.
+"""
+import numpy as np
+import pytest
+
+import paper_1711_07877_b200 as sbd
+from tests.conftest import GOLDEN, golden, golden_cases, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+CASES = [c["name"] for c in golden_cases()]
+PARITY = 1e-9
+
+
+@pytest.fixture(scope="module")
+def ops():
+    return {n: sbd.CompressedOperator.load(golden(n)[0]) for n in CASES}
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_apply_matches_reference_golden(ops, name):
+    _, g = golden(name)
+    q = ops[name].apply(g["f"])
+    assert rel_l2(q, g["q"]) <= PARITY
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_apply_adjoint_matches_reference_golden(ops, name):
+    _, g = golden(name)
+    qa = ops[name].apply_adjoint(g["u"])
+    assert rel_l2(qa, g["qa"]) <= PARITY
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_apply_random_rhs_vs_oracle(ops, oracle, name):
+    path, g = golden(name)
+    rng = np.random.default_rng(123)
+    n = len(g["f"])
+    f = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    assert rel_l2(ops[name].apply(f), oracle.op(path).apply(f)) <= PARITY
+
+
+def test_batched_rhs_equals_single(ops):
+    _, g = golden("lap_disk_n1000")
+    rng = np.random.default_rng(5)
+    F = rng.standard_normal((3, len(g["f"]))) + 0j
+    Q = ops["lap_disk_n1000"].apply(F)
+    for r in range(3):
+        assert rel_l2(Q[r], ops["lap_disk_n1000"].apply(F[r])) <= 1e-13
+
+
+def test_direct_sum_contract():
+    # test_operator.cpp:110-126 / north_star: |q - sum_{l!=k} G f_l| <= eps sum|f|
+    path, g = golden("lap_disk_n1000")
+    op = sbd.CompressedOperator.load(path)
+    z = op.source().points
+    f = g["f"]
+    q = op.apply(f)
+    rng = np.random.default_rng(0)
+    rows = rng.choice(len(z), 300, replace=False)
+    d = np.hypot(z[rows, None, 0] - z[None, :, 0], z[rows, None, 1] - z[None, :, 1])
+    with np.errstate(divide="ignore"):
+        G = np.where(d > 0, np.log(np.where(d > 0, d, 1.0)), 0.0)
+    want = G @ f
+    assert np.max(np.abs(q[rows] - want)) <= op.eps() * np.abs(f).sum()
+
+
+def test_helmholtz_direct_sum_contract():
+    from scipy.special import j0, y0
+    path, g = golden("helm_disk_n800")
+    op = sbd.CompressedOperator.load(path)
+    z = op.source().points
+    k = op.kernel().k
+    f = g["f"]
+    q = op.apply(f)
+    d = np.hypot(z[:, None, 0] - z[None, :, 0], z[:, None, 1] - z[None, :, 1])
+    mask = d > 0
+    dd = np.where(mask, d, 1.0)
+    G = np.where(mask, 0.25 * y0(k * dd) - 0.25j * j0(k * dd), 0.0)
+    assert np.max(np.abs(q - G @ f)) <= op.eps() * np.abs(f).sum()
+
+
+def test_linearity(ops):
+    op = ops["lap_star_n1500"]
+    rng = np.random.default_rng(107)
+    n = op.n_src()
+    f = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    h = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    a, b = 0.3 + 0.7j, -0.5 + 0.1j
+    qc, qf, qh = op.apply(a * f + b * h), op.apply(f), op.apply(h)
+    scale = max(1.0, np.max(np.abs(qc)))
+    assert np.max(np.abs(qc - (a * qf + b * qh))) <= 1e-12 * scale
+
+
+def test_save_load_roundtrip(ops, tmp_path):
+    path, g = golden("lap_two_clouds")
+    out = tmp_path / "rt.sbdop"
+    ops["lap_two_clouds"].save(str(out))
+    assert open(out, "rb").read() == open(path, "rb").read()  # byte-identical SBDOPv1
+    back = sbd.CompressedOperator.load(str(out))
+    assert rel_l2(back.apply(g["f"]), ops["lap_two_clouds"].apply(g["f"])) <= 1e-14
+
+
+def test_input_size_errors(ops):
+    with pytest.raises(ValueError):
+        ops["lap_disk_n1000"].apply(np.zeros(7))
+    with pytest.raises(ValueError):
+        ops["lap_two_clouds"].apply_adjoint(np.zeros(900))
+
+
+# ------------------------------------------------------------------ NUFFT
+@pytest.mark.parametrize("tol", [1e-4, 1e-8, 1e-12])
+@pytest.mark.parametrize("sign", [-1, 1])
+def test_nufft_plan_vs_reference_kat(tol, sign):
+    kat = np.load(f"{GOLDEN}/nufft_kat.npz")
+    key = f"tol{tol:.0e}_s{'p' if sign > 0 else 'm'}"
+    plan = sbd.NufftPlan(kat["pts"], kat["frq"], sign, sbd.NufftOptions(tol=tol, mode="fast"))
+    assert plan.fast_path()
+    a = plan.apply(kat["c"])
+    t = plan.apply_transpose(kat["v"])
+    assert rel_l2(a, kat["apply_" + key]) <= PARITY
+    assert rel_l2(t, kat["transpose_" + key]) <= PARITY
+    d = sbd.ndft_direct(kat["pts"], kat["frq"], kat["c"], sign)
+    assert np.max(np.abs(a - d)) <= tol * np.abs(kat["c"]).sum()
+
+
+@pytest.mark.parametrize("n", [64, 512, 4096])
+def test_nufft_accuracy_contract(n):
+    # test_nufft.cpp:63-92 / acceptance criterion 8
+    rng = np.random.default_rng(17 + n)
+    for tol in (1e-4, 1e-8, 1e-12):
+        pts = rng.uniform(-0.85, 0.85, (n, 2))
+        frq = rng.uniform(-40, 40, (n + 11, 2))
+        c = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+        for sign in (-1, 1):
+            got = sbd.NufftPlan(pts, frq, sign, sbd.NufftOptions(tol=tol, mode="fast")).apply(c)
+            want = sbd.ndft_direct(pts, frq, c, sign)
+            assert np.max(np.abs(got - want)) <= tol * np.abs(c).sum()
+
+
+def test_nufft_equispaced_matches_fft():
+    # test_nufft.cpp:94-126: output (a,b) <-> FFTW_BACKWARD bin (a,b)
+    n, h = 16, 0.37
+    a, b = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    pts = np.stack([a.ravel() * h, b.ravel() * h], 1)
+    frq = np.stack([2 * np.pi * a.ravel() / (n * h), 2 * np.pi * b.ravel() / (n * h)], 1)
+    rng = np.random.default_rng(29)
+    c = rng.uniform(-1, 1, n * n) + 1j * rng.uniform(-1, 1, n * n)
+    got = sbd.NufftPlan(pts, frq, +1, sbd.NufftOptions(tol=1e-12, mode="fast")).apply(c)
+    want = np.fft.ifft2(c.reshape(n, n)).ravel() * n * n
+    assert np.max(np.abs(got - want)) <= 1e-12 * np.abs(c).sum()
+
+
+def test_nufft_transpose_is_exact_transpose():
+    # test_nufft.cpp:173-191
+    rng = np.random.default_rng(47)
+    pts = rng.uniform(-0.7, 0.7, (300, 2))
+    frq = rng.uniform(-35, 35, (240, 2))
+    c = rng.uniform(-1, 1, 300) + 1j * rng.uniform(-1, 1, 300)
+    v = rng.uniform(-1, 1, 240) + 1j * rng.uniform(-1, 1, 240)
+    p = sbd.NufftPlan(pts, frq, +1, sbd.NufftOptions(tol=1e-7, mode="fast"))
+    lhs = np.sum(p.apply(c) * v)
+    rhs = np.sum(c * p.apply_transpose(v))
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+
+
+def test_nufft_auto_direct_and_guards():
+    rng = np.random.default_rng(37)
+    pts, frq = rng.uniform(-.5, .5, (100, 2)), rng.uniform(-10, 10, (100, 2))
+    c = rng.uniform(-1, 1, 100) + 0j
+    p = sbd.NufftPlan(pts, frq, +1)
+    assert not p.fast_path()
+    assert np.max(np.abs(p.apply(c) - sbd.ndft_direct(pts, frq, c, +1))) <= 1e-13 * np.abs(c).sum()
+    with pytest.raises(sbd.SbdError):
+        sbd.NufftPlan(pts, rng.uniform(-2500, 2500, (100, 2)), +1,
+                      sbd.NufftOptions(mode="fast", max_grid_bytes=1024))
+    with pytest.raises(ValueError):
+        p.apply(np.zeros(3))
