@@ -135,6 +135,10 @@ uint64_t sbd_kernel_launch_count(void);
  * for width w and shape beta, relative to the window peak I0(beta). */
 double sbd_window_fit_error(int w, double beta);
 
+/* Diagnostics: the host Bessel functions of the offline assembly.
+ * which: 0 J0, 1 J1, 2 Y0, 3 Y1. NaN on a domain error. */
+double sbd_bessel(int which, double x);
+
 #ifdef __cplusplus
 }
 #endif

@@ -75,6 +75,7 @@ _sig("sbd_nufft_info", _int, _vp, ctypes.POINTER(_int), ctypes.POINTER(_int),
 _sig("sbd_nufft_destroy", _int, _vp)
 _sig("sbd_ndft_direct", _int, _dp, _u64, _dp, _u64, _dp, _int, _int, _dp)
 _sig("sbd_window_fit_error", ctypes.c_double, _int, ctypes.c_double)
+_sig("sbd_bessel", ctypes.c_double, _int, ctypes.c_double)
 _sig("sbd_choose_parameters", _int, _u64, ctypes.c_double, ctypes.c_double, _dp,
      ctypes.POINTER(_int))
 
@@ -86,7 +87,7 @@ EXPORTED = [
     "sbd_op_apply_adjoint_device", "sbd_op_set_profiling", "sbd_op_stage_times",
     "sbd_nufft_create", "sbd_nufft_apply", "sbd_nufft_apply_transpose", "sbd_nufft_info",
     "sbd_nufft_destroy", "sbd_ndft_direct", "sbd_choose_parameters", "sbd_kernel_launch_count",
-    "sbd_window_fit_error",
+    "sbd_window_fit_error", "sbd_bessel",
 ]
 
 

@@ -21,8 +21,8 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["kernels.cu"]
-CPP_SOURCES = ["window.cpp", "plan.cpp", "op.cpp", "assemble.cpp"]
+CU_SOURCES = ["kernels.cu", "assemble_kernels.cu"]
+CPP_SOURCES = ["window.cpp", "plan.cpp", "op.cpp", "assemble.cpp", "bessel_host.cpp", "sbd_fit.cpp"]
 
 
 def _run(cmd, verbose):
@@ -60,11 +60,11 @@ def build(verbose: bool = False, force: bool = False) -> str:
         o = os.path.join(OBJ, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            _run(["g++", "-std=c++17", "-O2", "-fPIC", "-Wall", "-Wno-unused-function",
+            _run(["g++", "-std=gnu++17", "-O2", "-fPIC", "-fopenmp", "-Wall", "-Wno-unused-function",
                   f"-I{CUDA}/include", "-c", s, "-o", o], verbose)
     if force or _stale(LIB, objs):
         tmp = LIB + ".tmp"
-        _run(["g++", "-shared", "-o", tmp, *objs, f"-L{CUDA}/lib64", "-lcufft", "-lcudart_static",
+        _run(["g++", "-shared", "-o", tmp, *objs, f"-L{CUDA}/lib64", "-lcufft", "-lcusolver", "-lcudart_static", "-fopenmp",
               "-ldl", "-lrt", "-lpthread", f"-Wl,-rpath,{CUDA}/lib64"], verbose)
         shutil.move(tmp, LIB)
     return LIB

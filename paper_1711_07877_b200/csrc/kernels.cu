@@ -11,32 +11,15 @@
 //   adjoint q += D^H u              point_cloud.cpp:125-132 -> k_spmv_adjoint
 #include <cub/cub.cuh>
 
+#include "device_common.cuh"
 #include "sbd_internal.h"
 
 namespace sbdgpu {
 
 namespace {
 
+using namespace dev;
 constexpr double kPi = 3.14159265358979323846;
-
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-
-// kb_window_hat (nufft.cpp:34-45), arguments formed without FMA contraction so
-// they round exactly like the reference's host code.
-__device__ double kb_hat(double beta, double w) {
-    const double s2 = __dsub_rn(__dmul_rn(beta, beta), __dmul_rn(w, w));
-    if (s2 > 1e-12) {
-        const double s = sqrt(s2);
-        return __ddiv_rn(2.0 * sinh(s), s);
-    }
-    if (s2 < -1e-12) {
-        const double s = sqrt(-s2);
-        return __ddiv_rn(2.0 * sin(s), s);
-    }
-    return __dmul_rn(2.0, __dadd_rn(1.0, __ddiv_rn(s2, 6.0)));
-}
 
 // Per-point plan arrays (nufft.cpp:163-177).
 __global__ void k_plan_points(const double2* __restrict__ pts, uint64_t n, Axis ax, Axis ay,
@@ -97,36 +80,6 @@ __global__ void k_gather(const T* __restrict__ src, const uint32_t* __restrict__
                          T* __restrict__ dst, uint64_t n) {
     const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (k < n) dst[k] = src[perm[k]];
-}
-
-// Window taps at sub-cell offset u in [0,1): w[i] = phi((u - w/2 + i)/(w/2)).
-template <int W>
-__device__ __forceinline__ void kb_taps(double u, const WindowPoly& P, double (&wt)[W]) {
-    const double v = 2.0 * u - 1.0;
-    const double v2 = v * v;
-#pragma unroll
-    for (int i = 0; i < W / 2; ++i) {
-        double e = P.e[i][kHorner - 1], o = P.o[i][kHorner - 1];
-#pragma unroll
-        for (int h = kHorner - 2; h >= 0; --h) {
-            e = fma(e, v2, P.e[i][h]);
-            o = fma(o, v2, P.o[i][h]);
-        }
-        wt[i] = fma(v, o, e);
-        wt[W - 1 - i] = fma(-v, o, e);
-    }
-    if (W & 1) {
-        constexpr int m = W / 2;
-        double e = P.e[m][kHorner - 1];
-#pragma unroll
-        for (int h = kHorner - 2; h >= 0; --h) e = fma(e, v2, P.e[m][h]);
-        wt[m] = e;
-    }
-}
-
-__device__ __forceinline__ int wrap_base(int i, int n) {
-    int r = i % n;
-    return r < 0 ? r + n : r;
 }
 
 // Spread (nufft.cpp:229-250): one thread per point, fp64 reductions into the

@@ -16,6 +16,7 @@
 #include <mutex>
 
 #include "../../include/sbd_b200.h"
+#include "bessel_host.h"
 #include "opdata.h"
 #include "sbd_internal.h"
 
@@ -291,6 +292,19 @@ extern "C" {
 const char* sbd_last_error(void) { return g_err.c_str(); }
 const char* sbd_version(void) { return "sbd_b200 0.1.0 (sm_100a)"; }
 uint64_t sbd_kernel_launch_count(void) { return g_launches.load(); }
+
+double sbd_bessel(int which, double x) {
+    try {
+        switch (which) {
+            case 0: return bessel_j0(x);
+            case 1: return bessel_j1(x);
+            case 2: return bessel_y0(x);
+            case 3: return bessel_y1(x);
+        }
+    } catch (const std::exception&) {
+    }
+    return std::nan("");
+}
 
 double sbd_window_fit_error(int w, double beta) {
     double err = -1.0;

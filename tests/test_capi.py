@@ -76,3 +76,26 @@ def test_window_polynomial_accuracy(w):
     # reference can select (nufft.cpp:47-52, beta = 2.3562 w, :129).
     err = _capi.lib.sbd_window_fit_error(w, 2.3562 * w)
     assert 0 <= err <= 2e-15, err
+
+
+def test_host_bessel_vs_reference(reflib):
+    # The offline assembly's J0/J1/Y0/Y1 against the reference's (bessel.cpp),
+    # across the series / float128 / Hankel seams.
+    xs = np.concatenate([np.linspace(1e-3, 30, 997), np.geomspace(30, 2e4, 300)])
+    for which, name in enumerate(["j0", "j1", "y0", "y1"]):
+        got = np.array([_capi.lib.sbd_bessel(which, x) for x in xs])
+        want = np.array([reflib.bessel(name, x) for x in xs])
+        scale = np.maximum(np.abs(want), 1.0 / np.sqrt(xs))  # absolute near zeros
+        assert np.max(np.abs(got - want) / scale) <= 5e-14, name
+
+
+def test_host_bessel_golden_mpmath():
+    # 50-digit values (mpmath) at a few arguments, independent of the reference.
+    import mpmath as mp
+    mp.mp.dps = 30
+    for x in (0.1, 2.5, 11.9, 12.1, 15.9, 16.1, 100.0, 1234.5):
+        for which, f in enumerate([lambda t: mp.besselj(0, t), lambda t: mp.besselj(1, t),
+                                   lambda t: mp.bessely(0, t), lambda t: mp.bessely(1, t)]):
+            want = float(f(x))
+            got = _capi.lib.sbd_bessel(which, x)
+            assert abs(got - want) <= 2e-15 * max(abs(want), 1.0 / np.sqrt(x)), (which, x)
