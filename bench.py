@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""SBD apply throughput on B200 (BASELINE.json metric: "SBD apply points/s").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--config 4|3|1|2s]
+
+Workload (default, BASELINE.json configs[3] = "config 4"): Laplace kernel,
+N = 1e7 points i.i.d. uniform in a disk of diameter 1, real f ~ N(0,1),
+eps = 1e-6, delta_min = 2.74/sqrt(N); synthetic, seeded. It is the largest
+BASELINE config that fits one GPU (configs[1] as written needs a ~0.84 TB FFT
+grid).
+
+A step = one CompressedOperator::apply (conv_operator.cpp:301-309): both
+type-III NUFFTs (spread, cuFFT, deconvolve+interpolate), the omega-hat
+weighting and the CSR close correction, on device-resident f -> q.
+`value` = N * n_gpus * K / (max-over-ranks device time of K steps) [points/s];
+`e2e` = the same through the host-buffer C-ABI call sbd_op_apply (pinned host
+f in, host q out, copies inside the timed region).
+
+--impl reference times the reference's own CPU apply (oracle/_ref, the
+unmodified reference library compiled here) on the box's host cores on a
+bounded sample of the same workload (see cpu_baseline.sample).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from tests.clouds import disk_cloud, star_curve_cloud  # noqa: E402
+
+METRIC = "SBD apply points/s (N=1e6–1e7, ε=1e-6) at 1/2/4/8 B200; % HBM roofline"
+SEED = 20261019
+
+
+# ------------------------------------------------------------------ workloads
+def workload(name: str, scale: float = 1.0):
+    """Returns (description, points, kernel dict, eps, a_override_fn, f_complex)."""
+    rng = np.random.default_rng(SEED)
+    if name == "4":
+        n = int(1e7 * scale)
+        z = disk_cloud(n, rng)
+        return dict(desc=f"config4: Laplace, N={n} uniform disk d=1, eps=1e-6, delta_min=2.74/sqrt(N)",
+                    z=z, kind=0, kappa=0.0, eps=1e-6, dmin=2.74 / np.sqrt(n), f_complex=False)
+    if name == "3":
+        n = int(1e6 * scale)
+        z = disk_cloud(n, rng)
+        return dict(desc=f"config3: Helmholtz k*dmax=2pi*100, N={n} uniform disk d=1, eps=1e-6, "
+                         "delta_min=2.74/sqrt(N)", z=z, kind=1, kappa=2 * np.pi * 100, eps=1e-6,
+                    dmin=2.74 / np.sqrt(n), f_complex=True)
+    if name == "1":
+        n = int(1e4 * scale)
+        z = disk_cloud(n, rng)
+        return dict(desc=f"config1: Laplace, N={n} uniform disk d=1, eps=1e-6, delta_min=2.74/sqrt(N)",
+                    z=z, kind=0, kappa=0.0, eps=1e-6, dmin=2.74 / np.sqrt(n), f_complex=False)
+    if name == "2s":
+        n = int(1e6 * scale)
+        z = star_curve_cloud(n, rng)
+        return dict(desc=f"config2*: Laplace, N={n} star curve (jitter 0.1), eps=1e-6, reference a-rule",
+                    z=z, kind=0, kappa=0.0, eps=1e-6, dmin=None, f_complex=False)
+    raise SystemExit(f"unknown config {name}")
+
+
+def rhs(w, n, rng):
+    f = rng.standard_normal(n).astype(np.complex128)
+    if w["f_complex"]:
+        f += 1j * rng.standard_normal(n)
+    return f
+
+
+# ------------------------------------------------------------------ helpers
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = f"/tmp/sbd_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def stage_bytes(info, name):
+    """Algorithmic bytes per launch, SURVEY.md section 8(d) byte model."""
+    N, Nt, Nx, nnz = info["n_src"], info["n_tgt"], info["n_xi"], info["nnz"]
+    grid_in = 16 * info["n1_in"] * info["n2_in"]
+    grid_out = 16 * info["n1_out"] * info["n2_out"]
+    band = lambda n1, n2: 16 * (2 * (n1 // 4) + 1) * (2 * (n2 // 4) + 1)  # noqa: E731
+    return {
+        "spread_src": 16 * N + 16 * N + grid_in,                                   # B1
+        "interp_xi": band(info["n1_in"], info["n2_in"]) + 3 * 16 * Nx,             # B2
+        "spread_xi": 2 * 16 * Nx + grid_out,                                       # B3
+        "interp_tgt": band(info["n1_out"], info["n2_out"]) + 2 * 16 * Nt,          # B4
+        "spmv": 8 * (Nt + 1) + 20 * nnz + 16 * N + 32 * Nt,                        # B5
+    }.get(name)
+
+
+def ncu_traffic(stage):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        return json.load(fh).get(stage)
+
+
+# ------------------------------------------------------------------ reference arm
+def reference_sample(w, sample_n):
+    """Assemble the same workload at sample_n points with the reference's own
+    assemble (oracle/_ref) and return (ref lib, operator path, f)."""
+    from oracle.oracle import REF_SO, Oracle, RefLib
+    rng = np.random.default_rng(SEED + 1)
+    if w["desc"].startswith("config2"):
+        z = star_curve_cloud(sample_n, rng)
+    else:
+        z = disk_cloud(sample_n, rng)
+    path = f"/tmp/sbd_ref_sample_{os.getpid()}.sbdop"
+    kind = "reference" if os.path.exists(REF_SO) else "port"
+    if kind == "reference":
+        lib = RefLib()
+        d = lib.diameter(z)
+        a = (2.74 / np.sqrt(sample_n)) / d if w["dmin"] is not None else 0.0
+        lib.assemble_save(path, z, kind=w["kind"], k=w["kappa"] / d, eps=w["eps"], a_override=a)
+        op = lib.load(path)
+        apply = lambda f: op.apply(f, sample_n)  # noqa: E731
+    else:
+        import paper_1711_07877_b200 as sbd  # only to build the operator file for the port
+        d = sbd.cloud_diameter(z)
+        kern = sbd.kernel_helmholtz(w["kappa"] / d) if w["kind"] else sbd.kernel_laplace()
+        a = (2.74 / np.sqrt(sample_n)) / d if w["dmin"] is not None else 0.0
+        o = sbd.CompressedOperator.assemble(kern, z, opts=sbd.AssembleOptions(eps=w["eps"],
+                                                                               a_override=a))
+        o.save(path)
+        op = Oracle().op(path)
+        apply = op.apply
+    f = rhs(w, sample_n, np.random.default_rng(SEED + 2))
+    return kind, apply, f, path
+
+
+def time_reference(apply, f, threads, reps):
+    """`threads` concurrent applies (CompressedOperator::apply is const and
+    thread-safe, conv_operator.hpp:33-36), `reps` rounds; returns seconds/round."""
+    def work():
+        for _ in range(reps):
+            apply(f)
+    ts = [threading.Thread(target=work) for _ in range(threads)]
+    t0 = time.perf_counter()
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return (time.perf_counter() - t0) / reps
+
+
+def run_reference(args, w):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sample_n = args.sample_n
+    kind, apply, f, path = reference_sample(w, sample_n)
+    cores = os.cpu_count() or 1
+    threads = max(1, min(cores, args.ref_threads or cores))
+    for _ in range(args.warmup):
+        time_reference(apply, f, threads, 1)
+    per_round = time_reference(apply, f, threads, args.steps)
+    os.unlink(path)
+    value = sample_n * threads / per_round
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": per_round * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
+        "config": {"workload": w["desc"], "parallelism": f"host threads x{threads}"},
+        "cpu_baseline": {
+            "value": value, "unit": "points/s", "cores": threads, "kind": kind,
+            "sample": (f"same distribution/eps/delta_min rule at N={sample_n} (reference assemble + "
+                       f"{threads} concurrent single-threaded CompressedOperator::apply per step)")},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ B200 arm
+def run_b200(args, w):
+    import torch
+    import paper_1711_07877_b200 as sbd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    z = w["z"]
+    n = len(z)
+    t0 = time.perf_counter()
+    dmax = sbd.cloud_diameter(z)
+    kern = sbd.kernel_helmholtz(w["kappa"] / dmax) if w["kind"] else sbd.kernel_laplace()
+    a = w["dmin"] / dmax if w["dmin"] else 0.0
+    opts = sbd.AssembleOptions(eps=w["eps"], a_override=a, max_grid_bytes=96 << 30, device=local)
+    op = sbd.CompressedOperator.assemble(kern, z, opts=opts)
+    t_offline = time.perf_counter() - t0
+    info = op.info()
+
+    rng = np.random.default_rng(SEED + 3)
+    f = rhs(w, n, rng)
+    f_dev = torch.from_numpy(f.view(np.float64).copy()).cuda()
+    q_dev = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    def step():
+        op.apply_device(f_dev.data_ptr(), q_dev.data_ptr(), 1, sh)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)  # let the sampler start before the timed region
+    op.set_profiling(True)
+    launches0 = sbd.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = sbd.launch_count() - launches0
+    clk = clocks.stop()
+    ms_total = e0.elapsed_time(e1)
+    stages = op.stage_times()
+    op.set_profiling(False)
+    if dist:
+        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = n * world / (ms_step / 1e3)
+
+    # per-stage averages over the timed region (CUDA events on the launch stream)
+    agg = {}
+    for name, ms in stages:
+        agg.setdefault(name, []).append(ms)
+    avg = {k: sum(v) / len(v) for k, v in agg.items()}
+    cand = {k: v for k, v in avg.items() if stage_bytes(info, k) is not None}
+    dom = max(cand, key=cand.get)
+    peak, peak_src = measured_peak()
+    ach = stage_bytes(info, dom) / (avg[dom] / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": ncu_traffic(dom), "peak_source": peak_src,
+                "algorithmic_bytes": stage_bytes(info, dom), "avg_ms": avg[dom],
+                "stages_ms": {k: round(v, 4) for k, v in avg.items()},
+                "stages_frac": {k: round(stage_bytes(info, k) / (avg[k] / 1e3) / 1e9 / peak, 4)
+                                for k in cand}}
+
+    # end to end through the host-buffer C-ABI call, pinned host memory
+    fh = torch.from_numpy(f.view(np.float64).copy()).pin_memory()
+    qh = torch.empty(2 * n, dtype=torch.float64).pin_memory()
+    op.apply_host(fh.data_ptr(), qh.data_ptr(), 1)
+    if dist:
+        dist.barrier()
+    t1 = time.perf_counter()
+    for _ in range(args.steps):
+        op.apply_host(fh.data_ptr(), qh.data_ptr(), 1)
+    e2e_s = (time.perf_counter() - t1) / args.steps
+    if dist:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        kind, apply, fs, path = reference_sample(w, args.sample_n)
+        per = min(time_reference(apply, fs, 1, 1) for _ in range(2))
+        os.unlink(path)
+        cpu = {"value": args.sample_n / per, "unit": "points/s", "cores": 1, "kind": kind,
+               "sample": (f"same distribution/eps/delta_min rule at N={args.sample_n}, "
+                          "single-threaded CompressedOperator::apply, best of 2")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded clouds/RHS of the BASELINE.json shape)",
+            "config": {"workload": w["desc"], "N": n, "n_xi": info["n_xi"], "nnz": info["nnz"],
+                       "P": info["P"], "w": info["w"], "grid": [info["n1_in"], info["n2_in"]],
+                       "nufft_tol": info["nufft_tol"],
+                       "l2": "inputs larger than L2 (grid + xi + D >> 126 MB)",
+                       "parallelism": "single" if world == 1 else f"replicas x{world}",
+                       "offline_s": round(t_offline, 2)},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": n * world / e2e_s, "unit": "points/s",
+                    "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="4")
+    ap.add_argument("--scale", type=float, default=1.0, help="multiply the config's N (testing)")
+    ap.add_argument("--sample-n", type=int, default=50000, help="reference CPU sample size")
+    ap.add_argument("--ref-threads", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    w = workload(args.config, args.scale)
+    if args.impl == "reference":
+        run_reference(args, w)
+    else:
+        run_b200(args, w)
+
+
+if __name__ == "__main__":
+    main()

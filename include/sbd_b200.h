@@ -99,17 +99,23 @@ int sbd_op_get(const sbd_op* op, int which, void* dst, uint64_t* count);
  * q: nrhs x n_tgt, interleaved complex). Host buffers; copies are inside. */
 int sbd_op_apply(sbd_op* op, const double* f, double* q, int nrhs);
 int sbd_op_apply_adjoint(sbd_op* op, const double* u, double* q, int nrhs);
-/* Same on device buffers, enqueued on `stream` (cudaStream_t; NULL = the
- * operator's own stream). Returns without synchronising. */
+/* Same on device buffers, enqueued on `stream` (a cudaStream_t; NULL is the
+ * legacy default stream, as everywhere in CUDA). Returns without
+ * synchronising. */
 int sbd_op_apply_device(sbd_op* op, const double* d_f, double* d_q, int nrhs, void* stream);
 int sbd_op_apply_adjoint_device(sbd_op* op, const double* d_u, double* d_q, int nrhs,
                                 void* stream);
 
-/* Per-stage CUDA-event timing of the most recent apply (profiling must be
- * enabled first). names: "spread_src", "fft_in", "interp_xi", "spread_xi",
- * "fft_out", "interp_tgt", "spmv", ... ms[i] in milliseconds. Returns count. */
+/* Per-stage CUDA-event timing of every apply since profiling was enabled (or
+ * since the last reset). names: "spread_src", "fft_in", "interp_xi",
+ * "spread_xi", "fft_out", "interp_tgt", "spmv", ... ms[i] in milliseconds.
+ * Returns the number of records. */
 int sbd_op_set_profiling(sbd_op* op, int enable);
 int sbd_op_stage_times(sbd_op* op, double* ms, const char** names, int cap);
+int sbd_op_stage_times_reset(sbd_op* op);
+
+/* Exact diameter of a point cloud (make_cloud, point_cloud.cpp:13-65). */
+double sbd_cloud_diameter(const double* xy, uint64_t n);
 
 /* ---- standalone type-III NUFFT (NufftPlan) ---- */
 /* mode: 0 Auto, 1 Direct, 2 Fast (nufft.hpp:18-24). */

@@ -7,7 +7,7 @@ behind the C ABI in include/sbd_b200.h. See DESIGN.md.
 """
 from .sbd import (AssembleOptions, CompressedOperator, FrequencyQuadrature, KernelSpec,  # noqa: F401
                   MINUS, NufftOptions, NufftPlan, PLUS, PointCloud, SparsePairMatrix,
-                  choose_parameters, kernel_helmholtz, kernel_laplace, make_cloud, ndft_direct)
+                  choose_parameters, cloud_diameter, kernel_helmholtz, kernel_laplace, make_cloud, ndft_direct)
 from ._capi import (CudaError, DomainError, SbdConvergenceError, SbdError,  # noqa: F401
                     launch_count)
 

@@ -66,6 +66,8 @@ _sig("sbd_op_apply_device", _int, _vp, _vp, _vp, _int, _vp)
 _sig("sbd_op_apply_adjoint_device", _int, _vp, _vp, _vp, _int, _vp)
 _sig("sbd_op_set_profiling", _int, _vp, _int)
 _sig("sbd_op_stage_times", _int, _vp, _dp, ctypes.POINTER(ctypes.c_char_p), _int)
+_sig("sbd_op_stage_times_reset", _int, _vp)
+_sig("sbd_cloud_diameter", ctypes.c_double, _dp, _u64)
 _sig("sbd_nufft_create", _int, _dp, _u64, _dp, _u64, _int, ctypes.c_double, _int, _u64, _u64,
      _int, ctypes.POINTER(_vp))
 _sig("sbd_nufft_apply", _int, _vp, _dp, _dp)
@@ -85,6 +87,7 @@ EXPORTED = [
     "sbd_op_load", "sbd_op_save", "sbd_op_destroy", "sbd_op_info", "sbd_op_get",
     "sbd_op_apply", "sbd_op_apply_adjoint", "sbd_op_apply_device",
     "sbd_op_apply_adjoint_device", "sbd_op_set_profiling", "sbd_op_stage_times",
+    "sbd_op_stage_times_reset", "sbd_cloud_diameter",
     "sbd_nufft_create", "sbd_nufft_apply", "sbd_nufft_apply_transpose", "sbd_nufft_info",
     "sbd_nufft_destroy", "sbd_ndft_direct", "sbd_choose_parameters", "sbd_kernel_launch_count",
     "sbd_window_fit_error", "sbd_bessel",

@@ -41,8 +41,10 @@ struct P2 {
 
 double cross(P2 o, P2 a, P2 b) { return (a.x - o.x) * (b.y - o.y) - (a.y - o.y) * (b.x - o.x); }
 
+} // namespace
+
 // Exact diameter: monotone-chain hull, then the farthest antipodal pair by
-// rotating calipers.
+// rotating calipers (point_cloud.cpp:13-57).
 double cloud_diameter(const double* xy, uint64_t n) {
     if (n < 2) return 0.0;
     std::vector<P2> p(n);
@@ -77,6 +79,8 @@ double cloud_diameter(const double* xy, uint64_t n) {
     }
     return best;
 }
+
+namespace {
 
 // conv_operator.cpp:59-77
 double oscillation_a_cap(double kappa, double eps) {

@@ -35,4 +35,7 @@ struct CloseMatrixOutput {
 
 void build_close_matrix_gpu(const CloseMatrixInput& in, CloseMatrixOutput& out);
 
+// Exact cloud diameter (assemble.cpp).
+double cloud_diameter(const double* xy, uint64_t n);
+
 } // namespace sbdgpu

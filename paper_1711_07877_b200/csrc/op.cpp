@@ -16,6 +16,7 @@
 #include <mutex>
 
 #include "../../include/sbd_b200.h"
+#include "assemble_gpu.h"
 #include "bessel_host.h"
 #include "opdata.h"
 #include "sbd_internal.h"
@@ -432,8 +433,7 @@ int sbd_op_apply_device(sbd_op* op, const double* d_f, double* d_q, int nrhs, vo
         if (!op || !d_f || !d_q || nrhs < 1) throw Error(SBD_ERR_INVALID_ARGUMENT, "apply: bad argument");
         std::lock_guard<std::mutex> lk(op->mu);
         DeviceGuard g(op->device);
-        cudaStream_t st = stream ? (cudaStream_t)stream : op->stream;
-        op->tm.reset();
+        cudaStream_t st = (cudaStream_t)stream;
         op->tm.stream = st;
         const auto* f = reinterpret_cast<const double2*>(d_f);
         auto* q = reinterpret_cast<double2*>(d_q);
@@ -449,8 +449,7 @@ int sbd_op_apply_adjoint_device(sbd_op* op, const double* d_u, double* d_q, int 
         if (!op || !d_u || !d_q || nrhs < 1) throw Error(SBD_ERR_INVALID_ARGUMENT, "apply_adjoint: bad argument");
         std::lock_guard<std::mutex> lk(op->mu);
         DeviceGuard g(op->device);
-        cudaStream_t st = stream ? (cudaStream_t)stream : op->stream;
-        op->tm.reset();
+        cudaStream_t st = (cudaStream_t)stream;
         op->tm.stream = st;
         const auto* u = reinterpret_cast<const double2*>(d_u);
         auto* q = reinterpret_cast<double2*>(d_q);
@@ -472,8 +471,8 @@ static int host_apply(sbd_op* op, const double* in, double* out, int nrhs, bool 
             if (op->hq.n < nout * nrhs) op->hq.alloc(nout * nrhs);
             ck(cudaMemcpyAsync(op->hf.p, in, nin * nrhs * 16, cudaMemcpyHostToDevice, op->stream), "H2D f");
         }
-        const int rc = adjoint ? sbd_op_apply_adjoint_device(op, (double*)op->hf.p, (double*)op->hq.p, nrhs, nullptr)
-                               : sbd_op_apply_device(op, (double*)op->hf.p, (double*)op->hq.p, nrhs, nullptr);
+        const int rc = adjoint ? sbd_op_apply_adjoint_device(op, (double*)op->hf.p, (double*)op->hq.p, nrhs, op->stream)
+                               : sbd_op_apply_device(op, (double*)op->hf.p, (double*)op->hq.p, nrhs, op->stream);
         if (rc) throw Error(rc, g_err);
         std::lock_guard<std::mutex> lk(op->mu);
         DeviceGuard g(op->device);
@@ -504,6 +503,22 @@ int sbd_op_stage_times(sbd_op* op, double* ms, const char** names, int cap) {
     std::lock_guard<std::mutex> lk(op->mu);
     DeviceGuard g(op->device);
     return op->tm.read(ms, names, cap);
+}
+
+int sbd_op_stage_times_reset(sbd_op* op) {
+    return guarded([&] {
+        if (!op) throw Error(SBD_ERR_INVALID_ARGUMENT, "null operator");
+        std::lock_guard<std::mutex> lk(op->mu);
+        op->tm.reset();
+    });
+}
+
+double sbd_cloud_diameter(const double* xy, uint64_t n) {
+    try {
+        return cloud_diameter(xy, n);
+    } catch (const std::exception&) {
+        return std::nan("");
+    }
 }
 
 int sbd_nufft_create(const double* points, uint64_t np, const double* freqs, uint64_t nf, int sign,

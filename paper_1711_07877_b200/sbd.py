@@ -85,10 +85,16 @@ class PointCloud:
         return len(self.points)
 
 
+def cloud_diameter(points) -> float:
+    """Exact diameter (convex hull + rotating calipers, point_cloud.cpp:39-57)."""
+    p = _xy(points)
+    return float(lib.sbd_cloud_diameter(_ptr(p), len(p)))
+
+
 def make_cloud(points) -> PointCloud:
-    """point_cloud.hpp:20. The diameter is computed by the native assembler; it
-    is not needed on the Python side."""
-    return PointCloud(_xy(points))
+    """point_cloud.hpp:20."""
+    p = _xy(points)
+    return PointCloud(p, cloud_diameter(p))
 
 
 @dataclasses.dataclass
@@ -266,9 +272,14 @@ class CompressedOperator:
 
     def apply_device(self, f_ptr: int, q_ptr: int, nrhs: int = 1, stream: int = 0) -> None:
         """Device-buffer apply (interleaved complex128, nrhs x n). Enqueued on
-        `stream` (a cudaStream_t as int; 0 = the operator's own stream)."""
+        `stream` (a cudaStream_t as int; 0 = the legacy default stream)."""
         check(lib.sbd_op_apply_device(self._h, ctypes.c_void_p(f_ptr), ctypes.c_void_p(q_ptr),
                                       int(nrhs), ctypes.c_void_p(stream or None)))
+
+    def apply_host(self, f_ptr: int, q_ptr: int, nrhs: int = 1) -> None:
+        """sbd_op_apply on raw host pointers (e.g. pinned torch buffers)."""
+        check(lib.sbd_op_apply(self._h, ctypes.cast(f_ptr, _dp), ctypes.cast(q_ptr, _dp),
+                               int(nrhs)))
 
     def apply_adjoint_device(self, u_ptr: int, q_ptr: int, nrhs: int = 1, stream: int = 0) -> None:
         check(lib.sbd_op_apply_adjoint_device(self._h, ctypes.c_void_p(u_ptr),
@@ -278,12 +289,16 @@ class CompressedOperator:
     def set_profiling(self, on: bool) -> None:
         check(lib.sbd_op_set_profiling(self._h, 1 if on else 0))
 
-    def stage_times(self) -> list:
-        cap = 64
+    def stage_times(self, reset: bool = True) -> list:
+        """(stage, ms) for every profiled stage launch since the last reset."""
+        cap = 4096
         ms = (ctypes.c_double * cap)()
         names = (ctypes.c_char_p * cap)()
         n = lib.sbd_op_stage_times(self._h, ms, names, cap)
-        return [(names[i].decode(), ms[i]) for i in range(min(n, cap))]
+        out = [(names[i].decode(), ms[i]) for i in range(min(n, cap))]
+        if reset:
+            check(lib.sbd_op_stage_times_reset(self._h))
+        return out
 
 
 # --------------------------------------------------------------- NUFFT
