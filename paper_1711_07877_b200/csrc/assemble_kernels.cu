@@ -361,10 +361,7 @@ void build_close_matrix_gpu(const CloseMatrixInput& in, CloseMatrixOutput& out) 
         ck(cudaMemsetAsync(grid.p, 0, far.cells() * 16, st), "grid zero");
         launch_spread(far.w, far.win, gg, in.n_xi, far.perm_t.n ? far.perm_t.p : nullptr, w.p, far.t.p,
                       far.pre.p, nullptr, nullptr, nullptr, grid.p, 0, st);
-        ckfft(cufftSetStream(far.fft, st), "cufftSetStream");
-        ckfft(cufftExecZ2Z(far.fft, reinterpret_cast<cufftDoubleComplex*>(grid.p),
-                           reinterpret_cast<cufftDoubleComplex*>(grid.p), CUFFT_INVERSE),
-              "cufftExecZ2Z");
+        far.full_transform(grid.p, st);
         const double cxy = (2.0 * M_PI / (far.ax.n * far.ax.gamma)) * (2.0 * M_PI / (far.ay.n * far.ay.gamma));
         dispatch_w<CloseRun>(far.w, far.win, gg, far.ax, far.ay, cxy, far.dx.p, far.dy.p, grid.p, tgt.p,
                              src.p, row.p, cols.p, nnz, (int)in.single, diag, (int)in.laplace, vals.p,

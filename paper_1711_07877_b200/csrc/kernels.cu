@@ -11,6 +11,8 @@
 //   adjoint q += D^H u              point_cloud.cpp:125-132 -> k_spmv_adjoint
 #include <cub/cub.cuh>
 
+#include <climits>
+
 #include "device_common.cuh"
 #include "sbd_internal.h"
 
@@ -68,6 +70,52 @@ __global__ void k_bin_keys(const double2* __restrict__ pos, uint64_t n, GridGeom
     iy = ((iy % g.n2) + g.n2) % g.n2;
     const uint32_t ntx = (uint32_t)((g.n2 + tile - 1) / tile);
     keys[k] = (uint32_t)(ix / tile) * ntx + (uint32_t)(iy / tile);
+}
+
+__global__ void k_stencil_extent(const double2* __restrict__ pos, uint64_t n, double half,
+                                 int* __restrict__ ext) {
+    int a = INT_MAX, b = INT_MIN, c = INT_MAX, d = INT_MIN;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const double2 p = pos[k];
+        const int ix = (int)ceil(p.x - half), iy = (int)ceil(p.y - half);
+        a = min(a, ix);
+        b = max(b, ix);
+        c = min(c, iy);
+        d = max(d, iy);
+    }
+    for (int o = 16; o; o >>= 1) {
+        a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+        b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+        c = min(c, __shfl_xor_sync(0xffffffffu, c, o));
+        d = max(d, __shfl_xor_sync(0xffffffffu, d, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(ext + 0, a);
+        atomicMax(ext + 1, b);
+        atomicMin(ext + 2, c);
+        atomicMax(ext + 3, d);
+    }
+}
+
+__global__ void k_tile_keys(const double2* __restrict__ pos, uint64_t n, double half, TileGeom tg,
+                            uint32_t* __restrict__ keys) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double2 p = pos[k];
+    const int bx = ((int)ceil(p.x - half) - tg.rlo) / kTileR;
+    const int by = ((int)ceil(p.y - half) - tg.clo) / kTileC;
+    keys[k] = (uint32_t)bx * (uint32_t)tg.nby + (uint32_t)by;
+}
+
+// start[b] = first sorted position with key >= b, for b in [0, nbins]
+__global__ void k_bin_bounds(const uint32_t* __restrict__ key, uint64_t n, uint32_t nbins,
+                             uint32_t* __restrict__ start) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i > n) return;
+    const int64_t prev = i > 0 ? (int64_t)key[i - 1] : -1;
+    const int64_t cur = i < n ? (int64_t)key[i] : (int64_t)nbins;
+    for (int64_t b = prev + 1; b <= cur; ++b) start[b] = (uint32_t)i;
 }
 
 __global__ void k_iota(uint32_t* v, uint64_t n) {
@@ -130,6 +178,99 @@ __global__ void __launch_bounds__(256) k_spread(WindowPoly P, GridGeom g, uint64
             if (my >= g.n2) my -= g.n2;
             atomicAdd(row + 2 * my, bxr * wy[j]);
             atomicAdd(row + 2 * my + 1, bxi * wy[j]);
+        }
+    }
+}
+
+// Tile-owned spread (nufft.cpp:229-250 restated output-stationary). One warp
+// owns a kTileR x kTileC block of grid cells: lane = column, the kTileR rows of
+// that column live in registers. The warp scans the points binned in its own
+// tile and the three tiles above/left of it (a stencil starting there can
+// reach into this tile), stages the intersecting ones in its shared-memory
+// slice with their precomputed b*wx and wy taps (one polynomial window
+// evaluation per staged point, lane = point), then accumulates
+// acc[r] += (b wx)[row r] * wy[lane] point by point. Every cell of the tile is
+// written exactly once: no atomics and no zero-fill of the grid.
+template <int W>
+__global__ void __launch_bounds__(128) k_spread_tiles(WindowPoly P, GridGeom g, TileGeom tg,
+                                                      const uint32_t* __restrict__ bin_start,
+                                                      const uint32_t* __restrict__ perm,
+                                                      const double2* __restrict__ in,
+                                                      const double2* __restrict__ pos,
+                                                      const double2* __restrict__ phase,
+                                                      double2* __restrict__ grid) {
+    extern __shared__ double smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // per warp: bwx[32*W] (double2), wy[32*W] (double), ix[32], iy[32] (int)
+    double2* s_bwx = reinterpret_cast<double2*>(smem) + warp * 32 * W;
+    double* s_wy = smem + 4 * 64 * W + warp * 32 * W;
+    int* s_ix = reinterpret_cast<int*>(smem + 4 * 96 * W) + warp * 64;
+    int* s_iy = s_ix + 32;
+    const int tile = blockIdx.x * 4 + warp;
+    if (tile >= tg.nbx * tg.nby) return;
+    const int bx = tile / tg.nby, by = tile - (tile / tg.nby) * tg.nby;
+    const int X0 = tg.rlo + bx * kTileR, Y0 = tg.clo + by * kTileC;
+    double ar[kTileR], ai[kTileR];
+#pragma unroll
+    for (int r = 0; r < kTileR; ++r) ar[r] = ai[r] = 0.0;
+
+    for (int q = 0; q < 4; ++q) {
+        const int cbx = bx - (q >> 1), cby = by - (q & 1);
+        if (cbx < 0 || cby < 0) continue;
+        const int b = cbx * tg.nby + cby;
+        const uint32_t s0 = bin_start[b], s1 = bin_start[b + 1];
+        for (uint32_t s = s0; s < s1; s += 32) {
+            const uint32_t k = s + lane;
+            bool take = false;
+            int ix0 = 0, iy0 = 0;
+            double2 t = make_double2(0.0, 0.0);
+            if (k < s1) {
+                t = pos[k];
+                ix0 = (int)ceil(t.x - g.half);
+                iy0 = (int)ceil(t.y - g.half);
+                take = ix0 < X0 + kTileR && ix0 + W > X0 && iy0 < Y0 + kTileC && iy0 + W > Y0;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, take);
+            if (!m) continue;
+            if (take) {
+                const int slot = __popc(m & ((1u << lane) - 1u));
+                const double2 b2 = cmul(in[perm ? perm[k] : k], phase[k]);
+                double wx[W], wy[W];
+                kb_taps<W>((ix0 - t.x) + g.half, P, wx);
+                kb_taps<W>((iy0 - t.y) + g.half, P, wy);
+                s_ix[slot] = ix0;
+                s_iy[slot] = iy0;
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    s_bwx[slot * W + i] = make_double2(b2.x * wx[i], b2.y * wx[i]);
+                    s_wy[slot * W + i] = wy[i];
+                }
+            }
+            __syncwarp();
+            const int cnt = __popc(m);
+            for (int p = 0; p < cnt; ++p) {
+                const int ix = s_ix[p];
+                const int jl = Y0 + lane - s_iy[p];
+                const double wyl = (unsigned)jl < (unsigned)W ? s_wy[p * W + jl] : 0.0;
+#pragma unroll
+                for (int r = 0; r < kTileR; ++r) {
+                    const int i = X0 + r - ix;
+                    if ((unsigned)i < (unsigned)W) {
+                        const double2 v = s_bwx[p * W + i];
+                        ar[r] = fma(v.x, wyl, ar[r]);
+                        ai[r] = fma(v.y, wyl, ai[r]);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+    const int col = Y0 + lane;
+    if (col < g.n2) {
+#pragma unroll
+        for (int r = 0; r < kTileR; ++r) {
+            const int row = X0 + r;
+            if (row < g.n1) grid[(size_t)row * g.n2 + col] = make_double2(ar[r], ai[r]);
         }
     }
 }
@@ -287,6 +428,25 @@ struct SpreadRun {
 };
 
 template <int W>
+struct SpreadTilesRun {
+    static size_t smem() { return (size_t)4 * 32 * W * 24 + 4 * 64 * sizeof(int); }
+    static void run(const WindowPoly& P, GridGeom g, TileGeom tg, const uint32_t* bs,
+                    const uint32_t* perm, const double2* in, const double2* pos,
+                    const double2* phase, double2* grid, cudaStream_t st) {
+        static bool attr = false;
+        if (!attr) {
+            ck(cudaFuncSetAttribute(k_spread_tiles<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem()),
+               "smem attr");
+            attr = true;
+        }
+        const int tiles = tg.nbx * tg.nby;
+        k_spread_tiles<W><<<(tiles + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, perm, in, pos, phase,
+                                                                grid);
+    }
+};
+
+template <int W>
 struct InterpRun {
     static void run(const WindowPoly& P, GridGeom g, uint64_t n, const double2* pos,
                     const double2* phase, const double2* mult, const double* dx, const double* dy,
@@ -323,6 +483,41 @@ void launch_bin_keys(const double2* pos, uint64_t n, GridGeom g, int tile, uint3
     k_bin_keys<<<blocks(n, 256), 256, 0, st>>>(pos, n, g, tile, keys);
     count_launch();
     ck(cudaGetLastError(), "k_bin_keys");
+}
+
+void launch_stencil_extent(const double2* pos, uint64_t n, double half, int* ext, cudaStream_t st) {
+    const int init[4] = {INT_MAX, INT_MIN, INT_MAX, INT_MIN};
+    ck(cudaMemcpyAsync(ext, init, sizeof(init), cudaMemcpyHostToDevice, st), "ext init");
+    if (n) {
+        k_stencil_extent<<<(unsigned)std::min<uint64_t>(blocks(n, 256), 148 * 16), 256, 0, st>>>(
+            pos, n, half, ext);
+        count_launch();
+    }
+    ck(cudaGetLastError(), "k_stencil_extent");
+}
+
+void launch_tile_keys(const double2* pos, uint64_t n, double half, TileGeom tg, uint32_t* keys,
+                      cudaStream_t st) {
+    if (!n) return;
+    k_tile_keys<<<blocks(n, 256), 256, 0, st>>>(pos, n, half, tg, keys);
+    count_launch();
+    ck(cudaGetLastError(), "k_tile_keys");
+}
+
+void launch_bin_bounds(const uint32_t* sorted_keys, uint64_t n, uint32_t nbins, uint32_t* start,
+                       cudaStream_t st) {
+    k_bin_bounds<<<blocks(n + 1, 256), 256, 0, st>>>(sorted_keys, n, nbins, start);
+    count_launch();
+    ck(cudaGetLastError(), "k_bin_bounds");
+}
+
+void launch_spread_tiles(int w, const WindowPoly& win, GridGeom g, TileGeom tg,
+                         const uint32_t* bin_start, const uint32_t* perm, const double2* in,
+                         const double2* pos, const double2* phase, double2* grid, cudaStream_t st) {
+    if (tg.nbx * tg.nby == 0) return;
+    dispatch_w<SpreadTilesRun>(w, win, g, tg, bin_start, perm, in, pos, phase, grid, st);
+    count_launch();
+    ck(cudaGetLastError(), "k_spread_tiles");
 }
 
 void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st) {

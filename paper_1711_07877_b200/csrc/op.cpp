@@ -176,7 +176,8 @@ struct sbd_op {
     DevBuf<uint64_t> ro;
     DevBuf<uint32_t> cols;
     DevBuf<double2> vals;
-    DevBuf<double2> grid, spec;
+    FftWork work;
+    DevBuf<double2> spec;
     DevBuf<double2> hf, hq; // staging for the host-buffer API
     StageTimer tm;
     std::mutex mu;
@@ -215,15 +216,16 @@ struct sbd_op {
         ro.upload(d.row_offsets.data(), d.row_offsets.size(), stream);
         cols.upload(d.cols.data(), d.cols.size(), stream);
         vals.upload(reinterpret_cast<const double2*>(d.values.data()), d.nnz(), stream);
-        grid.alloc(std::max<uint64_t>({fwd_in->cells(), fwd_out->cells(), 1}));
+        fwd_in->ensure_work(work, stream);
+        fwd_out->ensure_work(work, stream);
         spec.alloc(std::max<uint64_t>(d.n_xi(), 1));
         ck(cudaStreamSynchronize(stream), "operator upload");
     }
 
     // conv_operator.cpp:301-309 on device buffers, one right-hand side.
     void apply_one(const double2* f, double2* q, cudaStream_t st) {
-        fwd_in->apply(f, spec.p, grid.p, st, &tm, w_sorted.p, "spread_src", "fft_in", "interp_xi");
-        fwd_out->apply(spec.p, q, grid.p, st, &tm, nullptr, "spread_xi", "fft_out", "interp_tgt");
+        fwd_in->apply(f, spec.p, work, st, &tm, w_sorted.p, "spread_src", "fft_in", "interp_xi");
+        fwd_out->apply(spec.p, q, work, st, &tm, nullptr, "spread_xi", "fft_out", "interp_tgt");
         if (tm.on) tm.start("spmv");
         launch_spmv(d.n_tgt(), ro.p, cols.p, vals.p, f, q, st);
         if (tm.on) tm.stop();
@@ -231,8 +233,8 @@ struct sbd_op {
 
     // conv_operator.cpp:311-324
     void apply_adjoint_one(const double2* u, double2* q, cudaStream_t st) {
-        fwd_out->apply_transpose(u, spec.p, grid.p, st, &tm, w_sorted.p, /*conj_in=*/1, 0);
-        fwd_in->apply_transpose(spec.p, q, grid.p, st, &tm, nullptr, 0, /*conj_out=*/1);
+        fwd_out->apply_transpose(u, spec.p, work, st, &tm, w_sorted.p, /*conj_in=*/1, 0);
+        fwd_in->apply_transpose(spec.p, q, work, st, &tm, nullptr, 0, /*conj_out=*/1);
         if (tm.on) tm.start("spmv_adjoint");
         launch_spmv_adjoint(d.n_tgt(), ro.p, cols.p, vals.p, u, q, st);
         if (tm.on) tm.stop();
@@ -240,7 +242,8 @@ struct sbd_op {
 
     size_t device_bytes() const {
         return fwd_in->device_bytes() + fwd_out->device_bytes() + w_sorted.bytes() + ro.bytes() +
-               cols.bytes() + vals.bytes() + grid.bytes() + spec.bytes() + hf.bytes() + hq.bytes();
+               cols.bytes() + vals.bytes() + work.grid.bytes() + work.T.bytes() + work.band.bytes() +
+               spec.bytes() + hf.bytes() + hq.bytes();
     }
 
     // conv_operator.cpp:338-353
@@ -261,7 +264,8 @@ struct sbd_nufft {
     std::unique_ptr<Plan> plan;
     int device = 0;
     cudaStream_t stream = nullptr;
-    DevBuf<double2> grid, in, out;
+    FftWork work;
+    DevBuf<double2> in, out;
     ~sbd_nufft() {
         if (stream) cudaStreamDestroy(stream);
     }
@@ -536,7 +540,7 @@ int sbd_nufft_create(const double* points, uint64_t np, const double* freqs, uin
         o.direct_threshold = direct_threshold;
         o.max_grid_bytes = max_grid_bytes ? max_grid_bytes : (uint64_t(4) << 30);
         p->plan = std::make_unique<Plan>(points, np, freqs, nf, sign, o, device, true, true, p->stream);
-        p->grid.alloc(std::max<uint64_t>(p->plan->cells(), 1));
+        p->plan->ensure_work(p->work, p->stream);
         *out = p.release();
     });
 }
@@ -550,9 +554,9 @@ static int nufft_run(sbd_nufft* p, const double* in, double* out, bool transpose
         p->in.upload(reinterpret_cast<const double2*>(in), nin, p->stream);
         if (p->out.n < nout) p->out.alloc(std::max<uint64_t>(nout, 1));
         if (transpose)
-            p->plan->apply_transpose(p->in.p, p->out.p, p->grid.p, p->stream, nullptr);
+            p->plan->apply_transpose(p->in.p, p->out.p, p->work, p->stream, nullptr);
         else
-            p->plan->apply(p->in.p, p->out.p, p->grid.p, p->stream, nullptr);
+            p->plan->apply(p->in.p, p->out.p, p->work, p->stream, nullptr);
         ck(cudaMemcpyAsync(out, p->out.p, nout * 16, cudaMemcpyDeviceToHost, p->stream), "D2H");
         ck(cudaStreamSynchronize(p->stream), "nufft sync");
     });

@@ -97,14 +97,39 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
     dx.upload(hx.data(), hx.size(), st);
     dy.upload(hy.data(), hy.size(), st);
 
-    // ---- sort both sides by grid tile of the stencil start
+    // ---- populated region of the spread (stencil starts never wrap: points
+    // sit in [n/4, 3n/4] of the grid, nufft.cpp:166-169), for the pruned path
     const GridGeom g{ax.n, ay.n, 0.5 * w};
+    {
+        DevBuf<int> ext(4);
+        launch_stencil_extent(t.p, np, g.half, ext.p, st);
+        int he[4];
+        ck(cudaMemcpyAsync(he, ext.p, sizeof(he), cudaMemcpyDeviceToHost, st), "extent D2H");
+        ck(cudaStreamSynchronize(st), "extent");
+        pruned = sort_points && np > 0 && he[0] >= 0 && he[1] + w <= ax.n && he[2] >= 0 &&
+                 he[3] + w <= ay.n;
+        if (pruned) {
+            tg.rlo = he[0];
+            tg.clo = he[2];
+            tg.nbx = (he[1] + w - he[0] + kTileR - 1) / kTileR;
+            tg.nby = (he[3] + w - he[2] + kTileC - 1) / kTileC;
+            rlo = tg.rlo;
+            clo = tg.clo;
+            rhi = std::min(ax.n, tg.rlo + tg.nbx * kTileR);
+            chi = std::min(ay.n, tg.clo + tg.nby * kTileC);
+        }
+    }
+
+    // ---- sort both sides by grid tile of the stencil start
     auto sort_side = [&](DevBuf<double2>& pos, DevBuf<double2>& ph, DevBuf<uint32_t>& perm,
-                         uint64_t n) {
-        if (n < 2) return;
+                         uint64_t n, bool tiles) {
+        if (n < 1) return;
         DevBuf<uint32_t> keys(n);
         perm.alloc(n);
-        launch_bin_keys(pos.p, n, g, kBinTile, keys.p, st);
+        if (tiles)
+            launch_tile_keys(pos.p, n, g.half, tg, keys.p, st);
+        else
+            launch_bin_keys(pos.p, n, g, kBinTile, keys.p, st);
         launch_iota(perm.p, n, st);
         sort_by_key(keys.p, perm.p, n, st);
         DevBuf<double2> a(n), b(n);
@@ -112,18 +137,94 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
         launch_gather(ph.p, perm.p, b.p, n, st);
         pos = std::move(a);
         ph = std::move(b);
+        if (tiles) {
+            const uint32_t nbins = (uint32_t)tg.nbx * (uint32_t)tg.nby;
+            bin_start.alloc(nbins + 1);
+            launch_bin_bounds(keys.p, n, nbins, bin_start.p, st);
+        }
+        ck(cudaStreamSynchronize(st), "sort side");
     };
-    if (sort_points) sort_side(t, pre, perm_t, np);
-    if (sort_outputs) sort_side(this->s, post, perm_s, nf);
+    if (sort_points) sort_side(t, pre, perm_t, np, pruned);
+    if (sort_outputs) sort_side(this->s, post, perm_s, nf, false);
 
-    // ---- cuFFT: unnormalised e^{+2 pi i jm/n} (FFTW_BACKWARD), row-major
-    // n1 x n2 with the second index fastest (nufft.cpp:207-213, 244).
-    ckfft(cufftPlan2d(&fft, ax.n, ay.n, CUFFT_Z2Z), "cufftPlan2d");
+    // ---- band-limited FFT plans (pruned path): the interpolation only reads
+    // modes |j| <= n/4 (nufft.cpp:194-205), so columns outside the band are
+    // never transformed and rows outside the populated region are zero.
+    band2 = ay.n / 4;
+    bc = 2 * band2 + 1;
+    {
+        std::vector<double> hb(bc);
+        for (int c = 0; c < bc; ++c) hb[c] = hy[c <= band2 ? c : ay.n + c - bc];
+        dy_band.upload(hb.data(), bc, st);
+    }
+    if (pruned) {
+        int n2[1] = {ay.n}, n1[1] = {ax.n};
+        ckfft(cufftPlanMany(&fft_row, 1, n2, n2, 1, ay.n, n2, 1, ay.n, CUFFT_Z2Z, rhi - rlo),
+              "cufftPlanMany rows");
+        ckfft(cufftPlanMany(&fft_colA, 1, n1, n1, ay.n, 1, n1, bc, 1, CUFFT_Z2Z, band2 + 1),
+              "cufftPlanMany cols A");
+        ckfft(cufftPlanMany(&fft_colB, 1, n1, n1, ay.n, 1, n1, bc, 1, CUFFT_Z2Z, band2),
+              "cufftPlanMany cols B");
+    }
     ck(cudaStreamSynchronize(st), "plan build");
 }
 
 Plan::~Plan() {
     if (fft) cufftDestroy(fft);
+    if (fft_row) cufftDestroy(fft_row);
+    if (fft_colA) cufftDestroy(fft_colA);
+    if (fft_colB) cufftDestroy(fft_colB);
+}
+
+void FftWork::ensure(int n1_, int n2_, int bc_, cudaStream_t st) {
+    if (n1_ == n1 && n2_ == n2 && bc_ == bc) return;
+    n1 = n1_;
+    n2 = n2_;
+    bc = bc_;
+    const size_t cells = (size_t)n1 * n2;
+    grid.alloc(std::max<size_t>(cells, 1));
+    T.alloc(std::max<size_t>(cells, 1));
+    band.alloc(std::max<size_t>((size_t)n1 * bc, 1));
+    ck(cudaMemsetAsync(grid.p, 0, grid.bytes(), st), "grid zero");
+    ck(cudaMemsetAsync(T.p, 0, T.bytes(), st), "T zero");
+    gr0 = gr1 = gc0 = gc1 = tr0 = tr1 = 0;
+}
+
+void Plan::ensure_work(FftWork& wk, cudaStream_t st) const {
+    if (fast) wk.ensure(std::max(wk.n1, ax.n), std::max(wk.n2, ay.n), std::max(wk.bc, bc), st);
+}
+
+namespace {
+
+// Zero the cells of rectangle D not covered by rectangle O (row-major, pitch n2).
+void zero_rect_minus(double2* base, int n2, int r0, int r1, int c0, int c1, int R0, int R1, int C0,
+                     int C1, cudaStream_t st) {
+    if (r1 <= r0 || c1 <= c0) return;
+    const size_t pitch = (size_t)n2 * sizeof(double2);
+    auto zero = [&](int a0, int a1, int b0, int b1) {
+        if (a1 <= a0 || b1 <= b0) return;
+        ck(cudaMemset2DAsync(base + (size_t)a0 * n2 + b0, pitch, 0, (size_t)(b1 - b0) * sizeof(double2),
+                             (size_t)(a1 - a0), st),
+           "zero strip");
+    };
+    zero(r0, std::min(r1, R0), c0, c1);           // rows above O
+    zero(std::max(r0, R1), r1, c0, c1);           // rows below O
+    const int m0 = std::max(r0, R0), m1 = std::min(r1, R1);
+    zero(m0, m1, c0, std::min(c1, C0));           // left of O
+    zero(m0, m1, std::max(c0, C1), c1);           // right of O
+}
+
+void full_fft(const Plan& p, double2* grid, cudaStream_t st) { p.full_transform(grid, st); }
+
+} // namespace
+
+void Plan::full_transform(double2* grid, cudaStream_t st) const {
+    if (!fft) ckfft(cufftPlan2d(&fft, ax.n, ay.n, CUFFT_Z2Z), "cufftPlan2d");
+    ckfft(cufftSetStream(fft, st), "cufftSetStream");
+    ckfft(cufftExecZ2Z(fft, reinterpret_cast<cufftDoubleComplex*>(grid),
+                       reinterpret_cast<cufftDoubleComplex*>(grid), CUFFT_INVERSE),
+          "cufftExecZ2Z");
+    count_launch();
 }
 
 size_t Plan::device_bytes() const {
@@ -132,9 +233,9 @@ size_t Plan::device_bytes() const {
 }
 
 // nufft.cpp:218-290
-void Plan::apply(const double2* in, double2* out, double2* grid, cudaStream_t st,
-                 StageTimer* tm, const double2* mult, const char* tag_spread,
-                 const char* tag_fft, const char* tag_interp) const {
+void Plan::apply(const double2* in, double2* out, FftWork& wk, cudaStream_t st, StageTimer* tm,
+                 const double2* mult, const char* tag_spread, const char* tag_fft,
+                 const char* tag_interp) const {
     if (!fast) {
         if (tm) tm->start(tag_interp);
         launch_ndft(pts.p, np, frq.p, nf, in, sign, out, st);
@@ -142,27 +243,63 @@ void Plan::apply(const double2* in, double2* out, double2* grid, cudaStream_t st
         if (tm) tm->stop();
         return;
     }
+    ensure_work(wk, st);
     const GridGeom g{ax.n, ay.n, 0.5 * w};
+    const int n2 = ay.n;
+    if (pruned) {
+        if (tm) tm->start(tag_spread);
+        zero_rect_minus(wk.grid.p, n2, wk.gr0, wk.gr1, wk.gc0, wk.gc1, rlo, rhi, clo, chi, st);
+        launch_spread_tiles(w, win, g, tg, bin_start.p, perm_t.n ? perm_t.p : nullptr, in, t.p, pre.p,
+                            wk.grid.p, st);
+        wk.gr0 = rlo;
+        wk.gr1 = rhi;
+        wk.gc0 = clo;
+        wk.gc1 = chi;
+        if (tm) tm->stop();
+        if (tm) tm->start(tag_fft);
+        // rows [rlo, rhi): grid -> T (out of place; T rows elsewhere stay zero)
+        zero_rect_minus(wk.T.p, n2, wk.tr0, wk.tr1, 0, n2, rlo, rhi, 0, n2, st);
+        auto* G = reinterpret_cast<cufftDoubleComplex*>(wk.grid.p);
+        auto* T = reinterpret_cast<cufftDoubleComplex*>(wk.T.p);
+        auto* B = reinterpret_cast<cufftDoubleComplex*>(wk.band.p);
+        ckfft(cufftSetStream(fft_row, st), "cufftSetStream");
+        ckfft(cufftExecZ2Z(fft_row, G + (size_t)rlo * n2, T + (size_t)rlo * n2, CUFFT_INVERSE), "fft rows");
+        wk.tr0 = rlo;
+        wk.tr1 = rhi;
+        // band columns of T -> band buffer (n1 x bc, columns in mode order mod bc)
+        ckfft(cufftSetStream(fft_colA, st), "cufftSetStream");
+        ckfft(cufftExecZ2Z(fft_colA, T, B, CUFFT_INVERSE), "fft cols A");
+        ckfft(cufftSetStream(fft_colB, st), "cufftSetStream");
+        ckfft(cufftExecZ2Z(fft_colB, T + (n2 - band2), B + (band2 + 1), CUFFT_INVERSE), "fft cols B");
+        count_launch(3);
+        if (tm) tm->stop();
+        if (tm) tm->start(tag_interp);
+        const GridGeom gb{ax.n, bc, 0.5 * w};
+        launch_interp(w, win, gb, nf, s.p, post.p, mult, dx.p, dy_band.p, wk.band.p,
+                      perm_s.n ? perm_s.p : nullptr, out, 0, 0, st);
+        if (tm) tm->stop();
+        return;
+    }
     if (tm) tm->start(tag_spread);
-    ck(cudaMemsetAsync(grid, 0, cells() * sizeof(double2), st), "grid zero");
+    ck(cudaMemsetAsync(wk.grid.p, 0, cells() * sizeof(double2), st), "grid zero");
     launch_spread(w, win, g, np, perm_t.n ? perm_t.p : nullptr, in, t.p, pre.p, nullptr, nullptr,
-                  nullptr, grid, 0, st);
+                  nullptr, wk.grid.p, 0, st);
     if (tm) tm->stop();
     if (tm) tm->start(tag_fft);
-    ckfft(cufftSetStream(fft, st), "cufftSetStream");
-    ckfft(cufftExecZ2Z(fft, reinterpret_cast<cufftDoubleComplex*>(grid),
-                       reinterpret_cast<cufftDoubleComplex*>(grid), CUFFT_INVERSE),
-          "cufftExecZ2Z");
-    count_launch();
+    full_fft(*this, wk.grid.p, st);
     if (tm) tm->stop();
     if (tm) tm->start(tag_interp);
-    launch_interp(w, win, g, nf, s.p, post.p, mult, dx.p, dy.p, grid,
+    launch_interp(w, win, g, nf, s.p, post.p, mult, dx.p, dy.p, wk.grid.p,
                   perm_s.n ? perm_s.p : nullptr, out, 0, 0, st);
     if (tm) tm->stop();
+    wk.gr0 = 0;
+    wk.gr1 = ax.n;
+    wk.gc0 = 0;
+    wk.gc1 = ay.n;
 }
 
 // nufft.cpp:295-367
-void Plan::apply_transpose(const double2* in, double2* out, double2* grid, cudaStream_t st,
+void Plan::apply_transpose(const double2* in, double2* out, FftWork& wk, cudaStream_t st,
                            StageTimer* tm, const double2* mult, int conj_in,
                            int conj_out) const {
     if (!fast) {
@@ -181,24 +318,25 @@ void Plan::apply_transpose(const double2* in, double2* out, double2* grid, cudaS
         if (conj_in) ck(cudaStreamSynchronize(st), "ndft_T tmp");
         return;
     }
+    ensure_work(wk, st);
     const GridGeom g{ax.n, ay.n, 0.5 * w};
     if (tm) tm->start("spread_T");
-    ck(cudaMemsetAsync(grid, 0, cells() * sizeof(double2), st), "grid zero");
+    ck(cudaMemsetAsync(wk.grid.p, 0, cells() * sizeof(double2), st), "grid zero");
     // spread at the frequency stencils with postphase, deconv folded in
     launch_spread(w, win, g, nf, perm_s.n ? perm_s.p : nullptr, in, s.p, post.p, nullptr, dx.p,
-                  dy.p, grid, conj_in, st);
+                  dy.p, wk.grid.p, conj_in, st);
     if (tm) tm->stop();
     if (tm) tm->start("fft_T");
-    ckfft(cufftSetStream(fft, st), "cufftSetStream");
-    ckfft(cufftExecZ2Z(fft, reinterpret_cast<cufftDoubleComplex*>(grid),
-                       reinterpret_cast<cufftDoubleComplex*>(grid), CUFFT_INVERSE),
-          "cufftExecZ2Z");
-    count_launch();
+    full_fft(*this, wk.grid.p, st);
     if (tm) tm->stop();
     if (tm) tm->start("interp_T");
-    launch_interp(w, win, g, np, t.p, pre.p, mult, nullptr, nullptr, grid,
+    launch_interp(w, win, g, np, t.p, pre.p, mult, nullptr, nullptr, wk.grid.p,
                   perm_t.n ? perm_t.p : nullptr, out, 0, conj_out, st);
     if (tm) tm->stop();
+    wk.gr0 = 0;
+    wk.gr1 = ax.n;
+    wk.gc0 = 0;
+    wk.gc1 = ay.n;
 }
 
 std::vector<uint32_t> Plan::adopt_point_order(cudaStream_t st) {

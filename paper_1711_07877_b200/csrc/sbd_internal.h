@@ -115,6 +115,25 @@ struct StageTimer {
     ~StageTimer();
 };
 
+// Grid / FFT scratch of one or more plans of equal grid size. The pruned
+// forward path keeps the invariant "grid and T are zero outside the recorded
+// dirty rectangles", so no full-grid memset is needed per apply.
+struct FftWork {
+    DevBuf<double2> grid, T, band;
+    int n1 = 0, n2 = 0, bc = 0;
+    int gr0 = 0, gr1 = 0, gc0 = 0, gc1 = 0; // grid cells possibly nonzero
+    int tr0 = 0, tr1 = 0;                   // rows of T possibly nonzero
+    void ensure(int n1_, int n2_, int bc_, cudaStream_t st);
+};
+
+// Spread tiles of the pruned forward path: one warp owns kTileR x kTileC
+// grid cells (lanes = columns, rows in registers).
+constexpr int kTileR = 16;
+constexpr int kTileC = 32;
+struct TileGeom {
+    int rlo, clo, nbx, nby;
+};
+
 // A type-III NUFFT plan on one device (reference NufftPlan, nufft.hpp:30-56).
 // Point side ("t": spread in apply, gather in apply_transpose) and output side
 // ("s": gather in apply, spread in apply_transpose) are stored in a sorted
@@ -145,7 +164,18 @@ class Plan {
     DevBuf<double2> t, pre;  // point side: grid coords (cells), prephase
     DevBuf<double2> s, post; // output side: mode coords, postphase
     DevBuf<double> dx, dy;   // deconvolution per FFT index (nufft.cpp:194-205)
-    cufftHandle fft = 0;
+    mutable cufftHandle fft = 0; // full 2D transform (transpose path), created lazily
+
+    // Pruned forward path (apply): points binned by kTileR x kTileC tiles of
+    // the populated region; row FFTs over the populated rows only, column FFTs
+    // over the band columns only (the only modes the interpolation reads).
+    bool pruned = false;
+    int rlo = 0, rhi = 0, clo = 0, chi = 0; // region written by the spread tiles
+    TileGeom tg{};
+    DevBuf<uint32_t> bin_start;
+    int band2 = 0, bc = 0;
+    DevBuf<double> dy_band;
+    cufftHandle fft_row = 0, fft_colA = 0, fft_colB = 0;
 
     uint64_t cells() const { return fast ? (uint64_t)ax.n * (uint64_t)ay.n : 0; }
     size_t device_bytes() const;
@@ -153,12 +183,16 @@ class Plan {
     // Enqueue apply / apply_transpose on stream `st`. in/out in caller order.
     // `grid` must hold cells() complex values. `extra` (optional) multiplies
     // the outputs elementwise in SORTED output order (used for omega-hat).
-    void apply(const double2* in, double2* out, double2* grid, cudaStream_t st,
+    void apply(const double2* in, double2* out, FftWork& wk, cudaStream_t st,
                StageTimer* tm, const double2* mult = nullptr, const char* tag_spread = "spread",
                const char* tag_fft = "fft", const char* tag_interp = "interp") const;
-    void apply_transpose(const double2* in, double2* out, double2* grid, cudaStream_t st,
+    void apply_transpose(const double2* in, double2* out, FftWork& wk, cudaStream_t st,
                          StageTimer* tm, const double2* mult = nullptr, int conj_in = 0,
                          int conj_out = 0) const;
+    void ensure_work(FftWork& wk, cudaStream_t st) const;
+    // In-place unnormalised e^{+2 pi i} 2D transform of a full n1 x n2 grid
+    // (FFTW_BACKWARD, nufft.cpp:207-213, 252).
+    void full_transform(double2* grid, cudaStream_t st) const;
     // Drop the point-side permutation: the caller promises to pass point-side
     // data in this plan's sorted order from now on. Returns the permutation
     // (sorted position -> caller index) on the host.
@@ -179,6 +213,16 @@ void launch_plan_outputs(const double2* frq, uint64_t n, Axis ax, Axis ay, doubl
 void launch_deconv_tables(Axis a, double beta, double* d, cudaStream_t st);
 void launch_bin_keys(const double2* pos, uint64_t n, GridGeom g, int tile, uint32_t* keys,
                      cudaStream_t st);
+// min/max of the stencil starts ceil(t - w/2): ext = {ixmin, ixmax, iymin, iymax}
+void launch_stencil_extent(const double2* pos, uint64_t n, double half, int* ext, cudaStream_t st);
+void launch_tile_keys(const double2* pos, uint64_t n, double half, TileGeom tg, uint32_t* keys,
+                      cudaStream_t st);
+void launch_bin_bounds(const uint32_t* sorted_keys, uint64_t n, uint32_t nbins, uint32_t* start,
+                       cudaStream_t st);
+// Tile-owned spread: writes every cell of the tiles (no atomics, no memset).
+void launch_spread_tiles(int w, const WindowPoly& win, GridGeom g, TileGeom tg,
+                         const uint32_t* bin_start, const uint32_t* perm, const double2* in,
+                         const double2* pos, const double2* phase, double2* grid, cudaStream_t st);
 void sort_by_key(uint32_t* keys, uint32_t* vals, uint64_t n, cudaStream_t st);
 void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st);
 template <typename T>
