@@ -182,15 +182,46 @@ __global__ void __launch_bounds__(256) k_spread(WindowPoly P, GridGeom g, uint64
     }
 }
 
+// Row accumulation for one staged point whose stencil starts D rows below the
+// warp tile's first row: rows r in [max(0,D), min(kTileR, D+W)) get
+// acc[r] += (b wx)[r-D] * wy[lane]. D is a template parameter so the row range
+// is straight-line code; rows_dispatch picks it with a binary search on d.
+template <int W, int D>
+__device__ __forceinline__ void rows_acc(const double2* __restrict__ bwx, double wyl,
+                                         double (&ar)[kTileR], double (&ai)[kTileR]) {
+    constexpr int r0 = D > 0 ? D : 0;
+    constexpr int r1 = D + W < kTileR ? D + W : kTileR;
+#pragma unroll
+    for (int r = r0; r < r1; ++r) {
+        const double2 v = bwx[r - D];
+        ar[r] = fma(v.x, wyl, ar[r]);
+        ai[r] = fma(v.y, wyl, ai[r]);
+    }
+}
+
+template <int W, int Lo, int Hi>
+__device__ __forceinline__ void rows_dispatch(int d, const double2* __restrict__ bwx, double wyl,
+                                              double (&ar)[kTileR], double (&ai)[kTileR]) {
+    if constexpr (Hi - Lo == 1) {
+        rows_acc<W, Lo>(bwx, wyl, ar, ai);
+    } else {
+        constexpr int Mid = (Lo + Hi) / 2;
+        if (d < Mid)
+            rows_dispatch<W, Lo, Mid>(d, bwx, wyl, ar, ai);
+        else
+            rows_dispatch<W, Mid, Hi>(d, bwx, wyl, ar, ai);
+    }
+}
+
 // Tile-owned spread (nufft.cpp:229-250 restated output-stationary). One warp
 // owns a kTileR x kTileC block of grid cells: lane = column, the kTileR rows of
 // that column live in registers. The warp scans the points binned in its own
 // tile and the three tiles above/left of it (a stencil starting there can
-// reach into this tile), stages the intersecting ones in its shared-memory
-// slice with their precomputed b*wx and wy taps (one polynomial window
-// evaluation per staged point, lane = point), then accumulates
-// acc[r] += (b wx)[row r] * wy[lane] point by point. Every cell of the tile is
-// written exactly once: no atomics and no zero-fill of the grid.
+// reach into this tile), queues the intersecting ones, evaluates their
+// windows 32 at a time (lane = point; b*wx and wy go to the warp's
+// shared-memory slice), then accumulates acc[r] += (b wx)[row] * wy[lane]
+// point by point. Every cell of the tile is written exactly once: no atomics
+// and no zero-fill of the grid.
 template <int W>
 __global__ void __launch_bounds__(128) k_spread_tiles(WindowPoly P, GridGeom g, TileGeom tg,
                                                       const uint32_t* __restrict__ bin_start,
@@ -201,10 +232,11 @@ __global__ void __launch_bounds__(128) k_spread_tiles(WindowPoly P, GridGeom g, 
                                                       double2* __restrict__ grid) {
     extern __shared__ double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // per warp: bwx[32*W] (double2), wy[32*W] (double), ix[32], iy[32] (int)
+    // per warp: bwx[32*W] (double2), wy[32*W] (double), queue k[64], ix[32], iy[32]
     double2* s_bwx = reinterpret_cast<double2*>(smem) + warp * 32 * W;
     double* s_wy = smem + 4 * 64 * W + warp * 32 * W;
-    int* s_ix = reinterpret_cast<int*>(smem + 4 * 96 * W) + warp * 64;
+    uint32_t* s_q = reinterpret_cast<uint32_t*>(smem + 4 * 96 * W) + warp * 128;
+    int* s_ix = reinterpret_cast<int*>(s_q + 64);
     int* s_iy = s_ix + 32;
     const int tile = blockIdx.x * 4 + warp;
     if (tile >= tg.nbx * tg.nby) return;
@@ -214,6 +246,35 @@ __global__ void __launch_bounds__(128) k_spread_tiles(WindowPoly P, GridGeom g, 
 #pragma unroll
     for (int r = 0; r < kTileR; ++r) ar[r] = ai[r] = 0.0;
 
+    int queued = 0; // warp-uniform
+    // Evaluate windows for the first n (<= 32) queued points and accumulate them.
+    auto flush = [&](int n) {
+        if (lane < n) {
+            const uint32_t k = s_q[lane];
+            const double2 t = pos[k];
+            const int ix0 = (int)ceil(t.x - g.half), iy0 = (int)ceil(t.y - g.half);
+            const double2 b2 = cmul(in[perm ? perm[k] : k], phase[k]);
+            double wx[W], wy[W];
+            kb_taps<W>((ix0 - t.x) + g.half, P, wx);
+            kb_taps<W>((iy0 - t.y) + g.half, P, wy);
+            s_ix[lane] = ix0 - X0;
+            s_iy[lane] = iy0;
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                s_bwx[lane * W + i] = make_double2(b2.x * wx[i], b2.y * wx[i]);
+                s_wy[lane * W + i] = wy[i];
+            }
+        }
+        __syncwarp();
+        for (int p = 0; p < n; ++p) {
+            const int d = s_ix[p];
+            const int jl = Y0 + lane - s_iy[p];
+            const double wyl = (unsigned)jl < (unsigned)W ? s_wy[p * W + jl] : 0.0;
+            rows_dispatch<W, 1 - W, kTileR>(d, s_bwx + p * W, wyl, ar, ai);
+        }
+        __syncwarp();
+    };
+
     for (int q = 0; q < 4; ++q) {
         const int cbx = bx - (q >> 1), cby = by - (q & 1);
         if (cbx < 0 || cby < 0) continue;
@@ -222,49 +283,24 @@ __global__ void __launch_bounds__(128) k_spread_tiles(WindowPoly P, GridGeom g, 
         for (uint32_t s = s0; s < s1; s += 32) {
             const uint32_t k = s + lane;
             bool take = false;
-            int ix0 = 0, iy0 = 0;
-            double2 t = make_double2(0.0, 0.0);
             if (k < s1) {
-                t = pos[k];
-                ix0 = (int)ceil(t.x - g.half);
-                iy0 = (int)ceil(t.y - g.half);
+                const double2 t = pos[k];
+                const int ix0 = (int)ceil(t.x - g.half), iy0 = (int)ceil(t.y - g.half);
                 take = ix0 < X0 + kTileR && ix0 + W > X0 && iy0 < Y0 + kTileC && iy0 + W > Y0;
             }
             const unsigned m = __ballot_sync(0xffffffffu, take);
-            if (!m) continue;
-            if (take) {
-                const int slot = __popc(m & ((1u << lane) - 1u));
-                const double2 b2 = cmul(in[perm ? perm[k] : k], phase[k]);
-                double wx[W], wy[W];
-                kb_taps<W>((ix0 - t.x) + g.half, P, wx);
-                kb_taps<W>((iy0 - t.y) + g.half, P, wy);
-                s_ix[slot] = ix0;
-                s_iy[slot] = iy0;
-#pragma unroll
-                for (int i = 0; i < W; ++i) {
-                    s_bwx[slot * W + i] = make_double2(b2.x * wx[i], b2.y * wx[i]);
-                    s_wy[slot * W + i] = wy[i];
-                }
-            }
+            if (take) s_q[queued + __popc(m & ((1u << lane) - 1u))] = k;
+            queued += __popc(m);
             __syncwarp();
-            const int cnt = __popc(m);
-            for (int p = 0; p < cnt; ++p) {
-                const int ix = s_ix[p];
-                const int jl = Y0 + lane - s_iy[p];
-                const double wyl = (unsigned)jl < (unsigned)W ? s_wy[p * W + jl] : 0.0;
-#pragma unroll
-                for (int r = 0; r < kTileR; ++r) {
-                    const int i = X0 + r - ix;
-                    if ((unsigned)i < (unsigned)W) {
-                        const double2 v = s_bwx[p * W + i];
-                        ar[r] = fma(v.x, wyl, ar[r]);
-                        ai[r] = fma(v.y, wyl, ai[r]);
-                    }
-                }
+            if (queued >= 32) {
+                flush(32);
+                if (lane < queued - 32) s_q[lane] = s_q[32 + lane];
+                queued -= 32;
+                __syncwarp();
             }
-            __syncwarp();
         }
     }
+    if (queued) flush(queued);
     const int col = Y0 + lane;
     if (col < g.n2) {
 #pragma unroll
@@ -429,7 +465,7 @@ struct SpreadRun {
 
 template <int W>
 struct SpreadTilesRun {
-    static size_t smem() { return (size_t)4 * 32 * W * 24 + 4 * 64 * sizeof(int); }
+    static size_t smem() { return (size_t)4 * 32 * W * 24 + 4 * 128 * sizeof(uint32_t); }
     static void run(const WindowPoly& P, GridGeom g, TileGeom tg, const uint32_t* bs,
                     const uint32_t* perm, const double2* in, const double2* pos,
                     const double2* phase, double2* grid, cudaStream_t st) {

@@ -188,6 +188,7 @@ void FftWork::ensure(int n1_, int n2_, int bc_, cudaStream_t st) {
     ck(cudaMemsetAsync(grid.p, 0, grid.bytes(), st), "grid zero");
     ck(cudaMemsetAsync(T.p, 0, T.bytes(), st), "T zero");
     gr0 = gr1 = gc0 = gc1 = tr0 = tr1 = 0;
+    g_pitch = t_pitch = 0;
 }
 
 void Plan::ensure_work(FftWork& wk, cudaStream_t st) const {
@@ -248,17 +249,24 @@ void Plan::apply(const double2* in, double2* out, FftWork& wk, cudaStream_t st, 
     const int n2 = ay.n;
     if (pruned) {
         if (tm) tm->start(tag_spread);
-        zero_rect_minus(wk.grid.p, n2, wk.gr0, wk.gr1, wk.gc0, wk.gc1, rlo, rhi, clo, chi, st);
+        if (wk.g_pitch == n2)
+            zero_rect_minus(wk.grid.p, n2, wk.gr0, wk.gr1, wk.gc0, wk.gc1, rlo, rhi, clo, chi, st);
+        else if (wk.g_pitch)  // written by a plan of another grid size: clear all of it
+            zero_rect_minus(wk.grid.p, wk.g_pitch, wk.gr0, wk.gr1, wk.gc0, wk.gc1, 0, 0, 0, 0, st);
         launch_spread_tiles(w, win, g, tg, bin_start.p, perm_t.n ? perm_t.p : nullptr, in, t.p, pre.p,
                             wk.grid.p, st);
         wk.gr0 = rlo;
         wk.gr1 = rhi;
         wk.gc0 = clo;
         wk.gc1 = chi;
+        wk.g_pitch = n2;
         if (tm) tm->stop();
         if (tm) tm->start(tag_fft);
         // rows [rlo, rhi): grid -> T (out of place; T rows elsewhere stay zero)
-        zero_rect_minus(wk.T.p, n2, wk.tr0, wk.tr1, 0, n2, rlo, rhi, 0, n2, st);
+        if (wk.t_pitch == n2)
+            zero_rect_minus(wk.T.p, n2, wk.tr0, wk.tr1, 0, n2, rlo, rhi, 0, n2, st);
+        else if (wk.t_pitch)
+            zero_rect_minus(wk.T.p, wk.t_pitch, wk.tr0, wk.tr1, 0, wk.t_pitch, 0, 0, 0, 0, st);
         auto* G = reinterpret_cast<cufftDoubleComplex*>(wk.grid.p);
         auto* T = reinterpret_cast<cufftDoubleComplex*>(wk.T.p);
         auto* B = reinterpret_cast<cufftDoubleComplex*>(wk.band.p);
@@ -266,6 +274,7 @@ void Plan::apply(const double2* in, double2* out, FftWork& wk, cudaStream_t st, 
         ckfft(cufftExecZ2Z(fft_row, G + (size_t)rlo * n2, T + (size_t)rlo * n2, CUFFT_INVERSE), "fft rows");
         wk.tr0 = rlo;
         wk.tr1 = rhi;
+        wk.t_pitch = n2;
         // band columns of T -> band buffer (n1 x bc, columns in mode order mod bc)
         ckfft(cufftSetStream(fft_colA, st), "cufftSetStream");
         ckfft(cufftExecZ2Z(fft_colA, T, B, CUFFT_INVERSE), "fft cols A");
@@ -296,6 +305,7 @@ void Plan::apply(const double2* in, double2* out, FftWork& wk, cudaStream_t st, 
     wk.gr1 = ax.n;
     wk.gc0 = 0;
     wk.gc1 = ay.n;
+    wk.g_pitch = ay.n;
 }
 
 // nufft.cpp:295-367
@@ -337,6 +347,7 @@ void Plan::apply_transpose(const double2* in, double2* out, FftWork& wk, cudaStr
     wk.gr1 = ax.n;
     wk.gc0 = 0;
     wk.gc1 = ay.n;
+    wk.g_pitch = ay.n;
 }
 
 std::vector<uint32_t> Plan::adopt_point_order(cudaStream_t st) {

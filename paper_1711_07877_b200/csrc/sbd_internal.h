@@ -121,8 +121,10 @@ struct StageTimer {
 struct FftWork {
     DevBuf<double2> grid, T, band;
     int n1 = 0, n2 = 0, bc = 0;
-    int gr0 = 0, gr1 = 0, gc0 = 0, gc1 = 0; // grid cells possibly nonzero
-    int tr0 = 0, tr1 = 0;                   // rows of T possibly nonzero
+    int gr0 = 0, gr1 = 0, gc0 = 0, gc1 = 0; // grid cells possibly nonzero ...
+    int g_pitch = 0;                        // ... in a row-major layout of this pitch
+    int tr0 = 0, tr1 = 0;                   // rows of T possibly nonzero ...
+    int t_pitch = 0;                        // ... at this pitch
     void ensure(int n1_, int n2_, int bc_, cudaStream_t st);
 };
 
