@@ -52,6 +52,32 @@ __device__ __forceinline__ void kb_taps(double u, const WindowPoly& P, double (&
     }
 }
 
+// Same taps as kb_taps, handed to a sink f(i, w_i) as they are produced (keeps
+// the register footprint small when the taps go straight to shared memory).
+template <int W, typename F>
+__device__ __forceinline__ void kb_taps_each(double u, const WindowPoly& P, F&& f) {
+    const double v = 2.0 * u - 1.0;
+    const double v2 = v * v;
+#pragma unroll
+    for (int i = 0; i < W / 2; ++i) {
+        double e = P.e[i][kHorner - 1], o = P.o[i][kHorner - 1];
+#pragma unroll
+        for (int h = kHorner - 2; h >= 0; --h) {
+            e = fma(e, v2, P.e[i][h]);
+            o = fma(o, v2, P.o[i][h]);
+        }
+        f(i, fma(v, o, e));
+        f(W - 1 - i, fma(-v, o, e));
+    }
+    if (W & 1) {
+        constexpr int m = W / 2;
+        double e = P.e[m][kHorner - 1];
+#pragma unroll
+        for (int h = kHorner - 2; h >= 0; --h) e = fma(e, v2, P.e[m][h]);
+        f(m, e);
+    }
+}
+
 __device__ __forceinline__ int wrap_base(int i, int n) {
     int r = i % n;
     return r < 0 ? r + n : r;

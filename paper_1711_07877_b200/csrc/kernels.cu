@@ -103,7 +103,7 @@ __global__ void k_tile_keys(const double2* __restrict__ pos, uint64_t n, double 
     const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (k >= n) return;
     const double2 p = pos[k];
-    const int bx = ((int)ceil(p.x - half) - tg.rlo) / kTileR;
+    const int bx = ((int)ceil(p.x - half) - tg.rlo) / tg.tr;
     const int by = ((int)ceil(p.y - half) - tg.clo) / kTileC;
     keys[k] = (uint32_t)bx * (uint32_t)tg.nby + (uint32_t)by;
 }
@@ -186,11 +186,11 @@ __global__ void __launch_bounds__(256) k_spread(WindowPoly P, GridGeom g, uint64
 // warp tile's first row: rows r in [max(0,D), min(kTileR, D+W)) get
 // acc[r] += (b wx)[r-D] * wy[lane]. D is a template parameter so the row range
 // is straight-line code; rows_dispatch picks it with a binary search on d.
-template <int W, int D>
+template <int W, int TR, int D>
 __device__ __forceinline__ void rows_acc(const double2* __restrict__ bwx, double wyl,
-                                         double (&ar)[kTileR], double (&ai)[kTileR]) {
+                                         double (&ar)[TR], double (&ai)[TR]) {
     constexpr int r0 = D > 0 ? D : 0;
-    constexpr int r1 = D + W < kTileR ? D + W : kTileR;
+    constexpr int r1 = D + W < TR ? D + W : TR;
 #pragma unroll
     for (int r = r0; r < r1; ++r) {
         const double2 v = bwx[r - D];
@@ -199,17 +199,17 @@ __device__ __forceinline__ void rows_acc(const double2* __restrict__ bwx, double
     }
 }
 
-template <int W, int Lo, int Hi>
+template <int W, int TR, int Lo, int Hi>
 __device__ __forceinline__ void rows_dispatch(int d, const double2* __restrict__ bwx, double wyl,
-                                              double (&ar)[kTileR], double (&ai)[kTileR]) {
+                                              double (&ar)[TR], double (&ai)[TR]) {
     if constexpr (Hi - Lo == 1) {
-        rows_acc<W, Lo>(bwx, wyl, ar, ai);
+        rows_acc<W, TR, Lo>(bwx, wyl, ar, ai);
     } else {
         constexpr int Mid = (Lo + Hi) / 2;
         if (d < Mid)
-            rows_dispatch<W, Lo, Mid>(d, bwx, wyl, ar, ai);
+            rows_dispatch<W, TR, Lo, Mid>(d, bwx, wyl, ar, ai);
         else
-            rows_dispatch<W, Mid, Hi>(d, bwx, wyl, ar, ai);
+            rows_dispatch<W, TR, Mid, Hi>(d, bwx, wyl, ar, ai);
     }
 }
 
@@ -222,13 +222,11 @@ __device__ __forceinline__ void rows_dispatch(int d, const double2* __restrict__
 // shared-memory slice), then accumulates acc[r] += (b wx)[row] * wy[lane]
 // point by point. Every cell of the tile is written exactly once: no atomics
 // and no zero-fill of the grid.
-template <int W>
-__global__ void __launch_bounds__(128) k_spread_tiles(WindowPoly P, GridGeom g, TileGeom tg,
+template <int W, int TR>
+__global__ void __launch_bounds__(128, TR == 16 ? 4 : 5) k_spread_tiles(WindowPoly P, GridGeom g, TileGeom tg,
                                                       const uint32_t* __restrict__ bin_start,
-                                                      const uint32_t* __restrict__ perm,
-                                                      const double2* __restrict__ in,
+                                                      const double2* __restrict__ bsorted,
                                                       const double2* __restrict__ pos,
-                                                      const double2* __restrict__ phase,
                                                       double2* __restrict__ grid) {
     extern __shared__ double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -241,10 +239,10 @@ __global__ void __launch_bounds__(128) k_spread_tiles(WindowPoly P, GridGeom g, 
     const int tile = blockIdx.x * 4 + warp;
     if (tile >= tg.nbx * tg.nby) return;
     const int bx = tile / tg.nby, by = tile - (tile / tg.nby) * tg.nby;
-    const int X0 = tg.rlo + bx * kTileR, Y0 = tg.clo + by * kTileC;
-    double ar[kTileR], ai[kTileR];
+    const int X0 = tg.rlo + bx * TR, Y0 = tg.clo + by * kTileC;
+    double ar[TR], ai[TR];
 #pragma unroll
-    for (int r = 0; r < kTileR; ++r) ar[r] = ai[r] = 0.0;
+    for (int r = 0; r < TR; ++r) ar[r] = ai[r] = 0.0;
 
     int queued = 0; // warp-uniform
     // Evaluate windows for the first n (<= 32) queued points and accumulate them.
@@ -253,24 +251,21 @@ __global__ void __launch_bounds__(128) k_spread_tiles(WindowPoly P, GridGeom g, 
             const uint32_t k = s_q[lane];
             const double2 t = pos[k];
             const int ix0 = (int)ceil(t.x - g.half), iy0 = (int)ceil(t.y - g.half);
-            const double2 b2 = cmul(in[perm ? perm[k] : k], phase[k]);
-            double wx[W], wy[W];
-            kb_taps<W>((ix0 - t.x) + g.half, P, wx);
-            kb_taps<W>((iy0 - t.y) + g.half, P, wy);
+            const double2 b2 = bsorted[k];
             s_ix[lane] = ix0 - X0;
             s_iy[lane] = iy0;
-#pragma unroll
-            for (int i = 0; i < W; ++i) {
-                s_bwx[lane * W + i] = make_double2(b2.x * wx[i], b2.y * wx[i]);
-                s_wy[lane * W + i] = wy[i];
-            }
+            double2* bw = s_bwx + lane * W;
+            double* wyp = s_wy + lane * W;
+            kb_taps_each<W>((ix0 - t.x) + g.half, P,
+                            [&](int i, double v) { bw[i] = make_double2(b2.x * v, b2.y * v); });
+            kb_taps_each<W>((iy0 - t.y) + g.half, P, [&](int i, double v) { wyp[i] = v; });
         }
         __syncwarp();
         for (int p = 0; p < n; ++p) {
             const int d = s_ix[p];
             const int jl = Y0 + lane - s_iy[p];
             const double wyl = (unsigned)jl < (unsigned)W ? s_wy[p * W + jl] : 0.0;
-            rows_dispatch<W, 1 - W, kTileR>(d, s_bwx + p * W, wyl, ar, ai);
+            rows_dispatch<W, TR, 1 - W, TR>(d, s_bwx + p * W, wyl, ar, ai);
         }
         __syncwarp();
     };
@@ -286,7 +281,7 @@ __global__ void __launch_bounds__(128) k_spread_tiles(WindowPoly P, GridGeom g, 
             if (k < s1) {
                 const double2 t = pos[k];
                 const int ix0 = (int)ceil(t.x - g.half), iy0 = (int)ceil(t.y - g.half);
-                take = ix0 < X0 + kTileR && ix0 + W > X0 && iy0 < Y0 + kTileC && iy0 + W > Y0;
+                take = ix0 < X0 + TR && ix0 + W > X0 && iy0 < Y0 + kTileC && iy0 + W > Y0;
             }
             const unsigned m = __ballot_sync(0xffffffffu, take);
             if (take) s_q[queued + __popc(m & ((1u << lane) - 1u))] = k;
@@ -304,7 +299,7 @@ __global__ void __launch_bounds__(128) k_spread_tiles(WindowPoly P, GridGeom g, 
     const int col = Y0 + lane;
     if (col < g.n2) {
 #pragma unroll
-        for (int r = 0; r < kTileR; ++r) {
+        for (int r = 0; r < TR; ++r) {
             const int row = X0 + r;
             if (row < g.n1) grid[(size_t)row * g.n2 + col] = make_double2(ar[r], ai[r]);
         }
@@ -322,6 +317,7 @@ __global__ void __launch_bounds__(256) k_interp(WindowPoly P, GridGeom g, uint64
                                                 const double* __restrict__ dyt,
                                                 const double2* __restrict__ grid,
                                                 const uint32_t* __restrict__ perm,
+                                                const double2* __restrict__ addend,
                                                 double2* __restrict__ out, int accumulate,
                                                 int conj_out) {
     const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -360,6 +356,11 @@ __global__ void __launch_bounds__(256) k_interp(WindowPoly P, GridGeom g, uint64
     double2 o = cmul(make_double2(ar, ai), phase[v]);
     if (mult) o = cmul(o, mult[v]);
     if (conj_out) o.y = -o.y;
+    if (addend) {
+        const double2 a = addend[v];
+        o.x += a.x;
+        o.y += a.y;
+    }
     const uint64_t dst = perm ? perm[v] : v;
     if (accumulate) {
         double2 q = out[dst];
@@ -390,6 +391,48 @@ __global__ void k_ndft(const double2* __restrict__ pts, uint64_t np,
         ai = __dadd_rn(ai, __dadd_rn(__dmul_rn(ck.x, sn), __dmul_rn(ck.y, cs)));
     }
     out[v] = make_double2(ar, ai);
+}
+
+// b[k] = in[perm[k]] * phase[k]; raw[k] = in[perm[k]] (optional): the spread
+// coefficients (nufft.cpp:233) and the sorted copy of f for the CSR pass.
+__global__ void k_gather_mul(const double2* __restrict__ in, const uint32_t* __restrict__ perm,
+                             const double2* __restrict__ phase, double2* __restrict__ b,
+                             double2* __restrict__ raw, uint64_t n) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double2 c = in[perm ? perm[k] : k];
+    b[k] = cmul(c, phase[k]);
+    if (raw) raw[k] = c;
+}
+
+// qs[r] = sum_{i in row r} D'_i f'_{col'_i} (point_cloud.cpp:116-123 on the
+// renumbered matrix); 8 lanes per row, coalesced over the row's entries.
+__global__ void __launch_bounds__(256) k_spmv_vec(uint64_t rows, const uint64_t* __restrict__ ro,
+                                                  const uint32_t* __restrict__ cols,
+                                                  const double2* __restrict__ vals,
+                                                  const double2* __restrict__ f,
+                                                  double2* __restrict__ qs) {
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t r = g >> 3;
+    const int sub = (int)(g & 7);
+    double ar = 0.0, ai = 0.0;
+    if (r < rows) {
+        const uint64_t e = ro[r + 1];
+        for (uint64_t i = ro[r] + sub; i < e; i += 8) {
+            const double2 v = vals[i];
+            const double2 x = f[cols[i]];
+            ar = fma(v.x, x.x, ar);
+            ar = fma(-v.y, x.y, ar);
+            ai = fma(v.x, x.y, ai);
+            ai = fma(v.y, x.x, ai);
+        }
+    }
+#pragma unroll
+    for (int o = 4; o; o >>= 1) {
+        ar += __shfl_xor_sync(0xffffffffu, ar, o);
+        ai += __shfl_xor_sync(0xffffffffu, ai, o);
+    }
+    if (r < rows && sub == 0) qs[r] = make_double2(ar, ai);
 }
 
 __global__ void k_mul(double2* x, const double2* __restrict__ m, uint64_t n) {
@@ -467,18 +510,22 @@ template <int W>
 struct SpreadTilesRun {
     static size_t smem() { return (size_t)4 * 32 * W * 24 + 4 * 128 * sizeof(uint32_t); }
     static void run(const WindowPoly& P, GridGeom g, TileGeom tg, const uint32_t* bs,
-                    const uint32_t* perm, const double2* in, const double2* pos,
-                    const double2* phase, double2* grid, cudaStream_t st) {
+                    const double2* b, const double2* pos, double2* grid, cudaStream_t st) {
         static bool attr = false;
         if (!attr) {
-            ck(cudaFuncSetAttribute(k_spread_tiles<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            ck(cudaFuncSetAttribute(k_spread_tiles<W, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem()),
+               "smem attr");
+            ck(cudaFuncSetAttribute(k_spread_tiles<W, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem()),
                "smem attr");
             attr = true;
         }
         const int tiles = tg.nbx * tg.nby;
-        k_spread_tiles<W><<<(tiles + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, perm, in, pos, phase,
-                                                                grid);
+        if (tg.tr == 8)
+            k_spread_tiles<W, 8><<<(tiles + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid);
+        else
+            k_spread_tiles<W, 16><<<(tiles + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid);
     }
 };
 
@@ -486,10 +533,10 @@ template <int W>
 struct InterpRun {
     static void run(const WindowPoly& P, GridGeom g, uint64_t n, const double2* pos,
                     const double2* phase, const double2* mult, const double* dx, const double* dy,
-                    const double2* grid, const uint32_t* perm, double2* out, int acc, int cj,
-                    cudaStream_t st) {
+                    const double2* grid, const uint32_t* perm, const double2* addend, double2* out,
+                    int acc, int cj, cudaStream_t st) {
         k_interp<W><<<blocks(n, 256), 256, 0, st>>>(P, g, n, pos, phase, mult, dx, dy, grid, perm,
-                                                    out, acc, cj);
+                                                    addend, out, acc, cj);
     }
 };
 
@@ -548,10 +595,10 @@ void launch_bin_bounds(const uint32_t* sorted_keys, uint64_t n, uint32_t nbins, 
 }
 
 void launch_spread_tiles(int w, const WindowPoly& win, GridGeom g, TileGeom tg,
-                         const uint32_t* bin_start, const uint32_t* perm, const double2* in,
-                         const double2* pos, const double2* phase, double2* grid, cudaStream_t st) {
+                         const uint32_t* bin_start, const double2* b, const double2* pos,
+                         double2* grid, cudaStream_t st) {
     if (tg.nbx * tg.nby == 0) return;
-    dispatch_w<SpreadTilesRun>(w, win, g, tg, bin_start, perm, in, pos, phase, grid, st);
+    dispatch_w<SpreadTilesRun>(w, win, g, tg, bin_start, b, pos, grid, st);
     count_launch();
     ck(cudaGetLastError(), "k_spread_tiles");
 }
@@ -601,10 +648,10 @@ void launch_spread(int w, const WindowPoly& win, GridGeom g, uint64_t n, const u
 void launch_interp(int w, const WindowPoly& win, GridGeom g, uint64_t n, const double2* pos,
                    const double2* phase, const double2* mult, const double* dx, const double* dy,
                    const double2* grid, const uint32_t* perm, double2* out, int accumulate,
-                   int conj_out, cudaStream_t st) {
+                   int conj_out, cudaStream_t st, const double2* addend) {
     if (!n) return;
-    dispatch_w<InterpRun>(w, win, g, n, pos, phase, mult, dx, dy, grid, perm, out, accumulate,
-                          conj_out, st);
+    dispatch_w<InterpRun>(w, win, g, n, pos, phase, mult, dx, dy, grid, perm, addend, out,
+                          accumulate, conj_out, st);
     count_launch();
     ck(cudaGetLastError(), "k_interp");
 }
@@ -615,6 +662,22 @@ void launch_ndft(const double2* pts, uint64_t np, const double2* frq, uint64_t n
     k_ndft<<<blocks(nf, 128), 128, 0, st>>>(pts, np, frq, nf, c, sign > 0 ? 1.0 : -1.0, out);
     count_launch();
     ck(cudaGetLastError(), "k_ndft");
+}
+
+void launch_gather_mul(const double2* in, const uint32_t* perm, const double2* phase, double2* b,
+                       double2* raw, uint64_t n, cudaStream_t st) {
+    if (!n) return;
+    k_gather_mul<<<blocks(n, 256), 256, 0, st>>>(in, perm, phase, b, raw, n);
+    count_launch();
+    ck(cudaGetLastError(), "k_gather_mul");
+}
+
+void launch_spmv_vec(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double2* vals,
+                     const double2* f, double2* qs, cudaStream_t st) {
+    if (!rows) return;
+    k_spmv_vec<<<blocks(rows * 8, 256), 256, 0, st>>>(rows, ro, cols, vals, f, qs);
+    count_launch();
+    ck(cudaGetLastError(), "k_spmv_vec");
 }
 
 void launch_mul(double2* x, const double2* m, uint64_t n, cudaStream_t st) {

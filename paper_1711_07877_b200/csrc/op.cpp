@@ -10,6 +10,7 @@
 //   each plan carries its own tile permutation internally.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -179,6 +180,15 @@ struct sbd_op {
     FftWork work;
     DevBuf<double2> spec;
     DevBuf<double2> hf, hq; // staging for the host-buffer API
+    // Fused forward path (both plans gridded): D renumbered to (sorted target
+    // row, sorted source column) so its f gathers are spatially local, and
+    // kappa = omega-hat * fwd_out prephase so the xi interpolation emits the
+    // xi spread's coefficients directly.
+    bool fused = false;
+    DevBuf<uint64_t> ro_s;
+    DevBuf<uint32_t> cols_s;
+    DevBuf<double2> vals_s;
+    DevBuf<double2> kappa, f_sorted, qs;
     StageTimer tm;
     std::mutex mu;
 
@@ -220,10 +230,60 @@ struct sbd_op {
         fwd_out->ensure_work(work, stream);
         spec.alloc(std::max<uint64_t>(d.n_xi(), 1));
         ck(cudaStreamSynchronize(stream), "operator upload");
+        build_fused();
+    }
+
+    void build_fused() {
+        fused = fwd_in->pruned && fwd_out->pruned && fwd_in->perm_t.n == d.n_src() &&
+                fwd_out->perm_s.n == d.n_tgt() && getenv("SBD_NO_FUSED") == nullptr;
+        if (!fused) return;
+        const uint64_t ns = d.n_src(), nt = d.n_tgt(), nx = d.n_xi();
+        // kappa = w_sorted * pre_out (conv_operator.cpp:305 then nufft.cpp:233)
+        kappa.alloc(nx);
+        ck(cudaMemcpyAsync(kappa.p, w_sorted.p, nx * 16, cudaMemcpyDeviceToDevice, stream), "kappa");
+        launch_mul(kappa.p, fwd_out->pre.p, nx, stream);
+        f_sorted.alloc(ns);
+        qs.alloc(nt);
+        // D' rows in target-sorted order, columns renumbered to source-sorted positions
+        std::vector<uint32_t> ps(ns), pt(nt), inv(ns);
+        ck(cudaMemcpyAsync(ps.data(), fwd_in->perm_t.p, ns * 4, cudaMemcpyDeviceToHost, stream), "perm");
+        ck(cudaMemcpyAsync(pt.data(), fwd_out->perm_s.p, nt * 4, cudaMemcpyDeviceToHost, stream), "perm");
+        ck(cudaStreamSynchronize(stream), "perm");
+        for (uint64_t i = 0; i < ns; ++i) inv[ps[i]] = (uint32_t)i;
+        std::vector<uint64_t> ro2(nt + 1, 0);
+        for (uint64_t r = 0; r < nt; ++r) ro2[r + 1] = ro2[r] + (d.row_offsets[pt[r] + 1] - d.row_offsets[pt[r]]);
+        std::vector<uint32_t> c2(d.nnz());
+        std::vector<double> v2(2 * d.nnz());
+#pragma omp parallel for schedule(static, 4096)
+        for (int64_t r = 0; r < (int64_t)nt; ++r) {
+            const uint64_t a = d.row_offsets[pt[r]], b = d.row_offsets[pt[r] + 1];
+            uint64_t o = ro2[r];
+            for (uint64_t i = a; i < b; ++i, ++o) {
+                c2[o] = inv[d.cols[i]];
+                v2[2 * o] = d.values[2 * i];
+                v2[2 * o + 1] = d.values[2 * i + 1];
+            }
+        }
+        ro_s.upload(ro2.data(), nt + 1, stream);
+        cols_s.upload(c2.data(), c2.size(), stream);
+        vals_s.upload(reinterpret_cast<const double2*>(v2.data()), d.nnz(), stream);
+        ck(cudaStreamSynchronize(stream), "fused upload");
     }
 
     // conv_operator.cpp:301-309 on device buffers, one right-hand side.
     void apply_one(const double2* f, double2* q, cudaStream_t st) {
+        if (fused) {
+            // spectrum_b = NUFFT-(f) * w * pre_out, with f_sorted kept for the CSR pass
+            fwd_in->apply_pruned(f, false, f_sorted.p, spec.p, kappa.p, nullptr, work, st, &tm,
+                                 "spread_src", "fft_in", "interp_xi");
+            if (tm.on) tm.start("spmv");
+            launch_spmv_vec(d.n_tgt(), ro_s.p, cols_s.p, vals_s.p, f_sorted.p, qs.p, st);
+            if (tm.on) tm.stop();
+            // q = NUFFT+(spectrum) + D f, scattered to the caller's target order
+            fwd_out->apply_pruned(spec.p, true, nullptr, q, nullptr, qs.p, work, st, &tm, "spread_xi",
+                                  "fft_out", "interp_tgt");
+            return;
+        }
         fwd_in->apply(f, spec.p, work, st, &tm, w_sorted.p, "spread_src", "fft_in", "interp_xi");
         fwd_out->apply(spec.p, q, work, st, &tm, nullptr, "spread_xi", "fft_out", "interp_tgt");
         if (tm.on) tm.start("spmv");
@@ -242,6 +302,8 @@ struct sbd_op {
 
     size_t device_bytes() const {
         return fwd_in->device_bytes() + fwd_out->device_bytes() + w_sorted.bytes() + ro.bytes() +
+               ro_s.bytes() + cols_s.bytes() + vals_s.bytes() + kappa.bytes() + f_sorted.bytes() +
+               qs.bytes() + work.bbuf.bytes() +
                cols.bytes() + vals.bytes() + work.grid.bytes() + work.T.bytes() + work.band.bytes() +
                spec.bytes() + hf.bytes() + hq.bytes();
     }

@@ -9,6 +9,7 @@
 // tile for locality.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "sbd_internal.h"
@@ -109,13 +110,15 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
         pruned = sort_points && np > 0 && he[0] >= 0 && he[1] + w <= ax.n && he[2] >= 0 &&
                  he[3] + w <= ay.n;
         if (pruned) {
+            const char* env = std::getenv("SBD_TILE_ROWS");
+            tg.tr = (env && std::atoi(env) == 8) ? 8 : 16;
             tg.rlo = he[0];
             tg.clo = he[2];
-            tg.nbx = (he[1] + w - he[0] + kTileR - 1) / kTileR;
+            tg.nbx = (he[1] + w - he[0] + tg.tr - 1) / tg.tr;
             tg.nby = (he[3] + w - he[2] + kTileC - 1) / kTileC;
             rlo = tg.rlo;
             clo = tg.clo;
-            rhi = std::min(ax.n, tg.rlo + tg.nbx * kTileR);
+            rhi = std::min(ax.n, tg.rlo + tg.nbx * tg.tr);
             chi = std::min(ay.n, tg.clo + tg.nby * kTileC);
         }
     }
@@ -248,45 +251,7 @@ void Plan::apply(const double2* in, double2* out, FftWork& wk, cudaStream_t st, 
     const GridGeom g{ax.n, ay.n, 0.5 * w};
     const int n2 = ay.n;
     if (pruned) {
-        if (tm) tm->start(tag_spread);
-        if (wk.g_pitch == n2)
-            zero_rect_minus(wk.grid.p, n2, wk.gr0, wk.gr1, wk.gc0, wk.gc1, rlo, rhi, clo, chi, st);
-        else if (wk.g_pitch)  // written by a plan of another grid size: clear all of it
-            zero_rect_minus(wk.grid.p, wk.g_pitch, wk.gr0, wk.gr1, wk.gc0, wk.gc1, 0, 0, 0, 0, st);
-        launch_spread_tiles(w, win, g, tg, bin_start.p, perm_t.n ? perm_t.p : nullptr, in, t.p, pre.p,
-                            wk.grid.p, st);
-        wk.gr0 = rlo;
-        wk.gr1 = rhi;
-        wk.gc0 = clo;
-        wk.gc1 = chi;
-        wk.g_pitch = n2;
-        if (tm) tm->stop();
-        if (tm) tm->start(tag_fft);
-        // rows [rlo, rhi): grid -> T (out of place; T rows elsewhere stay zero)
-        if (wk.t_pitch == n2)
-            zero_rect_minus(wk.T.p, n2, wk.tr0, wk.tr1, 0, n2, rlo, rhi, 0, n2, st);
-        else if (wk.t_pitch)
-            zero_rect_minus(wk.T.p, wk.t_pitch, wk.tr0, wk.tr1, 0, wk.t_pitch, 0, 0, 0, 0, st);
-        auto* G = reinterpret_cast<cufftDoubleComplex*>(wk.grid.p);
-        auto* T = reinterpret_cast<cufftDoubleComplex*>(wk.T.p);
-        auto* B = reinterpret_cast<cufftDoubleComplex*>(wk.band.p);
-        ckfft(cufftSetStream(fft_row, st), "cufftSetStream");
-        ckfft(cufftExecZ2Z(fft_row, G + (size_t)rlo * n2, T + (size_t)rlo * n2, CUFFT_INVERSE), "fft rows");
-        wk.tr0 = rlo;
-        wk.tr1 = rhi;
-        wk.t_pitch = n2;
-        // band columns of T -> band buffer (n1 x bc, columns in mode order mod bc)
-        ckfft(cufftSetStream(fft_colA, st), "cufftSetStream");
-        ckfft(cufftExecZ2Z(fft_colA, T, B, CUFFT_INVERSE), "fft cols A");
-        ckfft(cufftSetStream(fft_colB, st), "cufftSetStream");
-        ckfft(cufftExecZ2Z(fft_colB, T + (n2 - band2), B + (band2 + 1), CUFFT_INVERSE), "fft cols B");
-        count_launch(3);
-        if (tm) tm->stop();
-        if (tm) tm->start(tag_interp);
-        const GridGeom gb{ax.n, bc, 0.5 * w};
-        launch_interp(w, win, gb, nf, s.p, post.p, mult, dx.p, dy_band.p, wk.band.p,
-                      perm_s.n ? perm_s.p : nullptr, out, 0, 0, st);
-        if (tm) tm->stop();
+        apply_pruned(in, false, nullptr, out, mult, nullptr, wk, st, tm, tag_spread, tag_fft, tag_interp);
         return;
     }
     if (tm) tm->start(tag_spread);
@@ -306,6 +271,60 @@ void Plan::apply(const double2* in, double2* out, FftWork& wk, cudaStream_t st, 
     wk.gc0 = 0;
     wk.gc1 = ay.n;
     wk.g_pitch = ay.n;
+}
+
+void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, double2* out,
+                        const double2* mult, const double2* addend, FftWork& wk, cudaStream_t st,
+                        StageTimer* tm, const char* tag_spread, const char* tag_fft,
+                        const char* tag_interp) const {
+    if (!pruned) throw Error(3, "apply_pruned on a plan without the pruned path");
+    ensure_work(wk, st);
+    const GridGeom g{ax.n, ay.n, 0.5 * w};
+    const int n2 = ay.n;
+    if (tm) tm->start(tag_spread);
+    const double2* b = in;
+    if (!in_is_b) {
+        if (wk.bbuf.n < np) wk.bbuf.alloc(np);
+        launch_gather_mul(in, perm_t.n ? perm_t.p : nullptr, pre.p, wk.bbuf.p, raw_sorted, np, st);
+        b = wk.bbuf.p;
+    }
+    if (wk.g_pitch == n2)
+        zero_rect_minus(wk.grid.p, n2, wk.gr0, wk.gr1, wk.gc0, wk.gc1, rlo, rhi, clo, chi, st);
+    else if (wk.g_pitch)  // written by a plan of another grid size: clear all of it
+        zero_rect_minus(wk.grid.p, wk.g_pitch, wk.gr0, wk.gr1, wk.gc0, wk.gc1, 0, 0, 0, 0, st);
+    launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, wk.grid.p, st);
+    wk.gr0 = rlo;
+    wk.gr1 = rhi;
+    wk.gc0 = clo;
+    wk.gc1 = chi;
+    wk.g_pitch = n2;
+    if (tm) tm->stop();
+    if (tm) tm->start(tag_fft);
+    // rows [rlo, rhi): grid -> T (out of place; T rows elsewhere stay zero)
+    if (wk.t_pitch == n2)
+        zero_rect_minus(wk.T.p, n2, wk.tr0, wk.tr1, 0, n2, rlo, rhi, 0, n2, st);
+    else if (wk.t_pitch)
+        zero_rect_minus(wk.T.p, wk.t_pitch, wk.tr0, wk.tr1, 0, wk.t_pitch, 0, 0, 0, 0, st);
+    auto* G = reinterpret_cast<cufftDoubleComplex*>(wk.grid.p);
+    auto* T = reinterpret_cast<cufftDoubleComplex*>(wk.T.p);
+    auto* B = reinterpret_cast<cufftDoubleComplex*>(wk.band.p);
+    ckfft(cufftSetStream(fft_row, st), "cufftSetStream");
+    ckfft(cufftExecZ2Z(fft_row, G + (size_t)rlo * n2, T + (size_t)rlo * n2, CUFFT_INVERSE), "fft rows");
+    wk.tr0 = rlo;
+    wk.tr1 = rhi;
+    wk.t_pitch = n2;
+    // band columns of T -> band buffer (n1 x bc, columns in mode order mod bc)
+    ckfft(cufftSetStream(fft_colA, st), "cufftSetStream");
+    ckfft(cufftExecZ2Z(fft_colA, T, B, CUFFT_INVERSE), "fft cols A");
+    ckfft(cufftSetStream(fft_colB, st), "cufftSetStream");
+    ckfft(cufftExecZ2Z(fft_colB, T + (n2 - band2), B + (band2 + 1), CUFFT_INVERSE), "fft cols B");
+    count_launch(3);
+    if (tm) tm->stop();
+    if (tm) tm->start(tag_interp);
+    const GridGeom gb{ax.n, bc, 0.5 * w};
+    launch_interp(w, win, gb, nf, s.p, post.p, mult, dx.p, dy_band.p, wk.band.p,
+                  perm_s.n ? perm_s.p : nullptr, out, 0, 0, st, addend);
+    if (tm) tm->stop();
 }
 
 // nufft.cpp:295-367

@@ -120,6 +120,7 @@ struct StageTimer {
 // dirty rectangles", so no full-grid memset is needed per apply.
 struct FftWork {
     DevBuf<double2> grid, T, band;
+    DevBuf<double2> bbuf; // spread coefficients b = c * prephase, sorted point order
     int n1 = 0, n2 = 0, bc = 0;
     int gr0 = 0, gr1 = 0, gc0 = 0, gc1 = 0; // grid cells possibly nonzero ...
     int g_pitch = 0;                        // ... in a row-major layout of this pitch
@@ -134,6 +135,7 @@ constexpr int kTileR = 16;
 constexpr int kTileC = 32;
 struct TileGeom {
     int rlo, clo, nbx, nby;
+    int tr; // rows per tile (8 or 16)
 };
 
 // A type-III NUFFT plan on one device (reference NufftPlan, nufft.hpp:30-56).
@@ -188,6 +190,15 @@ class Plan {
     void apply(const double2* in, double2* out, FftWork& wk, cudaStream_t st,
                StageTimer* tm, const double2* mult = nullptr, const char* tag_spread = "spread",
                const char* tag_fft = "fft", const char* tag_interp = "interp") const;
+    // Pruned forward path with the operator's fused inputs/outputs:
+    //  in_is_b: `in` already holds b = c * prephase in this plan's sorted point
+    //           order (else b is formed from caller-order `in`, and the sorted
+    //           copy of `in` is written to raw_sorted when given);
+    //  addend:  per sorted output, added after mult before the scatter.
+    void apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, double2* out,
+                      const double2* mult, const double2* addend, FftWork& wk, cudaStream_t st,
+                      StageTimer* tm, const char* tag_spread, const char* tag_fft,
+                      const char* tag_interp) const;
     void apply_transpose(const double2* in, double2* out, FftWork& wk, cudaStream_t st,
                          StageTimer* tm, const double2* mult = nullptr, int conj_in = 0,
                          int conj_out = 0) const;
@@ -223,8 +234,12 @@ void launch_bin_bounds(const uint32_t* sorted_keys, uint64_t n, uint32_t nbins, 
                        cudaStream_t st);
 // Tile-owned spread: writes every cell of the tiles (no atomics, no memset).
 void launch_spread_tiles(int w, const WindowPoly& win, GridGeom g, TileGeom tg,
-                         const uint32_t* bin_start, const uint32_t* perm, const double2* in,
-                         const double2* pos, const double2* phase, double2* grid, cudaStream_t st);
+                         const uint32_t* bin_start, const double2* b, const double2* pos,
+                         double2* grid, cudaStream_t st);
+void launch_gather_mul(const double2* in, const uint32_t* perm, const double2* phase, double2* b,
+                       double2* raw, uint64_t n, cudaStream_t st);
+void launch_spmv_vec(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double2* vals,
+                     const double2* f, double2* qs, cudaStream_t st);
 void sort_by_key(uint32_t* keys, uint32_t* vals, uint64_t n, cudaStream_t st);
 void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st);
 template <typename T>
@@ -240,7 +255,7 @@ void launch_spread(int w, const WindowPoly& win, GridGeom g, uint64_t n, const u
 void launch_interp(int w, const WindowPoly& win, GridGeom g, uint64_t n, const double2* pos,
                    const double2* phase, const double2* mult, const double* dx, const double* dy,
                    const double2* grid, const uint32_t* perm, double2* out, int accumulate,
-                   int conj_out, cudaStream_t st);
+                   int conj_out, cudaStream_t st, const double2* addend = nullptr);
 // direct sum out[v] = sum_k c_k e^{i sign z_k . f_v}
 void launch_ndft(const double2* pts, uint64_t np, const double2* frq, uint64_t nf,
                  const double2* c, int sign, double2* out, cudaStream_t st);
