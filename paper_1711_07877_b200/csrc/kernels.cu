@@ -12,6 +12,7 @@
 #include <cub/cub.cuh>
 
 #include <climits>
+#include <cstdlib>
 
 #include "device_common.cuh"
 #include "sbd_internal.h"
@@ -98,14 +99,18 @@ __global__ void k_stencil_extent(const double2* __restrict__ pos, uint64_t n, do
     }
 }
 
+// key = tile index << 5 | 4x4 sub-tile index (kTileR = 16, kTileC = 32): points
+// consecutive in the sorted order are within a few cells of each other, which
+// is what makes 4-point MMA groups compact in the DMMA spread.
 __global__ void k_tile_keys(const double2* __restrict__ pos, uint64_t n, double half, TileGeom tg,
                             uint32_t* __restrict__ keys) {
     const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (k >= n) return;
     const double2 p = pos[k];
-    const int bx = ((int)ceil(p.x - half) - tg.rlo) / tg.tr;
-    const int by = ((int)ceil(p.y - half) - tg.clo) / kTileC;
-    keys[k] = (uint32_t)bx * (uint32_t)tg.nby + (uint32_t)by;
+    const int rx = (int)ceil(p.x - half) - tg.rlo, ry = (int)ceil(p.y - half) - tg.clo;
+    const int bx = rx / tg.tr, by = ry / kTileC;
+    const int sub = ((rx % tg.tr) >> 2) * (kTileC >> 2) + ((ry % kTileC) >> 2);
+    keys[k] = (((uint32_t)bx * (uint32_t)tg.nby + (uint32_t)by) << 5) | (uint32_t)(sub & 31);
 }
 
 // start[b] = first sorted position with key >= b, for b in [0, nbins]
@@ -113,8 +118,8 @@ __global__ void k_bin_bounds(const uint32_t* __restrict__ key, uint64_t n, uint3
                              uint32_t* __restrict__ start) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i > n) return;
-    const int64_t prev = i > 0 ? (int64_t)key[i - 1] : -1;
-    const int64_t cur = i < n ? (int64_t)key[i] : (int64_t)nbins;
+    const int64_t prev = i > 0 ? (int64_t)(key[i - 1] >> 5) : -1;
+    const int64_t cur = i < n ? (int64_t)(key[i] >> 5) : (int64_t)nbins;
     for (int64_t b = prev + 1; b <= cur; ++b) start[b] = (uint32_t)i;
 }
 
@@ -302,6 +307,150 @@ __global__ void __launch_bounds__(128, TR == 16 ? 4 : 5) k_spread_tiles(WindowPo
         for (int r = 0; r < TR; ++r) {
             const int row = X0 + r;
             if (row < g.n1) grid[(size_t)row * g.n2 + col] = make_double2(ar[r], ai[r]);
+        }
+    }
+}
+
+// fp64 tensor-core MMA: D(8x8) = A(8x4) B(4x8) + C (mma.sync m8n8k4 f64; SASS
+// DMMA.8x8x4). Fragments: a = A[lane/4][lane%4], b = B[lane%4][lane/4],
+// c = {C[lane/4][2(lane%4)], C[lane/4][2(lane%4)+1]}.
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// Spread on the fp64 tensor cores. Same tile ownership as k_spread_tiles (one
+// warp owns 16 x 32 cells, every cell written once), but the accumulation is
+// a sequence of 8x8x4 MMAs: for a group of 4 staged points,
+//   G[8 rows x 8 cols] += A[8 rows x 4 pts] B[4 pts x 8 cols],
+//   A[r][k] = (b_k wx_k)(row r) (real and imaginary parts: two MMAs),
+//   B[k][c] = wy_k(col c),
+// issued only for the 8x8 sub-tiles the group's stencils touch. One DMMA does
+// 256 multiply-adds, which removes the instruction-issue bound of the scalar
+// version; points are sorted by 4x4 sub-tile so a group's footprint is small.
+template <int W>
+__global__ void __launch_bounds__(128) k_spread_mma(WindowPoly P, GridGeom g, TileGeom tg,
+                                                    const uint32_t* __restrict__ bin_start,
+                                                    const double2* __restrict__ bsorted,
+                                                    const double2* __restrict__ pos,
+                                                    double2* __restrict__ grid) {
+    constexpr int TR = 16;
+    extern __shared__ double smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double2* s_bwx = reinterpret_cast<double2*>(smem) + warp * 32 * W;
+    double* s_wy = smem + 4 * 64 * W + warp * 32 * W;
+    uint32_t* s_q = reinterpret_cast<uint32_t*>(smem + 4 * 96 * W) + warp * 128;
+    int* s_ix = reinterpret_cast<int*>(s_q + 64);
+    int* s_iy = s_ix + 32;
+    const int tile = blockIdx.x * 4 + warp;
+    if (tile >= tg.nbx * tg.nby) return;
+    const int bx = tile / tg.nby, by = tile - (tile / tg.nby) * tg.nby;
+    const int X0 = tg.rlo + bx * TR, Y0 = tg.clo + by * kTileC;
+    const int gid = lane >> 2, kq = lane & 3;
+    double cr[2][4][2], ci[2][4][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+
+    int queued = 0;
+    auto flush = [&](int n) {
+        if (lane < n) {
+            const uint32_t k = s_q[lane];
+            const double2 t = pos[k];
+            const int ix0 = (int)ceil(t.x - g.half), iy0 = (int)ceil(t.y - g.half);
+            const double2 b2 = bsorted[k];
+            s_ix[lane] = ix0 - X0;
+            s_iy[lane] = iy0 - Y0;
+            double2* bw = s_bwx + lane * W;
+            double* wyp = s_wy + lane * W;
+            kb_taps_each<W>((ix0 - t.x) + g.half, P,
+                            [&](int i, double v) { bw[i] = make_double2(b2.x * v, b2.y * v); });
+            kb_taps_each<W>((iy0 - t.y) + g.half, P, [&](int i, double v) { wyp[i] = v; });
+        } else {
+            s_ix[lane] = -4 * W; // out of every tile: zero fragments
+            s_iy[lane] = -4 * W;
+        }
+        __syncwarp();
+        for (int grp = 0; grp < n; grp += 4) {
+            const int node = grp + kq;
+            const int dx = s_ix[node], dy = s_iy[node];
+            const bool real = node < n;
+            // warp-uniform footprint of the group
+            int rmin = real ? dx : 1 << 20, rmax = real ? dx + W : -(1 << 20);
+            int cmin = real ? dy : 1 << 20, cmax = real ? dy + W : -(1 << 20);
+#pragma unroll
+            for (int o = 1; o <= 2; o <<= 1) {
+                rmin = min(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
+                rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+                cmin = min(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+                cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+            }
+            double ar[2], ai[2], bb[4];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int idx = 8 * i + gid - dx;
+                const double2 v = (real && (unsigned)idx < (unsigned)W) ? s_bwx[node * W + idx]
+                                                                        : make_double2(0.0, 0.0);
+                ar[i] = v.x;
+                ai[i] = v.y;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int idx = 8 * j + gid - dy;
+                bb[j] = (real && (unsigned)idx < (unsigned)W) ? s_wy[node * W + idx] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                if (rmax <= 8 * i || rmin >= 8 * i + 8) continue;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (cmax <= 8 * j || cmin >= 8 * j + 8) continue;
+                    dmma(cr[i][j][0], cr[i][j][1], ar[i], bb[j]);
+                    dmma(ci[i][j][0], ci[i][j][1], ai[i], bb[j]);
+                }
+            }
+        }
+        __syncwarp();
+    };
+
+    for (int q = 0; q < 4; ++q) {
+        const int cbx = bx - (q >> 1), cby = by - (q & 1);
+        if (cbx < 0 || cby < 0) continue;
+        const int b = cbx * tg.nby + cby;
+        const uint32_t s0 = bin_start[b], s1 = bin_start[b + 1];
+        for (uint32_t s = s0; s < s1; s += 32) {
+            const uint32_t k = s + lane;
+            bool take = false;
+            if (k < s1) {
+                const double2 t = pos[k];
+                const int ix0 = (int)ceil(t.x - g.half), iy0 = (int)ceil(t.y - g.half);
+                take = ix0 < X0 + TR && ix0 + W > X0 && iy0 < Y0 + kTileC && iy0 + W > Y0;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, take);
+            if (take) s_q[queued + __popc(m & ((1u << lane) - 1u))] = k;
+            queued += __popc(m);
+            __syncwarp();
+            if (queued >= 32) {
+                flush(32);
+                if (lane < queued - 32) s_q[lane] = s_q[32 + lane];
+                queued -= 32;
+                __syncwarp();
+            }
+        }
+    }
+    if (queued) flush(queued);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int row = X0 + 8 * i + gid;
+        if (row >= g.n1) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int col = Y0 + 8 * j + 2 * kq;
+            double2* dst = grid + (size_t)row * g.n2 + col;
+            if (col < g.n2) dst[0] = make_double2(cr[i][j][0], ci[i][j][0]);
+            if (col + 1 < g.n2) dst[1] = make_double2(cr[i][j][1], ci[i][j][1]);
         }
     }
 }
@@ -522,7 +671,17 @@ struct SpreadTilesRun {
             attr = true;
         }
         const int tiles = tg.nbx * tg.nby;
-        if (tg.tr == 8)
+        static int use_mma = -1;
+        if (use_mma < 0) {
+            const char* e = getenv("SBD_SPREAD");
+            use_mma = !(e && e[0] == 's');
+            ck(cudaFuncSetAttribute(k_spread_mma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem()),
+               "smem attr");
+        }
+        if (use_mma && tg.tr == 16)
+            k_spread_mma<W><<<(tiles + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid);
+        else if (tg.tr == 8)
             k_spread_tiles<W, 8><<<(tiles + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid);
         else
             k_spread_tiles<W, 16><<<(tiles + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid);
