@@ -78,6 +78,12 @@ __device__ __forceinline__ void kb_taps_each(double u, const WindowPoly& P, F&& 
     }
 }
 
+// i mod n for i in [-n, 2n) without an integer division.
+__device__ __forceinline__ int wrap_near(int i, int n) {
+    i = i < 0 ? i + n : i;
+    return i >= n ? i - n : i;
+}
+
 __device__ __forceinline__ int wrap_base(int i, int n) {
     int r = i % n;
     return r < 0 ? r + n : r;

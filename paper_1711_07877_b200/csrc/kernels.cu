@@ -354,62 +354,58 @@ __global__ void __launch_bounds__(128) k_spread_mma(WindowPoly P, GridGeom g, Ti
 #pragma unroll
         for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
 
+    // 8 tiles x 32 list entries per warp, after all four warps' queues
+    uint32_t* s_list = reinterpret_cast<uint32_t*>(smem + 4 * 96 * W) + 4 * 128 + warp * 256;
     int queued = 0;
+    // Evaluate the windows of the first n queued points (lane = point), build
+    // per-8x8-tile lists of the points whose stencil reaches that tile, and
+    // feed each tile's list to the tensor cores 4 points at a time.
     auto flush = [&](int n) {
+        int dx = -4 * W, dy = -4 * W;
         if (lane < n) {
             const uint32_t k = s_q[lane];
             const double2 t = pos[k];
             const int ix0 = (int)ceil(t.x - g.half), iy0 = (int)ceil(t.y - g.half);
             const double2 b2 = bsorted[k];
-            s_ix[lane] = ix0 - X0;
-            s_iy[lane] = iy0 - Y0;
+            dx = ix0 - X0;
+            dy = iy0 - Y0;
             double2* bw = s_bwx + lane * W;
             double* wyp = s_wy + lane * W;
             kb_taps_each<W>((ix0 - t.x) + g.half, P,
                             [&](int i, double v) { bw[i] = make_double2(b2.x * v, b2.y * v); });
             kb_taps_each<W>((iy0 - t.y) + g.half, P, [&](int i, double v) { wyp[i] = v; });
-        } else {
-            s_ix[lane] = -4 * W; // out of every tile: zero fragments
-            s_iy[lane] = -4 * W;
+        }
+        const uint32_t packed = (uint32_t)lane | ((uint32_t)(dx + 64) << 8) | ((uint32_t)(dy + 64) << 16);
+        int cnt[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const int i = t >> 2, j = t & 3;
+            const bool hit = dx < 8 * i + 8 && dx + W > 8 * i && dy < 8 * j + 8 && dy + W > 8 * j;
+            const unsigned m = __ballot_sync(0xffffffffu, hit);
+            if (hit) s_list[t * 32 + __popc(m & ((1u << lane) - 1u))] = packed;
+            cnt[t] = __popc(m);
         }
         __syncwarp();
-        for (int grp = 0; grp < n; grp += 4) {
-            const int node = grp + kq;
-            const int dx = s_ix[node], dy = s_iy[node];
-            const bool real = node < n;
-            // warp-uniform footprint of the group
-            int rmin = real ? dx : 1 << 20, rmax = real ? dx + W : -(1 << 20);
-            int cmin = real ? dy : 1 << 20, cmax = real ? dy + W : -(1 << 20);
 #pragma unroll
-            for (int o = 1; o <= 2; o <<= 1) {
-                rmin = min(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
-                rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
-                cmin = min(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
-                cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
-            }
-            double ar[2], ai[2], bb[4];
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                const int idx = 8 * i + gid - dx;
-                const double2 v = (real && (unsigned)idx < (unsigned)W) ? s_bwx[node * W + idx]
-                                                                        : make_double2(0.0, 0.0);
-                ar[i] = v.x;
-                ai[i] = v.y;
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int idx = 8 * j + gid - dy;
-                bb[j] = (real && (unsigned)idx < (unsigned)W) ? s_wy[node * W + idx] : 0.0;
-            }
-#pragma unroll
-            for (int i = 0; i < 2; ++i) {
-                if (rmax <= 8 * i || rmin >= 8 * i + 8) continue;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    if (cmax <= 8 * j || cmin >= 8 * j + 8) continue;
-                    dmma(cr[i][j][0], cr[i][j][1], ar[i], bb[j]);
-                    dmma(ci[i][j][0], ci[i][j][1], ai[i], bb[j]);
+        for (int t = 0; t < 8; ++t) {
+            const int i = t >> 2, j = t & 3;
+            for (int grp = 0; grp < cnt[t]; grp += 4) {
+                const int idx = grp + kq;
+                double a_r = 0.0, a_i = 0.0, bv = 0.0;
+                if (idx < cnt[t]) {
+                    const uint32_t e = s_list[t * 32 + idx];
+                    const int node = e & 255;
+                    const int rr = 8 * i + gid - ((int)((e >> 8) & 255) - 64);
+                    const int cc = 8 * j + gid - ((int)(e >> 16) - 64);
+                    if ((unsigned)rr < (unsigned)W) {
+                        const double2 v = s_bwx[node * W + rr];
+                        a_r = v.x;
+                        a_i = v.y;
+                    }
+                    if ((unsigned)cc < (unsigned)W) bv = s_wy[node * W + cc];
                 }
+                dmma(cr[i][j][0], cr[i][j][1], a_r, bv);
+                dmma(ci[i][j][0], ci[i][j][1], a_i, bv);
             }
         }
         __syncwarp();
@@ -420,23 +416,30 @@ __global__ void __launch_bounds__(128) k_spread_mma(WindowPoly P, GridGeom g, Ti
         if (cbx < 0 || cby < 0) continue;
         const int b = cbx * tg.nby + cby;
         const uint32_t s0 = bin_start[b], s1 = bin_start[b + 1];
-        for (uint32_t s = s0; s < s1; s += 32) {
-            const uint32_t k = s + lane;
-            bool take = false;
-            if (k < s1) {
-                const double2 t = pos[k];
-                const int ix0 = (int)ceil(t.x - g.half), iy0 = (int)ceil(t.y - g.half);
-                take = ix0 < X0 + TR && ix0 + W > X0 && iy0 < Y0 + kTileC && iy0 + W > Y0;
+        for (uint32_t s = s0; s < s1; s += 128) {
+            // four independent position loads in flight per lane
+            double2 tt[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t k = s + 32 * u + lane;
+                tt[u] = k < s1 ? pos[k] : make_double2(-1e30, -1e30);
             }
-            const unsigned m = __ballot_sync(0xffffffffu, take);
-            if (take) s_q[queued + __popc(m & ((1u << lane) - 1u))] = k;
-            queued += __popc(m);
-            __syncwarp();
-            if (queued >= 32) {
-                flush(32);
-                if (lane < queued - 32) s_q[lane] = s_q[32 + lane];
-                queued -= 32;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t k = s + 32 * u + lane;
+                const int ix0 = (int)ceil(tt[u].x - g.half), iy0 = (int)ceil(tt[u].y - g.half);
+                const bool take = k < s1 && ix0 < X0 + TR && ix0 + W > X0 && iy0 < Y0 + kTileC &&
+                                  iy0 + W > Y0;
+                const unsigned m = __ballot_sync(0xffffffffu, take);
+                if (take) s_q[queued + __popc(m & ((1u << lane) - 1u))] = k;
+                queued += __popc(m);
                 __syncwarp();
+                if (queued >= 32) {
+                    flush(32);
+                    if (lane < queued - 32) s_q[lane] = s_q[32 + lane];
+                    queued -= 32;
+                    __syncwarp();
+                }
             }
         }
     }
@@ -518,6 +521,151 @@ __global__ void __launch_bounds__(256) k_interp(WindowPoly P, GridGeom g, uint64
         out[dst] = q;
     } else {
         out[dst] = o;
+    }
+}
+
+// Interp on the fp64 tensor cores (nufft.cpp:254-283 restated). A warp
+// takes 32 consecutive sorted outputs, evaluates their windows (lane =
+// output; deconvolution factors folded in), then handles them 8 at a time:
+//   H[8 rows x 8 outputs] = G[8 rows x 4 cols] WY[4 cols x 8 outputs]
+// accumulated over the group's column footprint (two MMAs: Re G, Im G), for
+// each 8-row slice of the group's row footprint; each thread then applies the
+// x taps of its two outputs to its row of H, and the 8 row-lanes are reduced
+// with shuffles. Grid fragments come straight from L1/L2 (the band buffer).
+template <int W>
+__global__ void __launch_bounds__(128) k_interp_mma(WindowPoly P, GridGeom g, uint64_t n,
+                                                    const double2* __restrict__ pos,
+                                                    const double2* __restrict__ phase,
+                                                    const double2* __restrict__ mult,
+                                                    const double* __restrict__ dxt,
+                                                    const double* __restrict__ dyt,
+                                                    const double2* __restrict__ grid,
+                                                    const uint32_t* __restrict__ perm,
+                                                    const double2* __restrict__ addend,
+                                                    double2* __restrict__ out) {
+    __shared__ double s_wx[4][32 * W];
+    __shared__ double s_wy[4][32 * W];
+    __shared__ int s_jx[4][32], s_jy[4][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, kq = lane & 3;
+    double* wxs = s_wx[warp];
+    double* wys = s_wy[warp];
+    int* jxs = s_jx[warp];
+    int* jys = s_jy[warp];
+    const uint64_t nwarps = (uint64_t)gridDim.x * 4;
+    for (uint64_t base = ((uint64_t)blockIdx.x * 4 + warp) * 32; base < n; base += nwarps * 32) {
+        {
+            const uint64_t v = base + lane;
+            int jx0 = 1 << 28, jy0 = 1 << 28;
+            if (v < n) {
+                const double2 s = pos[v];
+                jx0 = (int)ceil(s.x - g.half);
+                jy0 = (int)ceil(s.y - g.half);
+                const int mx0 = wrap_base(jx0, g.n1), my0 = wrap_base(jy0, g.n2);
+                double* wxp = wxs + lane * W;
+                double* wyp = wys + lane * W;
+                kb_taps_each<W>((jx0 - s.x) + g.half, P, [&](int i, double w) {
+                    int mx = mx0 + i;
+                    if (mx >= g.n1) mx -= g.n1;
+                    wxp[i] = dxt ? w * dxt[mx] : w;
+                });
+                kb_taps_each<W>((jy0 - s.y) + g.half, P, [&](int j, double w) {
+                    int my = my0 + j;
+                    if (my >= g.n2) my -= g.n2;
+                    wyp[j] = dyt ? w * dyt[my] : w;
+                });
+            }
+            jxs[lane] = jx0;
+            jys[lane] = jy0;
+        }
+        __syncwarp();
+#pragma unroll 1
+        for (int grp = 0; grp < 4; ++grp) {
+            const int o8 = grp * 8;
+            // footprint of the 8 outputs (warp-uniform); absent outputs excluded
+            const int e = lane & 7;
+            const int jxe = jxs[o8 + e], jye = jys[o8 + e];
+            const bool real = jxe != (1 << 28);
+            int rmin = real ? jxe : 1 << 29, rmax = real ? jxe + W : -(1 << 29);
+            int cmin = real ? jye : 1 << 29, cmax = real ? jye + W : -(1 << 29);
+#pragma unroll
+            for (int o = 1; o <= 4; o <<= 1) {
+                rmin = min(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
+                rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+                cmin = min(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+                cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+            }
+            if (rmax < rmin) break; // no outputs left
+            const int nb = o8 + gid;              // output of this lane's B column
+            const int jyb = jys[nb];
+            const int na = o8 + 2 * kq;           // outputs of this lane's C columns
+            const int jxa0 = jxs[na], jxa1 = jxs[na + 1];
+            double p0r = 0.0, p0i = 0.0, p1r = 0.0, p1i = 0.0;
+            // up to three 8-row slices at once: six independent DMMA chains,
+            // one B fragment per column step shared by all slices
+            for (int r0 = rmin; r0 < rmax; r0 += 24) {
+                const int nrt = min(3, (rmax - r0 + 7) >> 3);
+                double hr[3][2], hi[3][2];
+                const double2* grow[3];
+#pragma unroll
+                for (int t = 0; t < 3; ++t) {
+                    hr[t][0] = hr[t][1] = hi[t][0] = hi[t][1] = 0.0;
+                    grow[t] = grid + (size_t)wrap_near(r0 + 8 * t + gid, g.n1) * g.n2;
+                }
+                for (int c0 = cmin; c0 < cmax; c0 += 4) {
+                    const int col = wrap_near(c0 + kq, g.n2);
+                    double2 a[3];
+#pragma unroll
+                    for (int t = 0; t < 3; ++t)
+                        a[t] = t < nrt ? __ldg(grow[t] + col) : make_double2(0.0, 0.0);
+                    const int jb = c0 + kq - jyb;
+                    const double b = (unsigned)jb < (unsigned)W ? wys[nb * W + jb] : 0.0;
+#pragma unroll
+                    for (int t = 0; t < 3; ++t) {
+                        if (t < nrt) {
+                            dmma(hr[t][0], hr[t][1], a[t].x, b);
+                            dmma(hi[t][0], hi[t][1], a[t].y, b);
+                        }
+                    }
+                }
+                // apply x taps: this lane holds H[row][na], H[row][na+1] per slice
+#pragma unroll
+                for (int t = 0; t < 3; ++t) {
+                    if (t >= nrt) continue;
+                    const int row = r0 + 8 * t + gid;
+                    const int i0 = row - jxa0, i1 = row - jxa1;
+                    const double w0 = (unsigned)i0 < (unsigned)W ? wxs[na * W + i0] : 0.0;
+                    const double w1 = (unsigned)i1 < (unsigned)W ? wxs[(na + 1) * W + i1] : 0.0;
+                    p0r = fma(hr[t][0], w0, p0r);
+                    p0i = fma(hi[t][0], w0, p0i);
+                    p1r = fma(hr[t][1], w1, p1r);
+                    p1i = fma(hi[t][1], w1, p1i);
+                }
+            }
+#pragma unroll
+            for (int o = 4; o <= 16; o <<= 1) {
+                p0r += __shfl_xor_sync(0xffffffffu, p0r, o);
+                p0i += __shfl_xor_sync(0xffffffffu, p0i, o);
+                p1r += __shfl_xor_sync(0xffffffffu, p1r, o);
+                p1i += __shfl_xor_sync(0xffffffffu, p1i, o);
+            }
+            if (gid == 0) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint64_t v = base + na + h;
+                    if (v >= n) continue;
+                    double2 o2 = cmul(h ? make_double2(p1r, p1i) : make_double2(p0r, p0i), phase[v]);
+                    if (mult) o2 = cmul(o2, mult[v]);
+                    if (addend) {
+                        const double2 ad = addend[v];
+                        o2.x += ad.x;
+                        o2.y += ad.y;
+                    }
+                    out[perm ? perm[v] : v] = o2;
+                }
+            }
+        }
+        __syncwarp();
     }
 }
 
@@ -657,7 +805,7 @@ struct SpreadRun {
 
 template <int W>
 struct SpreadTilesRun {
-    static size_t smem() { return (size_t)4 * 32 * W * 24 + 4 * 128 * sizeof(uint32_t); }
+    static size_t smem() { return (size_t)4 * 32 * W * 24 + 4 * 128 * sizeof(uint32_t) + 4 * 256 * sizeof(uint32_t); }
     static void run(const WindowPoly& P, GridGeom g, TileGeom tg, const uint32_t* bs,
                     const double2* b, const double2* pos, double2* grid, cudaStream_t st) {
         static bool attr = false;
@@ -694,6 +842,18 @@ struct InterpRun {
                     const double2* phase, const double2* mult, const double* dx, const double* dy,
                     const double2* grid, const uint32_t* perm, const double2* addend, double2* out,
                     int acc, int cj, cudaStream_t st) {
+        static int use_mma = -1;
+        if (use_mma < 0) {
+            const char* e = getenv("SBD_INTERP");  // experimental: SBD_INTERP=mma
+            use_mma = e && e[0] == 'm';
+        }
+        if (use_mma && !acc && !cj) {
+            const uint64_t warps = (n + 31) / 32;
+            const unsigned grid_blocks = (unsigned)std::min<uint64_t>((warps + 3) / 4, 148ull * 16);
+            k_interp_mma<W><<<grid_blocks, 128, 0, st>>>(P, g, n, pos, phase, mult, dx, dy, grid,
+                                                          perm, addend, out);
+            return;
+        }
         k_interp<W><<<blocks(n, 256), 256, 0, st>>>(P, g, n, pos, phase, mult, dx, dy, grid, perm,
                                                     addend, out, acc, cj);
     }

@@ -20,7 +20,6 @@ namespace {
 
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kSigma = 2.0; // nufft.cpp:19
-constexpr int kBinTile = 32;
 
 void span(const double* v, uint64_t n, int comp, double s, double& lo, double& hi) {
     lo = 1e300;
@@ -131,8 +130,8 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
         perm.alloc(n);
         if (tiles)
             launch_tile_keys(pos.p, n, g.half, tg, keys.p, st);
-        else
-            launch_bin_keys(pos.p, n, g, kBinTile, keys.p, st);
+        else  // outputs: 4x4-cell bins so 8 consecutive outputs share a small footprint
+            launch_bin_keys(pos.p, n, g, 4, keys.p, st);
         launch_iota(perm.p, n, st);
         sort_by_key(keys.p, perm.p, n, st);
         DevBuf<double2> a(n), b(n);
