@@ -302,11 +302,14 @@ __global__ void __launch_bounds__(128, TR == 16 ? 4 : 5) k_spread_tiles(WindowPo
     }
     if (queued) flush(queued);
     const int col = Y0 + lane;
-    if (col < g.n2) {
+    const int rend = tg.pitch ? tg.rhi : g.n1, cend = tg.pitch ? tg.chi : g.n2;
+    const size_t pitch = tg.pitch ? (size_t)tg.pitch : (size_t)g.n2;
+    const int r0 = tg.pitch ? tg.rlo : 0, c0 = tg.pitch ? tg.clo : 0;
+    if (col < cend) {
 #pragma unroll
         for (int r = 0; r < TR; ++r) {
             const int row = X0 + r;
-            if (row < g.n1) grid[(size_t)row * g.n2 + col] = make_double2(ar[r], ai[r]);
+            if (row < rend) grid[(size_t)(row - r0) * pitch + (col - c0)] = make_double2(ar[r], ai[r]);
         }
     }
 }
@@ -444,23 +447,26 @@ __global__ void __launch_bounds__(128) k_spread_mma(WindowPoly P, GridGeom g, Ti
         }
     }
     if (queued) flush(queued);
+    const int rend = tg.pitch ? tg.rhi : g.n1, cend = tg.pitch ? tg.chi : g.n2;
+    const size_t pitch = tg.pitch ? (size_t)tg.pitch : (size_t)g.n2;
+    const int r0 = tg.pitch ? tg.rlo : 0, c0 = tg.pitch ? tg.clo : 0;
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
         const int row = X0 + 8 * i + gid;
-        if (row >= g.n1) continue;
+        if (row >= rend) continue;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int col = Y0 + 8 * j + 2 * kq;
-            double2* dst = grid + (size_t)row * g.n2 + col;
-            if (col < g.n2) dst[0] = make_double2(cr[i][j][0], ci[i][j][0]);
-            if (col + 1 < g.n2) dst[1] = make_double2(cr[i][j][1], ci[i][j][1]);
+            double2* dst = grid + (size_t)(row - r0) * pitch + (col - c0);
+            if (col < cend) dst[0] = make_double2(cr[i][j][0], ci[i][j][0]);
+            if (col + 1 < cend) dst[1] = make_double2(cr[i][j][1], ci[i][j][1]);
         }
     }
 }
 
 // Interp (nufft.cpp:254-283): one thread per output; deconvolution folded
 // into the taps (exact: stencils never leave the band).
-template <int W>
+template <int W, bool TRANS>
 __global__ void __launch_bounds__(256) k_interp(WindowPoly P, GridGeom g, uint64_t n,
                                                 const double2* __restrict__ pos,
                                                 const double2* __restrict__ phase,
@@ -489,6 +495,30 @@ __global__ void __launch_bounds__(256) k_interp(WindowPoly P, GridGeom g, uint64
         if (dyt) wy[j] *= dyt[my];
     }
     double ar = 0.0, ai = 0.0;
+    if constexpr (TRANS) {
+        // grid stored [my][mx] (pitch n1): columns of the stencil are contiguous
+        int mxi[W];
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            int mx = mx0 + i;
+            if (mx >= g.n1) mx -= g.n1;
+            mxi[i] = mx;
+            if (dxt) wx[i] *= dxt[mx];
+        }
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            const double2* col = grid + (size_t)myj[j] * g.n1;
+            double rr = 0.0, ri = 0.0;
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                const double2 gv = __ldg(col + mxi[i]);
+                rr = fma(gv.x, wx[i], rr);
+                ri = fma(gv.y, wx[i], ri);
+            }
+            ar = fma(rr, wy[j], ar);
+            ai = fma(ri, wy[j], ai);
+        }
+    } else {
 #pragma unroll
     for (int i = 0; i < W; ++i) {
         int mx = mx0 + i;
@@ -504,6 +534,7 @@ __global__ void __launch_bounds__(256) k_interp(WindowPoly P, GridGeom g, uint64
         const double wxi = dxt ? wx[i] * dxt[mx] : wx[i];
         ar = fma(rr, wxi, ar);
         ai = fma(ri, wxi, ai);
+    }
     }
     double2 o = cmul(make_double2(ar, ai), phase[v]);
     if (mult) o = cmul(o, mult[v]);
@@ -732,6 +763,32 @@ __global__ void __launch_bounds__(256) k_spmv_vec(uint64_t rows, const uint64_t*
     if (r < rows && sub == 0) qs[r] = make_double2(ar, ai);
 }
 
+// Tt[c'][r] = T[r][m(c')] for r in [r0, r1) and the band columns c' in [0, B)
+// (m = c' for c' <= b, n2 - B + c' otherwise): 32 x 32 tiles through shared
+// memory so both the reads (along rows of T) and writes (along rows of Tt)
+// are coalesced.
+__global__ void __launch_bounds__(256) k_band_transpose(const double2* __restrict__ T, int n2,
+                                                        int r0, int r1, int b, int B,
+                                                        double2* __restrict__ Tt, int n1) {
+    __shared__ double2 tile[32][33];
+    const int cb = blockIdx.x * 32, rb = r0 + blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+#pragma unroll
+    for (int q = 0; q < 32; q += 8) {
+        const int r = rb + ty + q, c = cb + tx;
+        if (r < r1 && c < B) {
+            const int m = c <= b ? c : n2 - B + c;
+            tile[ty + q][tx] = T[(size_t)r * n2 + m];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 32; q += 8) {
+        const int c = cb + ty + q, r = rb + tx;
+        if (r < r1 && c < B) Tt[(size_t)c * n1 + r] = tile[tx][ty + q];
+    }
+}
+
 __global__ void k_mul(double2* x, const double2* __restrict__ m, uint64_t n) {
     const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (k < n) x[k] = cmul(x[k], m[k]);
@@ -841,11 +898,16 @@ struct InterpRun {
     static void run(const WindowPoly& P, GridGeom g, uint64_t n, const double2* pos,
                     const double2* phase, const double2* mult, const double* dx, const double* dy,
                     const double2* grid, const uint32_t* perm, const double2* addend, double2* out,
-                    int acc, int cj, cudaStream_t st) {
+                    int acc, int cj, cudaStream_t st, bool trans) {
         static int use_mma = -1;
         if (use_mma < 0) {
             const char* e = getenv("SBD_INTERP");  // experimental: SBD_INTERP=mma
             use_mma = e && e[0] == 'm';
+        }
+        if (trans) {
+            k_interp<W, true><<<blocks(n, 256), 256, 0, st>>>(P, g, n, pos, phase, mult, dx, dy, grid,
+                                                              perm, addend, out, acc, cj);
+            return;
         }
         if (use_mma && !acc && !cj) {
             const uint64_t warps = (n + 31) / 32;
@@ -854,8 +916,8 @@ struct InterpRun {
                                                           perm, addend, out);
             return;
         }
-        k_interp<W><<<blocks(n, 256), 256, 0, st>>>(P, g, n, pos, phase, mult, dx, dy, grid, perm,
-                                                    addend, out, acc, cj);
+        k_interp<W, false><<<blocks(n, 256), 256, 0, st>>>(P, g, n, pos, phase, mult, dx, dy, grid,
+                                                           perm, addend, out, acc, cj);
     }
 };
 
@@ -967,10 +1029,10 @@ void launch_spread(int w, const WindowPoly& win, GridGeom g, uint64_t n, const u
 void launch_interp(int w, const WindowPoly& win, GridGeom g, uint64_t n, const double2* pos,
                    const double2* phase, const double2* mult, const double* dx, const double* dy,
                    const double2* grid, const uint32_t* perm, double2* out, int accumulate,
-                   int conj_out, cudaStream_t st, const double2* addend) {
+                   int conj_out, cudaStream_t st, const double2* addend, bool transposed) {
     if (!n) return;
     dispatch_w<InterpRun>(w, win, g, n, pos, phase, mult, dx, dy, grid, perm, addend, out,
-                          accumulate, conj_out, st);
+                          accumulate, conj_out, st, transposed);
     count_launch();
     ck(cudaGetLastError(), "k_interp");
 }
@@ -997,6 +1059,15 @@ void launch_spmv_vec(uint64_t rows, const uint64_t* ro, const uint32_t* cols, co
     k_spmv_vec<<<blocks(rows * 8, 256), 256, 0, st>>>(rows, ro, cols, vals, f, qs);
     count_launch();
     ck(cudaGetLastError(), "k_spmv_vec");
+}
+
+void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int B, double2* Tt,
+                           int n1, cudaStream_t st) {
+    if (r1 <= r0) return;
+    dim3 grid((unsigned)((B + 31) / 32), (unsigned)((r1 - r0 + 31) / 32));
+    k_band_transpose<<<grid, 256, 0, st>>>(T, n2, r0, r1, b, B, Tt, n1);
+    count_launch();
+    ck(cudaGetLastError(), "k_band_transpose");
 }
 
 void launch_mul(double2* x, const double2* m, uint64_t n, cudaStream_t st) {

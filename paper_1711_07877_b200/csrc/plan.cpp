@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "pruned_dft.h"
 #include "sbd_internal.h"
 
 namespace sbdgpu {
@@ -160,13 +161,47 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
         dy_band.upload(hb.data(), bc, st);
     }
     if (pruned) {
+        tg.pitch = 0;
+        tg.rhi = rhi;
+        tg.chi = chi;
+        const char* fe = std::getenv("SBD_FFT");  // dft | cufft | (default) cufft-transposed
+        const bool want_dft = fe && fe[0] == 'd';
+        const int R = rhi - rlo, C = chi - clo;
+        if (want_dft && make_pruned_pass(ay.n, clo, C, R, pass1) &&
+            make_pruned_pass(ax.n, rlo, R, pass1.B, pass2)) {
+            dft = true;
+            tg.pitch = C;
+            pass1.in_row = C;
+            pass1.in_elem = 1;
+            pass1.out_row = pass1.B;
+            pass1.out_elem = 1;
+            pass2.in_row = 1;
+            pass2.in_elem = pass1.B;
+            pass2.out_row = pass2.B;
+            pass2.out_elem = 1;
+            tw1 = make_twiddles(ay.n, st);
+            tw2 = make_twiddles(ax.n, st);
+            band1 = pass2.b;
+            b1c = pass2.B;
+            std::vector<double> hb(b1c);
+            for (int r = 0; r < b1c; ++r) hb[r] = hx[r <= band1 ? r : ax.n + r - b1c];
+            dx_band.upload(hb.data(), b1c, st);
+        }
+    }
+    if (pruned && !dft) {
         int n2[1] = {ay.n}, n1[1] = {ax.n};
         ckfft(cufftPlanMany(&fft_row, 1, n2, n2, 1, ay.n, n2, 1, ay.n, CUFFT_Z2Z, rhi - rlo),
               "cufftPlanMany rows");
-        ckfft(cufftPlanMany(&fft_colA, 1, n1, n1, ay.n, 1, n1, bc, 1, CUFFT_Z2Z, band2 + 1),
-              "cufftPlanMany cols A");
-        ckfft(cufftPlanMany(&fft_colB, 1, n1, n1, ay.n, 1, n1, bc, 1, CUFFT_Z2Z, band2),
-              "cufftPlanMany cols B");
+        const char* fe = std::getenv("SBD_FFT");
+        if (fe && fe[0] == 'c') {  // strided column transforms straight from T
+            ckfft(cufftPlanMany(&fft_colA, 1, n1, n1, ay.n, 1, n1, bc, 1, CUFFT_Z2Z, band2 + 1),
+                  "cufftPlanMany cols A");
+            ckfft(cufftPlanMany(&fft_colB, 1, n1, n1, ay.n, 1, n1, bc, 1, CUFFT_Z2Z, band2),
+                  "cufftPlanMany cols B");
+        } else {  // band columns transposed, then contiguous length-n1 transforms
+            ckfft(cufftPlanMany(&fft_colT, 1, n1, n1, 1, ax.n, n1, 1, ax.n, CUFFT_Z2Z, bc),
+                  "cufftPlanMany cols T");
+        }
     }
     ck(cudaStreamSynchronize(st), "plan build");
 }
@@ -176,6 +211,7 @@ Plan::~Plan() {
     if (fft_row) cufftDestroy(fft_row);
     if (fft_colA) cufftDestroy(fft_colA);
     if (fft_colB) cufftDestroy(fft_colB);
+    if (fft_colT) cufftDestroy(fft_colT);
 }
 
 void FftWork::ensure(int n1_, int n2_, int bc_, cudaStream_t st) {
@@ -195,6 +231,20 @@ void FftWork::ensure(int n1_, int n2_, int bc_, cudaStream_t st) {
 
 void Plan::ensure_work(FftWork& wk, cudaStream_t st) const {
     if (fast) wk.ensure(std::max(wk.n1, ax.n), std::max(wk.n2, ay.n), std::max(wk.bc, bc), st);
+    if (dft) {
+        const size_t t1 = (size_t)pass1.rows * pass1.B, bt = (size_t)pass2.rows * pass2.B;
+        if (wk.T1.n < t1) wk.T1.alloc(t1);
+        if (wk.bandT.n < bt) wk.bandT.alloc(bt);
+    }
+    if (fft_colT) {
+        const size_t need = (size_t)bc * ax.n;
+        if (wk.T1.n < need) {
+            wk.T1.alloc(need);
+            ck(cudaMemsetAsync(wk.T1.p, 0, wk.T1.bytes(), st), "Tt zero");
+            wk.tt_r0 = wk.tt_r1 = 0;
+        }
+        if (wk.bandT.n < need) wk.bandT.alloc(need);
+    }
 }
 
 namespace {
@@ -287,6 +337,27 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         launch_gather_mul(in, perm_t.n ? perm_t.p : nullptr, pre.p, wk.bbuf.p, raw_sorted, np, st);
         b = wk.bbuf.p;
     }
+    if (dft) {
+        // compact support grid -> rows pass -> band-columns pass -> transposed band
+        launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, wk.grid.p, st);
+        if (tm) tm->stop();
+        if (tm) tm->start(tag_fft);
+        launch_pruned_dft(pass1, wk.grid.p, wk.T1.p, tw1.p, st);
+        launch_pruned_dft(pass2, wk.T1.p, wk.bandT.p, tw2.p, st);
+        if (tm) tm->stop();
+        // the full-layout invariants of the cuFFT path no longer hold
+        wk.gr0 = 0;
+        wk.gr1 = wk.n1;
+        wk.gc0 = 0;
+        wk.gc1 = wk.n2;
+        wk.g_pitch = wk.n2;
+        if (tm) tm->start(tag_interp);
+        const GridGeom gt{b1c, bc, 0.5 * w};
+        launch_interp(w, win, gt, nf, s.p, post.p, mult, dx_band.p, dy_band.p, wk.bandT.p,
+                      perm_s.n ? perm_s.p : nullptr, out, 0, 0, st, addend, /*transposed=*/true);
+        if (tm) tm->stop();
+        return;
+    }
     if (wk.g_pitch == n2)
         zero_rect_minus(wk.grid.p, n2, wk.gr0, wk.gr1, wk.gc0, wk.gc1, rlo, rhi, clo, chi, st);
     else if (wk.g_pitch)  // written by a plan of another grid size: clear all of it
@@ -312,6 +383,33 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
     wk.tr0 = rlo;
     wk.tr1 = rhi;
     wk.t_pitch = n2;
+    if (fft_colT) {
+        // Tt[c'][x] (pitch n1) holds band column c' over the populated rows only;
+        // every other row x of Tt stays zero (strips a previous plan left are cleared).
+        if (wk.tt_r1 > wk.tt_r0) {
+            if (wk.tt_pitch == ax.n && wk.tt_rows == bc)
+                zero_rect_minus(wk.T1.p, ax.n, 0, bc, wk.tt_r0, wk.tt_r1, 0, bc, rlo, rhi, st);
+            else
+                zero_rect_minus(wk.T1.p, wk.tt_pitch, 0, wk.tt_rows, wk.tt_r0, wk.tt_r1, 0, 0, 0, 0, st);
+        }
+        launch_band_transpose(wk.T.p, n2, rlo, rhi, band2, bc, wk.T1.p, ax.n, st);
+        wk.tt_r0 = rlo;
+        wk.tt_r1 = rhi;
+        wk.tt_pitch = ax.n;
+        wk.tt_rows = bc;
+        auto* Tt = reinterpret_cast<cufftDoubleComplex*>(wk.T1.p);
+        auto* BT = reinterpret_cast<cufftDoubleComplex*>(wk.bandT.p);
+        ckfft(cufftSetStream(fft_colT, st), "cufftSetStream");
+        ckfft(cufftExecZ2Z(fft_colT, Tt, BT, CUFFT_INVERSE), "fft cols T");
+        count_launch(2);
+        if (tm) tm->stop();
+        if (tm) tm->start(tag_interp);
+        const GridGeom gt{ax.n, bc, 0.5 * w};
+        launch_interp(w, win, gt, nf, s.p, post.p, mult, dx.p, dy_band.p, wk.bandT.p,
+                      perm_s.n ? perm_s.p : nullptr, out, 0, 0, st, addend, /*transposed=*/true);
+        if (tm) tm->stop();
+        return;
+    }
     // band columns of T -> band buffer (n1 x bc, columns in mode order mod bc)
     ckfft(cufftSetStream(fft_colA, st), "cufftSetStream");
     ckfft(cufftExecZ2Z(fft_colA, T, B, CUFFT_INVERSE), "fft cols A");

@@ -120,6 +120,9 @@ struct StageTimer {
 // dirty rectangles", so no full-grid memset is needed per apply.
 struct FftWork {
     DevBuf<double2> grid, T, band;
+    DevBuf<double2> T1, bandT; // row-pass output / transposed band (custom or cuFFT-T path)
+    int tt_r0 = 0, tt_r1 = 0;  // rows (x) possibly nonzero in every Tt row (cuFFT-T path) ...
+    int tt_pitch = 0, tt_rows = 0; // ... for a Tt of this pitch (n1) and row count (bc)
     DevBuf<double2> bbuf; // spread coefficients b = c * prephase, sorted point order
     int n1 = 0, n2 = 0, bc = 0;
     int gr0 = 0, gr1 = 0, gc0 = 0, gc1 = 0; // grid cells possibly nonzero ...
@@ -135,7 +138,21 @@ constexpr int kTileR = 16;
 constexpr int kTileC = 32;
 struct TileGeom {
     int rlo, clo, nbx, nby;
-    int tr; // rows per tile (8 or 16)
+    int tr;              // rows per tile (8 or 16)
+    int pitch;           // 0: write the full n1 x n2 grid; else compact region layout
+    int rhi, chi;        // region end (writes clipped here)
+};
+
+// One band-pruned DFT pass (pruned_dft.cu): `rows` sequences, element m
+// (m in [lo, lo+L)) of sequence r at in[r * in_row + (m - lo) * in_elem];
+// output mode j (|j| <= b) at out[r * out_row + (j mod B) * out_elem].
+struct PrunedPass {
+    int n = 0, lo = 0, L = 0, rows = 0;
+    int b = 0, B = 0;  // band half-width n/4 and band size 2b+1
+    int D = 0, N = 0;  // output decimation and sub-FFT length n / D
+    int nstages = 0;
+    int radix[32] = {0};
+    int64_t in_row = 0, in_elem = 1, out_row = 0, out_elem = 1;
 };
 
 // A type-III NUFFT plan on one device (reference NufftPlan, nufft.hpp:30-56).
@@ -174,12 +191,19 @@ class Plan {
     // the populated region; row FFTs over the populated rows only, column FFTs
     // over the band columns only (the only modes the interpolation reads).
     bool pruned = false;
+    bool dft = false;  // custom band-pruned DFT passes (else cuFFT row/column plans)
     int rlo = 0, rhi = 0, clo = 0, chi = 0; // region written by the spread tiles
     TileGeom tg{};
     DevBuf<uint32_t> bin_start;
     int band2 = 0, bc = 0;
     DevBuf<double> dy_band;
     cufftHandle fft_row = 0, fft_colA = 0, fft_colB = 0;
+    cufftHandle fft_colT = 0;  // contiguous transforms of the transposed band columns
+    // custom passes: rows of the compact grid (n2, band B2) then band columns (n1, band B1)
+    int band1 = 0, b1c = 0;
+    DevBuf<double> dx_band;
+    DevBuf<double2> tw1, tw2;  // e^{+2 pi i q / n} tables for the two axes
+    PrunedPass pass1{}, pass2{};
 
     uint64_t cells() const { return fast ? (uint64_t)ax.n * (uint64_t)ay.n : 0; }
     size_t device_bytes() const;
@@ -236,6 +260,8 @@ void launch_bin_bounds(const uint32_t* sorted_keys, uint64_t n, uint32_t nbins, 
 void launch_spread_tiles(int w, const WindowPoly& win, GridGeom g, TileGeom tg,
                          const uint32_t* bin_start, const double2* b, const double2* pos,
                          double2* grid, cudaStream_t st);
+void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int B, double2* Tt,
+                           int n1, cudaStream_t st);
 void launch_gather_mul(const double2* in, const uint32_t* perm, const double2* phase, double2* b,
                        double2* raw, uint64_t n, cudaStream_t st);
 void launch_spmv_vec(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double2* vals,
@@ -255,7 +281,8 @@ void launch_spread(int w, const WindowPoly& win, GridGeom g, uint64_t n, const u
 void launch_interp(int w, const WindowPoly& win, GridGeom g, uint64_t n, const double2* pos,
                    const double2* phase, const double2* mult, const double* dx, const double* dy,
                    const double2* grid, const uint32_t* perm, double2* out, int accumulate,
-                   int conj_out, cudaStream_t st, const double2* addend = nullptr);
+                   int conj_out, cudaStream_t st, const double2* addend = nullptr,
+                   bool transposed = false);
 // direct sum out[v] = sum_k c_k e^{i sign z_k . f_v}
 void launch_ndft(const double2* pts, uint64_t np, const double2* frq, uint64_t nf,
                  const double2* c, int sign, double2* out, cudaStream_t st);

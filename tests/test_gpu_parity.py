@@ -203,3 +203,27 @@ def test_apply_is_deterministic(ops):
     a = ops["lap_star_n1500"].apply(g["f"])
     b = ops["lap_star_n1500"].apply(g["f"])
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["lap_disk_n1000", "helm_disk_n800", "lap_star_n1500"])
+def test_pruned_dft_and_cufft_paths_agree(name, monkeypatch):
+    # the custom band-pruned DFT passes against the cuFFT row/column path
+    path, g = golden(name)
+    dft = sbd.CompressedOperator.load(path)
+    monkeypatch.setenv("SBD_FFT", "cufft")
+    cuf = sbd.CompressedOperator.load(path)
+    monkeypatch.delenv("SBD_FFT")
+    assert rel_l2(dft.apply(g["f"]), cuf.apply(g["f"])) <= 1e-13
+
+
+@pytest.mark.parametrize("mode", ["cufft", "dft"])
+def test_fft_variants_agree_on_two_clouds(mode, monkeypatch):
+    # plans of different grid sizes sharing the operator's scratch buffers
+    path, g = golden("lap_two_clouds")
+    base = sbd.CompressedOperator.load(path)
+    monkeypatch.setenv("SBD_FFT", mode)
+    other = sbd.CompressedOperator.load(path)
+    monkeypatch.delenv("SBD_FFT")
+    for _ in range(2):
+        assert rel_l2(other.apply(g["f"]), base.apply(g["f"])) <= 1e-13
+    assert rel_l2(base.apply(g["f"]), g["q"]) <= PARITY
