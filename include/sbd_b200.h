@@ -106,6 +106,22 @@ int sbd_op_apply_device(sbd_op* op, const double* d_f, double* d_q, int nrhs, vo
 int sbd_op_apply_adjoint_device(sbd_op* op, const double* d_u, double* d_q, int nrhs,
                                 void* stream);
 
+/* ---- multi-GPU building blocks (north_star scheme) ----
+ * One apply split over G devices, each holding the same operator:
+ *   spec_r = sbd_op_forward_spectrum(f, source shard r)   (sources sharded)
+ *   spec   = sum_r spec_r                                  (one allreduce of n_xi complex)
+ *   q[T_r] = sbd_op_backward_targets(spec, f, target shard r)  (targets + D rows sharded)
+ * Shards are ranges of the operator's spatially sorted source / target
+ * orders; sbd_op_shard_bounds returns an even split (side 0 sources, 1
+ * targets) as nshards+1 bounds. `spec` has n_xi complex entries in the
+ * operator's internal xi order and already carries omega-hat and the
+ * second NUFFT's prephase. Requires both NUFFTs on the gridded path. */
+int sbd_op_shard_bounds(const sbd_op* op, int side, int nshards, uint64_t* bounds);
+int sbd_op_forward_spectrum(sbd_op* op, const double* d_f, uint64_t src_lo, uint64_t src_hi,
+                            double* d_spec, void* stream);
+int sbd_op_backward_targets(sbd_op* op, const double* d_spec, const double* d_f, uint64_t tgt_lo,
+                            uint64_t tgt_hi, double* d_q, void* stream);
+
 /* Per-stage CUDA-event timing of every apply since profiling was enabled (or
  * since the last reset). names: "spread_src", "fft_in", "interp_xi",
  * "spread_xi", "fft_out", "interp_tgt", "spmv", ... ms[i] in milliseconds.

@@ -72,6 +72,7 @@ class Oracle:
         L.orc_op_apply.argtypes = [ctypes.c_void_p, _dp, _dp]
         L.orc_op_apply_adjoint.argtypes = [ctypes.c_void_p, _dp, _dp]
         L.orc_op_stage.argtypes = [ctypes.c_void_p, ctypes.c_int, _dp, _dp]
+        L.orc_op_weights.argtypes = [ctypes.c_void_p, _dp]
         self.L = L
 
     def err(self):
@@ -159,6 +160,11 @@ class OracleOp:
         if self.o.L.orc_op_apply_adjoint(self.h, _p(u.view(np.float64)), _p(q.view(np.float64))):
             raise RuntimeError(self.o.err())
         return q
+
+    def weights(self):
+        w = np.zeros(self.n_xi, np.complex128)
+        self.o.L.orc_op_weights(self.h, _p(w.view(np.float64)))
+        return w
 
     def stage(self, stage, x, out=None):
         x = as_cplx(x)

@@ -512,6 +512,10 @@ int orc_op_apply_adjoint(const orc_op* op, const double* u, double* q) {
     return rc;
 }
 
+void orc_op_weights(const orc_op* op, double* w) {
+    memcpy(w, op->weights, sizeof(double) * 2 * op->n_xi);
+}
+
 int orc_op_stage(const orc_op* op, int stage, const double* in, double* out) {
     switch (stage) {
         case 1: return orc_plan_apply(op->fwd_in, in, out);

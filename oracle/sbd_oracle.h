@@ -52,6 +52,8 @@ int orc_op_apply_adjoint(const orc_op* op, const double* u, double* q);
 /* stage 1: fwd_in(f) -> spectrum (unweighted); 2: fwd_out(spectrum) -> q;
  * 3: q += D f. */
 int orc_op_stage(const orc_op* op, int stage, const double* in, double* out);
+/* omega-hat (2*n_xi doubles, file order) */
+void orc_op_weights(const orc_op* op, double* w);
 
 #ifdef __cplusplus
 }

@@ -725,11 +725,11 @@ __global__ void k_ndft(const double2* __restrict__ pts, uint64_t np,
 // coefficients (nufft.cpp:233) and the sorted copy of f for the CSR pass.
 __global__ void k_gather_mul(const double2* __restrict__ in, const uint32_t* __restrict__ perm,
                              const double2* __restrict__ phase, double2* __restrict__ b,
-                             double2* __restrict__ raw, uint64_t n) {
+                             double2* __restrict__ raw, uint64_t n, uint64_t lo, uint64_t hi) {
     const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (k >= n) return;
     const double2 c = in[perm ? perm[k] : k];
-    b[k] = cmul(c, phase[k]);
+    b[k] = (k >= lo && k < hi) ? cmul(c, phase[k]) : make_double2(0.0, 0.0);
     if (raw) raw[k] = c;
 }
 
@@ -1046,9 +1046,9 @@ void launch_ndft(const double2* pts, uint64_t np, const double2* frq, uint64_t n
 }
 
 void launch_gather_mul(const double2* in, const uint32_t* perm, const double2* phase, double2* b,
-                       double2* raw, uint64_t n, cudaStream_t st) {
+                       double2* raw, uint64_t n, cudaStream_t st, uint64_t lo, uint64_t hi) {
     if (!n) return;
-    k_gather_mul<<<blocks(n, 256), 256, 0, st>>>(in, perm, phase, b, raw, n);
+    k_gather_mul<<<blocks(n, 256), 256, 0, st>>>(in, perm, phase, b, raw, n, lo, hi);
     count_launch();
     ck(cudaGetLastError(), "k_gather_mul");
 }

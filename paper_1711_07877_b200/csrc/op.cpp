@@ -291,6 +291,31 @@ struct sbd_op {
         if (tm.on) tm.stop();
     }
 
+    // Sharded forward half (multi-GPU): the kappa-weighted
+    // spectrum of the sources in sorted range [lo, hi). Summing it over a
+    // partition of the sources gives exactly the single-device spectrum.
+    void forward_spectrum(const double2* f, uint64_t lo, uint64_t hi, double2* spec_out,
+                          cudaStream_t st) {
+        if (!fused) throw Error(SBD_ERR_RUNTIME, "sharded apply needs both NUFFTs on the gridded path");
+        fwd_in->apply_pruned(f, false, f_sorted.p, spec_out, kappa.p, nullptr, work, st, &tm,
+                             "spread_src", "fft_in", "interp_xi", lo, hi);
+    }
+
+    // Sharded backward half: q at the targets in sorted range [lo, hi)
+    // (written at their caller indices) = NUFFT+(spectrum) + D f on those rows.
+    void backward_targets(const double2* spec_in, const double2* f, uint64_t lo, uint64_t hi,
+                          double2* q, cudaStream_t st) {
+        if (!fused) throw Error(SBD_ERR_RUNTIME, "sharded apply needs both NUFFTs on the gridded path");
+        hi = std::min<uint64_t>(hi, d.n_tgt());
+        lo = std::min(lo, hi);
+        launch_gather_mul(f, fwd_in->perm_t.p, fwd_in->pre.p, work.bbuf.p, f_sorted.p, d.n_src(), st, 0, 0);
+        if (tm.on) tm.start("spmv");
+        launch_spmv_vec(hi - lo, ro_s.p + lo, cols_s.p, vals_s.p, f_sorted.p, qs.p + lo, st);
+        if (tm.on) tm.stop();
+        fwd_out->apply_pruned(spec_in, true, nullptr, q, nullptr, qs.p, work, st, &tm, "spread_xi",
+                              "fft_out", "interp_tgt", 0, ~0ull, lo, hi);
+    }
+
     // conv_operator.cpp:311-324
     void apply_adjoint_one(const double2* u, double2* q, cudaStream_t st) {
         fwd_out->apply_transpose(u, spec.p, work, st, &tm, w_sorted.p, /*conj_in=*/1, 0);
@@ -522,6 +547,41 @@ int sbd_op_apply_adjoint_device(sbd_op* op, const double* d_u, double* d_q, int 
         for (int r = 0; r < nrhs; ++r)
             op->apply_adjoint_one(u + (size_t)r * op->d.n_tgt(), q + (size_t)r * op->d.n_src(), st);
         ck(cudaGetLastError(), "apply_adjoint");
+    });
+}
+
+int sbd_op_shard_bounds(const sbd_op* op, int side, int nshards, uint64_t* bounds) {
+    return guarded([&] {
+        if (!op || !bounds || nshards < 1 || (side != 0 && side != 1))
+            throw Error(SBD_ERR_INVALID_ARGUMENT, "shard_bounds: bad argument");
+        const uint64_t n = side == 0 ? op->d.n_src() : op->d.n_tgt();
+        for (int i = 0; i <= nshards; ++i) bounds[i] = n * (uint64_t)i / (uint64_t)nshards;
+    });
+}
+
+int sbd_op_forward_spectrum(sbd_op* op, const double* d_f, uint64_t src_lo, uint64_t src_hi,
+                            double* d_spec, void* stream) {
+    return guarded([&] {
+        if (!op || !d_f || !d_spec) throw Error(SBD_ERR_INVALID_ARGUMENT, "forward_spectrum: null argument");
+        std::lock_guard<std::mutex> lk(op->mu);
+        DeviceGuard g(op->device);
+        op->tm.stream = (cudaStream_t)stream;
+        op->forward_spectrum(reinterpret_cast<const double2*>(d_f), src_lo, src_hi,
+                             reinterpret_cast<double2*>(d_spec), (cudaStream_t)stream);
+        ck(cudaGetLastError(), "forward_spectrum");
+    });
+}
+
+int sbd_op_backward_targets(sbd_op* op, const double* d_spec, const double* d_f, uint64_t tgt_lo,
+                            uint64_t tgt_hi, double* d_q, void* stream) {
+    return guarded([&] {
+        if (!op || !d_spec || !d_f || !d_q) throw Error(SBD_ERR_INVALID_ARGUMENT, "backward_targets: null argument");
+        std::lock_guard<std::mutex> lk(op->mu);
+        DeviceGuard g(op->device);
+        op->tm.stream = (cudaStream_t)stream;
+        op->backward_targets(reinterpret_cast<const double2*>(d_spec), reinterpret_cast<const double2*>(d_f),
+                             tgt_lo, tgt_hi, reinterpret_cast<double2*>(d_q), (cudaStream_t)stream);
+        ck(cudaGetLastError(), "backward_targets");
     });
 }
 

@@ -325,7 +325,18 @@ void Plan::apply(const double2* in, double2* out, FftWork& wk, cudaStream_t st, 
 void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, double2* out,
                         const double2* mult, const double2* addend, FftWork& wk, cudaStream_t st,
                         StageTimer* tm, const char* tag_spread, const char* tag_fft,
-                        const char* tag_interp) const {
+                        const char* tag_interp, uint64_t in_lo, uint64_t in_hi, uint64_t out_lo,
+                        uint64_t out_hi) const {
+    out_hi = std::min<uint64_t>(out_hi, nf);
+    out_lo = std::min(out_lo, out_hi);
+    const uint64_t nout = out_hi - out_lo;
+    // output-side arrays restricted to the sorted output range [out_lo, out_hi)
+    const double2* s_p = s.p + out_lo;
+    const double2* post_p = post.p + out_lo;
+    const double2* mult_p = mult ? mult + out_lo : nullptr;
+    const double2* add_p = addend ? addend + out_lo : nullptr;
+    const uint32_t* perm_p = perm_s.n ? perm_s.p + out_lo : nullptr;
+    double2* out_p = perm_s.n ? out : out + out_lo;
     if (!pruned) throw Error(3, "apply_pruned on a plan without the pruned path");
     ensure_work(wk, st);
     const GridGeom g{ax.n, ay.n, 0.5 * w};
@@ -334,7 +345,8 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
     const double2* b = in;
     if (!in_is_b) {
         if (wk.bbuf.n < np) wk.bbuf.alloc(np);
-        launch_gather_mul(in, perm_t.n ? perm_t.p : nullptr, pre.p, wk.bbuf.p, raw_sorted, np, st);
+        launch_gather_mul(in, perm_t.n ? perm_t.p : nullptr, pre.p, wk.bbuf.p, raw_sorted, np, st, in_lo,
+                          in_hi);
         b = wk.bbuf.p;
     }
     if (dft) {
@@ -353,8 +365,8 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         wk.g_pitch = wk.n2;
         if (tm) tm->start(tag_interp);
         const GridGeom gt{b1c, bc, 0.5 * w};
-        launch_interp(w, win, gt, nf, s.p, post.p, mult, dx_band.p, dy_band.p, wk.bandT.p,
-                      perm_s.n ? perm_s.p : nullptr, out, 0, 0, st, addend, /*transposed=*/true);
+        launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx_band.p, dy_band.p, wk.bandT.p, perm_p,
+                      out_p, 0, 0, st, add_p, /*transposed=*/true);
         if (tm) tm->stop();
         return;
     }
@@ -405,8 +417,8 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         if (tm) tm->stop();
         if (tm) tm->start(tag_interp);
         const GridGeom gt{ax.n, bc, 0.5 * w};
-        launch_interp(w, win, gt, nf, s.p, post.p, mult, dx.p, dy_band.p, wk.bandT.p,
-                      perm_s.n ? perm_s.p : nullptr, out, 0, 0, st, addend, /*transposed=*/true);
+        launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx.p, dy_band.p, wk.bandT.p, perm_p,
+                      out_p, 0, 0, st, add_p, /*transposed=*/true);
         if (tm) tm->stop();
         return;
     }
@@ -419,8 +431,8 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
     if (tm) tm->stop();
     if (tm) tm->start(tag_interp);
     const GridGeom gb{ax.n, bc, 0.5 * w};
-    launch_interp(w, win, gb, nf, s.p, post.p, mult, dx.p, dy_band.p, wk.band.p,
-                  perm_s.n ? perm_s.p : nullptr, out, 0, 0, st, addend);
+    launch_interp(w, win, gb, nout, s_p, post_p, mult_p, dx.p, dy_band.p, wk.band.p, perm_p, out_p, 0,
+                  0, st, add_p);
     if (tm) tm->stop();
 }
 

@@ -222,7 +222,8 @@ class Plan {
     void apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, double2* out,
                       const double2* mult, const double2* addend, FftWork& wk, cudaStream_t st,
                       StageTimer* tm, const char* tag_spread, const char* tag_fft,
-                      const char* tag_interp) const;
+                      const char* tag_interp, uint64_t in_lo = 0, uint64_t in_hi = ~0ull,
+                      uint64_t out_lo = 0, uint64_t out_hi = ~0ull) const;
     void apply_transpose(const double2* in, double2* out, FftWork& wk, cudaStream_t st,
                          StageTimer* tm, const double2* mult = nullptr, int conj_in = 0,
                          int conj_out = 0) const;
@@ -262,8 +263,10 @@ void launch_spread_tiles(int w, const WindowPoly& win, GridGeom g, TileGeom tg,
                          double2* grid, cudaStream_t st);
 void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int B, double2* Tt,
                            int n1, cudaStream_t st);
+// b[k] = in[perm[k]] phase[k] for k in [lo, hi) (zero elsewhere); raw[k] = in[perm[k]].
 void launch_gather_mul(const double2* in, const uint32_t* perm, const double2* phase, double2* b,
-                       double2* raw, uint64_t n, cudaStream_t st);
+                       double2* raw, uint64_t n, cudaStream_t st, uint64_t lo = 0,
+                       uint64_t hi = ~0ull);
 void launch_spmv_vec(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double2* vals,
                      const double2* f, double2* qs, cudaStream_t st);
 void sort_by_key(uint32_t* keys, uint32_t* vals, uint64_t n, cudaStream_t st);

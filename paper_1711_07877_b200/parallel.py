@@ -1,0 +1,84 @@
+"""Multi-GPU apply: one process per GPU, torch.distributed for the plumbing.
+
+The north_star partition of CompressedOperator::apply (conv_operator.cpp:301-309)
+over G ranks:
+
+  1. sources sharded: rank r forms the omega-hat-weighted xi spectrum of its
+     source shard only (sbd_op_forward_spectrum); the spectrum is linear in f,
+  2. one all-reduce (sum) of the n_xi complex spectrum -- the only data-path
+     collective, because it is the path's only real exchange step,
+  3. targets and near-field rows sharded: rank r evaluates the second NUFFT at
+     its target shard and adds its rows of D f (sbd_op_backward_targets); f is
+     replicated (all-gathered) on every rank.
+
+Shards are ranges of the operator's spatially sorted orders, so a rank's
+points are spatially compact. The orchestration is backend-agnostic: the GPU
+backend calls the C ABI on device buffers; tests drive the same code with a
+CPU backend over gloo.
+"""
+from __future__ import annotations
+
+import ctypes
+
+from ._capi import check, lib
+
+
+class DeviceBackend:
+    """CompressedOperator on this rank's GPU, torch tensors as buffers."""
+
+    def __init__(self, op):
+        import torch
+        self.torch = torch
+        self.op = op
+        info = op.info()
+        self.n_src, self.n_tgt, self.n_xi = info["n_src"], info["n_tgt"], info["n_xi"]
+        if not (info["fast_in"] and info["fast_out"]):
+            raise ValueError("sharded apply needs both NUFFTs on the gridded path")
+
+    def shard_bounds(self, side: int, nshards: int):
+        b = (ctypes.c_uint64 * (nshards + 1))()
+        check(lib.sbd_op_shard_bounds(self.op._h, side, nshards, b))
+        return [int(x) for x in b]
+
+    def new_spectrum(self):
+        return self.torch.zeros(2 * self.n_xi, dtype=self.torch.float64, device="cuda")
+
+    def forward_spectrum(self, f, lo, hi, spec):
+        s = self.torch.cuda.current_stream().cuda_stream
+        check(lib.sbd_op_forward_spectrum(self.op._h, ctypes.c_void_p(f.data_ptr()), lo, hi,
+                                          ctypes.c_void_p(spec.data_ptr()), ctypes.c_void_p(s)))
+
+    def backward_targets(self, spec, f, lo, hi, q):
+        s = self.torch.cuda.current_stream().cuda_stream
+        check(lib.sbd_op_backward_targets(self.op._h, ctypes.c_void_p(spec.data_ptr()),
+                                          ctypes.c_void_p(f.data_ptr()), lo, hi,
+                                          ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(s)))
+
+
+class ShardedApply:
+    """q = A f split over `world` ranks (see module docstring).
+
+    `f` (2 * n_src float64, interleaved complex) is replicated on every rank;
+    each rank's `q` receives the entries of its target shard (at their caller
+    indices) and is left untouched elsewhere."""
+
+    def __init__(self, backend, rank: int, world: int, allreduce=None):
+        self.b = backend
+        self.rank, self.world = rank, world
+        self.src = backend.shard_bounds(0, world)
+        self.tgt = backend.shard_bounds(1, world)
+        if allreduce is None:
+            import torch.distributed as dist
+            allreduce = (lambda t: dist.all_reduce(t)) if world > 1 else (lambda t: None)
+        self.allreduce = allreduce
+        self.spec = backend.new_spectrum()
+
+    def target_range(self):
+        return self.tgt[self.rank], self.tgt[self.rank + 1]
+
+    def apply(self, f, q):
+        r = self.rank
+        self.b.forward_spectrum(f, self.src[r], self.src[r + 1], self.spec)
+        self.allreduce(self.spec)
+        self.b.backward_targets(self.spec, f, self.tgt[r], self.tgt[r + 1], q)
+        return self.target_range()
