@@ -67,6 +67,13 @@ def build(verbose: bool = False, force: bool = False) -> str:
         _run(["g++", "-shared", "-o", tmp, *objs, f"-L{CUDA}/lib64", "-lcufft", "-lcusolver", "-lcudart_static", "-fopenmp",
               "-ldl", "-lrt", "-lpthread", f"-Wl,-rpath,{CUDA}/lib64"], verbose)
         shutil.move(tmp, LIB)
+    # the C++ API example (include/sbd_b200.hpp) links the library like a user would
+    ex_src = os.path.join(HERE, "..", "examples", "apply_example.cpp")
+    ex_bin = os.path.join(OBJ, "apply_example")
+    if os.path.exists(ex_src) and (force or _stale(ex_bin, [ex_src, LIB] + headers +
+                                                   [os.path.join(HERE, "..", "include", "sbd_b200.hpp")])):
+        _run(["g++", "-std=c++17", "-O2", f"-I{os.path.join(HERE, '..', 'include')}", ex_src, "-o", ex_bin,
+              f"-L{HERE}", "-lsbd_b200", f"-Wl,-rpath,{HERE}"], verbose)
     return LIB
 
 

@@ -227,3 +227,13 @@ def test_fft_variants_agree_on_two_clouds(mode, monkeypatch):
     for _ in range(2):
         assert rel_l2(other.apply(g["f"]), base.apply(g["f"])) <= 1e-13
     assert rel_l2(base.apply(g["f"]), g["q"]) <= PARITY
+
+
+def test_cpp_api_example():
+    # include/sbd_b200.hpp used from C++ exactly like the reference API
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(sbd.__file__), "_build", "apply_example")
+    r = subprocess.run([exe, "20000"], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0 and "PASS" in r.stdout
