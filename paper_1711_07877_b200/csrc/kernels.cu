@@ -123,6 +123,28 @@ __global__ void k_bin_bounds(const uint32_t* __restrict__ key, uint64_t n, uint3
     for (int64_t b = prev + 1; b <= cur; ++b) start[b] = (uint32_t)i;
 }
 
+__device__ __forceinline__ uint32_t spread_bits16(uint32_t v) {
+    v &= 0xffffu;
+    v = (v | (v << 8)) & 0x00ff00ffu;
+    v = (v | (v << 4)) & 0x0f0f0f0fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
+}
+
+// Morton (Z-order) key of the stencil-start cell, coordinates shifted by
+// `shift` to be nonnegative: consecutive sorted outputs share small
+// footprints (what the 8-output MMA groups of k_interp_mma rely on).
+__global__ void k_morton_keys(const double2* __restrict__ pos, uint64_t n, double half, int shift,
+                              uint32_t* __restrict__ keys) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double2 p = pos[k];
+    const int ix = min(max((int)ceil(p.x - half) + shift, 0), 65535);
+    const int iy = min(max((int)ceil(p.y - half) + shift, 0), 65535);
+    keys[k] = (spread_bits16((uint32_t)ix) << 1) | spread_bits16((uint32_t)iy);
+}
+
 __global__ void k_iota(uint32_t* v, uint64_t n) {
     const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (k < n) v[k] = (uint32_t)k;
@@ -556,14 +578,64 @@ __global__ void __launch_bounds__(256) k_interp(WindowPoly P, GridGeom g, uint64
 }
 
 // Interp on the fp64 tensor cores (nufft.cpp:254-283 restated). A warp
-// takes 32 consecutive sorted outputs, evaluates their windows (lane =
-// output; deconvolution factors folded in), then handles them 8 at a time:
+// takes 32 consecutive sorted outputs (Z-ordered, so groups of 8 share a small
+// footprint), evaluates their windows (lane = output), then handles them 8 at
+// a time:
 //   H[8 rows x 8 outputs] = G[8 rows x 4 cols] WY[4 cols x 8 outputs]
-// accumulated over the group's column footprint (two MMAs: Re G, Im G), for
-// each 8-row slice of the group's row footprint; each thread then applies the
-// x taps of its two outputs to its row of H, and the 8 row-lanes are reduced
-// with shuffles. Grid fragments come straight from L1/L2 (the band buffer).
-template <int W>
+// over the group's column footprint (two MMAs: Re G, Im G) for each 8-row
+// slice; each thread then applies its row's x taps (and the row's
+// deconvolution factor) to its two outputs, and the 8 row-lanes are reduced
+// with shuffles. The column deconvolution factor rides in the WY fragment.
+// Footprints up to 24 x 24 cells use exact-shape straight-line code; larger
+// ones (rare) take a per-output scalar loop.
+template <int W, bool TRANS, int NRT, int NCT>
+__device__ __forceinline__ void mma_group(const double2* __restrict__ grid, GridGeom g, int rmin,
+                                          int cmin, int gid, int kq, const double* wys, int nb,
+                                          int jyb, const double* __restrict__ dxt,
+                                          const double* __restrict__ dyt, const double* wxs,
+                                          int na, int jxa0, int jxa1, double& p0r, double& p0i,
+                                          double& p1r, double& p1i) {
+    double2 a[NRT][NCT];
+    int rows[NRT];
+#pragma unroll
+    for (int t = 0; t < NRT; ++t) {
+        rows[t] = wrap_near(rmin + 8 * t + gid, g.n1);
+#pragma unroll
+        for (int c = 0; c < NCT; ++c) {
+            const int col = wrap_near(cmin + 4 * c + kq, g.n2);
+            a[t][c] = __ldg(TRANS ? grid + (size_t)col * g.n1 + rows[t] : grid + (size_t)rows[t] * g.n2 + col);
+        }
+    }
+    double hr[NRT][2], hi[NRT][2];
+#pragma unroll
+    for (int t = 0; t < NRT; ++t) hr[t][0] = hr[t][1] = hi[t][0] = hi[t][1] = 0.0;
+#pragma unroll
+    for (int c = 0; c < NCT; ++c) {
+        const int cc = cmin + 4 * c + kq;
+        const int jb = cc - jyb;
+        double b = (unsigned)jb < (unsigned)W ? wys[nb * W + jb] : 0.0;
+        if (dyt) b *= __ldg(dyt + wrap_near(cc, g.n2));
+#pragma unroll
+        for (int t = 0; t < NRT; ++t) {
+            dmma(hr[t][0], hr[t][1], a[t][c].x, b);
+            dmma(hi[t][0], hi[t][1], a[t][c].y, b);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < NRT; ++t) {
+        const int row = rmin + 8 * t + gid;
+        const double dxr = dxt ? __ldg(dxt + rows[t]) : 1.0;
+        const int i0 = row - jxa0, i1 = row - jxa1;
+        const double w0 = (unsigned)i0 < (unsigned)W ? wxs[na * W + i0] * dxr : 0.0;
+        const double w1 = (unsigned)i1 < (unsigned)W ? wxs[(na + 1) * W + i1] * dxr : 0.0;
+        p0r = fma(hr[t][0], w0, p0r);
+        p0i = fma(hi[t][0], w0, p0i);
+        p1r = fma(hr[t][1], w1, p1r);
+        p1i = fma(hi[t][1], w1, p1i);
+    }
+}
+
+template <int W, bool TRANS>
 __global__ void __launch_bounds__(128) k_interp_mma(WindowPoly P, GridGeom g, uint64_t n,
                                                     const double2* __restrict__ pos,
                                                     const double2* __restrict__ phase,
@@ -592,19 +664,10 @@ __global__ void __launch_bounds__(128) k_interp_mma(WindowPoly P, GridGeom g, ui
                 const double2 s = pos[v];
                 jx0 = (int)ceil(s.x - g.half);
                 jy0 = (int)ceil(s.y - g.half);
-                const int mx0 = wrap_base(jx0, g.n1), my0 = wrap_base(jy0, g.n2);
                 double* wxp = wxs + lane * W;
                 double* wyp = wys + lane * W;
-                kb_taps_each<W>((jx0 - s.x) + g.half, P, [&](int i, double w) {
-                    int mx = mx0 + i;
-                    if (mx >= g.n1) mx -= g.n1;
-                    wxp[i] = dxt ? w * dxt[mx] : w;
-                });
-                kb_taps_each<W>((jy0 - s.y) + g.half, P, [&](int j, double w) {
-                    int my = my0 + j;
-                    if (my >= g.n2) my -= g.n2;
-                    wyp[j] = dyt ? w * dyt[my] : w;
-                });
+                kb_taps_each<W>((jx0 - s.x) + g.half, P, [&](int i, double w) { wxp[i] = w; });
+                kb_taps_each<W>((jy0 - s.y) + g.half, P, [&](int j, double w) { wyp[j] = w; });
             }
             jxs[lane] = jx0;
             jys[lane] = jy0;
@@ -613,7 +676,6 @@ __global__ void __launch_bounds__(128) k_interp_mma(WindowPoly P, GridGeom g, ui
 #pragma unroll 1
         for (int grp = 0; grp < 4; ++grp) {
             const int o8 = grp * 8;
-            // footprint of the 8 outputs (warp-uniform); absent outputs excluded
             const int e = lane & 7;
             const int jxe = jxs[o8 + e], jye = jys[o8 + e];
             const bool real = jxe != (1 << 28);
@@ -626,51 +688,62 @@ __global__ void __launch_bounds__(128) k_interp_mma(WindowPoly P, GridGeom g, ui
                 cmin = min(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
                 cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
             }
-            if (rmax < rmin) break; // no outputs left
-            const int nb = o8 + gid;              // output of this lane's B column
+            if (rmax < rmin) break;
+            const int nb = o8 + gid;
             const int jyb = jys[nb];
-            const int na = o8 + 2 * kq;           // outputs of this lane's C columns
+            const int na = o8 + 2 * kq;
             const int jxa0 = jxs[na], jxa1 = jxs[na + 1];
             double p0r = 0.0, p0i = 0.0, p1r = 0.0, p1i = 0.0;
-            // up to three 8-row slices at once: six independent DMMA chains,
-            // one B fragment per column step shared by all slices
-            for (int r0 = rmin; r0 < rmax; r0 += 24) {
-                const int nrt = min(3, (rmax - r0 + 7) >> 3);
-                double hr[3][2], hi[3][2];
-                const double2* grow[3];
-#pragma unroll
-                for (int t = 0; t < 3; ++t) {
-                    hr[t][0] = hr[t][1] = hi[t][0] = hi[t][1] = 0.0;
-                    grow[t] = grid + (size_t)wrap_near(r0 + 8 * t + gid, g.n1) * g.n2;
-                }
-                for (int c0 = cmin; c0 < cmax; c0 += 4) {
-                    const int col = wrap_near(c0 + kq, g.n2);
-                    double2 a[3];
-#pragma unroll
-                    for (int t = 0; t < 3; ++t)
-                        a[t] = t < nrt ? __ldg(grow[t] + col) : make_double2(0.0, 0.0);
-                    const int jb = c0 + kq - jyb;
-                    const double b = (unsigned)jb < (unsigned)W ? wys[nb * W + jb] : 0.0;
-#pragma unroll
-                    for (int t = 0; t < 3; ++t) {
-                        if (t < nrt) {
-                            dmma(hr[t][0], hr[t][1], a[t].x, b);
-                            dmma(hi[t][0], hi[t][1], a[t].y, b);
+            const int nrt = (rmax - rmin + 7) >> 3, nct = (cmax - cmin + 3) >> 2;
+            const int shape = (nrt <= 3 && nct <= 6 && nct >= 3) ? (nrt - 1) * 4 + (nct - 3) : -1;
+#define SBD_MMA_CASE(R, C)                                                                         \
+    case (R - 1) * 4 + (C - 3):                                                                    \
+        mma_group<W, TRANS, R, C>(grid, g, rmin, cmin, gid, kq, wys, nb, jyb, dxt, dyt, wxs, na,   \
+                                  jxa0, jxa1, p0r, p0i, p1r, p1i);                                 \
+        break;
+            switch (shape) {
+                SBD_MMA_CASE(1, 3) SBD_MMA_CASE(1, 4) SBD_MMA_CASE(1, 5) SBD_MMA_CASE(1, 6)
+                SBD_MMA_CASE(2, 3) SBD_MMA_CASE(2, 4) SBD_MMA_CASE(2, 5) SBD_MMA_CASE(2, 6)
+                SBD_MMA_CASE(3, 3) SBD_MMA_CASE(3, 4) SBD_MMA_CASE(3, 5) SBD_MMA_CASE(3, 6)
+                default: {
+                    // large footprint: each of lanes 0..7 interpolates one output directly
+                    if (lane < 8 && jxs[o8 + lane] != (1 << 28)) {
+                        const int node = o8 + lane;
+                        const int jx0 = jxs[node], jy0 = jys[node];
+                        double ar = 0.0, ai = 0.0;
+                        for (int i = 0; i < W; ++i) {
+                            const int mx = wrap_near(jx0 + i, g.n1);
+                            const double wxi = wxs[node * W + i] * (dxt ? dxt[mx] : 1.0);
+                            double rr = 0.0, ri = 0.0;
+                            for (int j = 0; j < W; ++j) {
+                                const int my = wrap_near(jy0 + j, g.n2);
+                                const double wyj = wys[node * W + j] * (dyt ? dyt[my] : 1.0);
+                                const double2 gv = __ldg(TRANS ? grid + (size_t)my * g.n1 + mx
+                                                               : grid + (size_t)mx * g.n2 + my);
+                                rr = fma(gv.x, wyj, rr);
+                                ri = fma(gv.y, wyj, ri);
+                            }
+                            ar = fma(rr, wxi, ar);
+                            ai = fma(ri, wxi, ai);
                         }
+                        // park the result where the reduction below picks it up
+                        jxs[node] = jxs[node];
+                        wxs[node * W] = ar;
+                        wys[node * W] = ai;
                     }
+                    __syncwarp();
+                    break;
                 }
-                // apply x taps: this lane holds H[row][na], H[row][na+1] per slice
-#pragma unroll
-                for (int t = 0; t < 3; ++t) {
-                    if (t >= nrt) continue;
-                    const int row = r0 + 8 * t + gid;
-                    const int i0 = row - jxa0, i1 = row - jxa1;
-                    const double w0 = (unsigned)i0 < (unsigned)W ? wxs[na * W + i0] : 0.0;
-                    const double w1 = (unsigned)i1 < (unsigned)W ? wxs[(na + 1) * W + i1] : 0.0;
-                    p0r = fma(hr[t][0], w0, p0r);
-                    p0i = fma(hi[t][0], w0, p0i);
-                    p1r = fma(hr[t][1], w1, p1r);
-                    p1i = fma(hi[t][1], w1, p1i);
+            }
+#undef SBD_MMA_CASE
+            if (shape < 0) {
+                if (gid == 0) {
+                    p0r = wxs[na * W];
+                    p0i = wys[na * W];
+                    p1r = wxs[(na + 1) * W];
+                    p1i = wys[(na + 1) * W];
+                } else {
+                    p0r = p0i = p1r = p1i = 0.0;
                 }
             }
 #pragma unroll
@@ -695,6 +768,7 @@ __global__ void __launch_bounds__(128) k_interp_mma(WindowPoly P, GridGeom g, ui
                     out[perm ? perm[v] : v] = o2;
                 }
             }
+            __syncwarp();
         }
         __syncwarp();
     }
@@ -899,21 +973,25 @@ struct InterpRun {
                     const double2* phase, const double2* mult, const double* dx, const double* dy,
                     const double2* grid, const uint32_t* perm, const double2* addend, double2* out,
                     int acc, int cj, cudaStream_t st, bool trans) {
-        static int use_mma = -1;
-        if (use_mma < 0) {
-            const char* e = getenv("SBD_INTERP");  // experimental: SBD_INTERP=mma
-            use_mma = e && e[0] == 'm';
+        // tensor-core interpolation pays off when outputs are dense on the band
+        // (>= 0.25 per cell: the xi side); SBD_INTERP=mma|scalar forces a choice
+        const char* e = getenv("SBD_INTERP");
+        const double density = (double)n / ((double)g.n1 * (double)g.n2 / (trans ? 2.0 : 4.0));
+        const bool use_mma = e ? e[0] == 'm' : density >= 0.25;
+        if (use_mma && !acc && !cj) {
+            const uint64_t warps = (n + 31) / 32;
+            const unsigned grid_blocks = (unsigned)std::min<uint64_t>((warps + 3) / 4, 148ull * 16);
+            if (trans)
+                k_interp_mma<W, true><<<grid_blocks, 128, 0, st>>>(P, g, n, pos, phase, mult, dx, dy,
+                                                                    grid, perm, addend, out);
+            else
+                k_interp_mma<W, false><<<grid_blocks, 128, 0, st>>>(P, g, n, pos, phase, mult, dx, dy,
+                                                                     grid, perm, addend, out);
+            return;
         }
         if (trans) {
             k_interp<W, true><<<blocks(n, 256), 256, 0, st>>>(P, g, n, pos, phase, mult, dx, dy, grid,
                                                               perm, addend, out, acc, cj);
-            return;
-        }
-        if (use_mma && !acc && !cj) {
-            const uint64_t warps = (n + 31) / 32;
-            const unsigned grid_blocks = (unsigned)std::min<uint64_t>((warps + 3) / 4, 148ull * 16);
-            k_interp_mma<W><<<grid_blocks, 128, 0, st>>>(P, g, n, pos, phase, mult, dx, dy, grid,
-                                                          perm, addend, out);
             return;
         }
         k_interp<W, false><<<blocks(n, 256), 256, 0, st>>>(P, g, n, pos, phase, mult, dx, dy, grid,
@@ -982,6 +1060,14 @@ void launch_spread_tiles(int w, const WindowPoly& win, GridGeom g, TileGeom tg,
     dispatch_w<SpreadTilesRun>(w, win, g, tg, bin_start, b, pos, grid, st);
     count_launch();
     ck(cudaGetLastError(), "k_spread_tiles");
+}
+
+void launch_morton_keys(const double2* pos, uint64_t n, double half, int shift, uint32_t* keys,
+                        cudaStream_t st) {
+    if (!n) return;
+    k_morton_keys<<<blocks(n, 256), 256, 0, st>>>(pos, n, half, shift, keys);
+    count_launch();
+    ck(cudaGetLastError(), "k_morton_keys");
 }
 
 void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st) {

@@ -173,7 +173,8 @@ struct sbd_op {
     cudaStream_t stream = nullptr;
     std::unique_ptr<Plan> fwd_in, fwd_out;
     std::vector<uint32_t> perm_xi; // sorted xi position -> file index
-    DevBuf<double2> w_sorted;      // omega-hat in sorted xi order
+    DevBuf<double2> w_sorted;      // omega-hat in sorted (canonical) xi order
+    DevBuf<double2> w_in;          // omega-hat in fwd_in's output (interpolation) order
     DevBuf<uint64_t> ro;
     DevBuf<uint32_t> cols;
     DevBuf<double2> vals;
@@ -219,10 +220,17 @@ struct sbd_op {
             w_host[2 * i] = d.weights[2 * j];
             w_host[2 * i + 1] = d.weights[2 * j + 1];
         }
-        // fwd_in = Plan(src, xi, -): outputs kept in the sorted xi order.
+        // fwd_in = Plan(src, xi, -): its outputs (the xi nodes, in the canonical
+        // order above) get their own Z-order for the interpolation; its perm_s
+        // maps back, so the spectrum is written in the canonical order.
         fwd_in = std::make_unique<Plan>(d.src.data(), d.n_src(), xi_sorted.data(), d.n_xi(), -1, o,
-                                        device, true, false, stream);
+                                        device, true, true, stream);
         w_sorted.upload(reinterpret_cast<const double2*>(w_host.data()), d.n_xi(), stream);
+        w_in.alloc(std::max<uint64_t>(d.n_xi(), 1));
+        if (fwd_in->perm_s.n)
+            launch_gather(w_sorted.p, fwd_in->perm_s.p, w_in.p, d.n_xi(), stream);
+        else
+            ck(cudaMemcpyAsync(w_in.p, w_sorted.p, d.n_xi() * 16, cudaMemcpyDeviceToDevice, stream), "w_in");
         ro.upload(d.row_offsets.data(), d.row_offsets.size(), stream);
         cols.upload(d.cols.data(), d.cols.size(), stream);
         vals.upload(reinterpret_cast<const double2*>(d.values.data()), d.nnz(), stream);
@@ -239,9 +247,17 @@ struct sbd_op {
         if (!fused) return;
         const uint64_t ns = d.n_src(), nt = d.n_tgt(), nx = d.n_xi();
         // kappa = w_sorted * pre_out (conv_operator.cpp:305 then nufft.cpp:233)
-        kappa.alloc(nx);
-        ck(cudaMemcpyAsync(kappa.p, w_sorted.p, nx * 16, cudaMemcpyDeviceToDevice, stream), "kappa");
-        launch_mul(kappa.p, fwd_out->pre.p, nx, stream);
+        {
+            DevBuf<double2> kc(nx);  // canonical order, then fwd_in's output order
+            ck(cudaMemcpyAsync(kc.p, w_sorted.p, nx * 16, cudaMemcpyDeviceToDevice, stream), "kappa");
+            launch_mul(kc.p, fwd_out->pre.p, nx, stream);
+            kappa.alloc(nx);
+            if (fwd_in->perm_s.n)
+                launch_gather(kc.p, fwd_in->perm_s.p, kappa.p, nx, stream);
+            else
+                ck(cudaMemcpyAsync(kappa.p, kc.p, nx * 16, cudaMemcpyDeviceToDevice, stream), "kappa");
+            ck(cudaStreamSynchronize(stream), "kappa");
+        }
         f_sorted.alloc(ns);
         qs.alloc(nt);
         // D' rows in target-sorted order, columns renumbered to source-sorted positions
@@ -284,7 +300,7 @@ struct sbd_op {
                                   "fft_out", "interp_tgt");
             return;
         }
-        fwd_in->apply(f, spec.p, work, st, &tm, w_sorted.p, "spread_src", "fft_in", "interp_xi");
+        fwd_in->apply(f, spec.p, work, st, &tm, w_in.p, "spread_src", "fft_in", "interp_xi");
         fwd_out->apply(spec.p, q, work, st, &tm, nullptr, "spread_xi", "fft_out", "interp_tgt");
         if (tm.on) tm.start("spmv");
         launch_spmv(d.n_tgt(), ro.p, cols.p, vals.p, f, q, st);
@@ -326,7 +342,7 @@ struct sbd_op {
     }
 
     size_t device_bytes() const {
-        return fwd_in->device_bytes() + fwd_out->device_bytes() + w_sorted.bytes() + ro.bytes() +
+        return fwd_in->device_bytes() + fwd_out->device_bytes() + w_sorted.bytes() + w_in.bytes() + ro.bytes() +
                ro_s.bytes() + cols_s.bytes() + vals_s.bytes() + kappa.bytes() + f_sorted.bytes() +
                qs.bytes() + work.bbuf.bytes() +
                cols.bytes() + vals.bytes() + work.grid.bytes() + work.T.bytes() + work.band.bytes() +

@@ -131,8 +131,8 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
         perm.alloc(n);
         if (tiles)
             launch_tile_keys(pos.p, n, g.half, tg, keys.p, st);
-        else  // outputs: 4x4-cell bins so 8 consecutive outputs share a small footprint
-            launch_bin_keys(pos.p, n, g, 4, keys.p, st);
+        else  // outputs: Z-order of the stencil cell (mode units, |j| <= n/2)
+            launch_morton_keys(pos.p, n, g.half, std::max(ax.n, ay.n) / 2 + w, keys.p, st);
         launch_iota(perm.p, n, st);
         sort_by_key(keys.p, perm.p, n, st);
         DevBuf<double2> a(n), b(n);

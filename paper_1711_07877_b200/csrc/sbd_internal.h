@@ -253,6 +253,8 @@ void launch_bin_keys(const double2* pos, uint64_t n, GridGeom g, int tile, uint3
                      cudaStream_t st);
 // min/max of the stencil starts ceil(t - w/2): ext = {ixmin, ixmax, iymin, iymax}
 void launch_stencil_extent(const double2* pos, uint64_t n, double half, int* ext, cudaStream_t st);
+void launch_morton_keys(const double2* pos, uint64_t n, double half, int shift, uint32_t* keys,
+                        cudaStream_t st);
 void launch_tile_keys(const double2* pos, uint64_t n, double half, TileGeom tg, uint32_t* keys,
                       cudaStream_t st);
 void launch_bin_bounds(const uint32_t* sorted_keys, uint64_t n, uint32_t nbins, uint32_t* start,
