@@ -15,8 +15,11 @@
 //
 // Offline only: reported, not optimised (north_star).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <complex>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
@@ -147,8 +150,23 @@ void build_ring_quadrature(const std::vector<Ring>& rings, double offset, double
 
 } // namespace
 
+namespace {
+struct PhaseLog {
+    bool on = std::getenv("SBD_VERBOSE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[sbd assemble] %-28s %8.3f s\n", what,
+                     std::chrono::duration<double>(now - t).count());
+        t = now;
+    }
+};
+} // namespace
+
 void assemble_opdata(int kind, double k, const double* src_xy, uint64_t n_src, const double* tgt_xy,
                      uint64_t n_tgt, const sbd_assemble_options& o, OpData& d) {
+    PhaseLog plog;
     if (n_src == 0 || (tgt_xy && n_tgt == 0)) throw Error(SBD_ERR_INVALID_ARGUMENT, "assemble: clouds must be nonempty");
     if (kind != 0 && kind != 1) throw Error(SBD_ERR_INVALID_ARGUMENT, "assemble: unknown kernel kind");
     if (kind == 1 && !(k > 0.0)) throw Error(SBD_ERR_DOMAIN, "kernel_helmholtz: k must be positive");
@@ -183,6 +201,7 @@ void assemble_opdata(int kind, double k, const double* src_xy, uint64_t n_src, c
     }
     if (kind == 1) d.a = std::min(d.a, oscillation_a_cap(k * d.dmax, o.eps));
     d.dmin = d.a * d.dmax;
+    plog.mark("diameter + a");
 
     // ---- spectral model (conv_operator.cpp:79-117)
     const double tol = kSbdToleranceShare * o.eps;
@@ -202,6 +221,18 @@ void assemble_opdata(int kind, double k, const double* src_xy, uint64_t n_src, c
             fk.eval = [kap](double r) { return 0.25 * bessel_y0(kap * r); };
             fk.deriv = [kap](double r) { return -0.25 * kap * bessel_y1(kap * r); };
             fk.oscillation_freq = kap;
+            // Lommel: int r J1(rho r) Y1(kap r) dr = r [kap J1(rho r) Y0(kap r) - rho J0(rho r) Y1(kap r)]
+            // / (rho^2 - kap^2); with G' = -kap Y1(kap r)/4. Exact where the reference's
+            // relative-tolerance quadrature (gram.cpp:69-84) needs up to 2^14 panel doublings
+            // for the nearly cancelling entries.
+            fk.rhs_integral = [kap](double rho, double a) {
+                auto F = [&](double r) {
+                    return r * (kap * bessel_j1(rho * r) * bessel_y0(kap * r) -
+                                rho * bessel_j0(rho * r) * bessel_y1(kap * r)) /
+                           (rho * rho - kap * kap);
+                };
+                return -0.25 * kap * (F(1.0) - F(a));
+            };
             return fk;
         };
         // kernels.cpp:53-66 regime selection
@@ -221,8 +252,10 @@ void assemble_opdata(int kind, double k, const double* src_xy, uint64_t n_src, c
     }
     for (int p = 0; p < fit.P; ++p)
         rings.push_back({fit.roots[p] * fit.radial_scale, std::complex<double>(fit.coeffs[p] * fit.norms[p], 0.0)});
+    plog.mark("SBD fit");
     build_ring_quadrature(rings, fit.constant_offset, o.eps, d);
     for (double& v : d.freqs) v /= dmax;
+    plog.mark("ring quadrature");
 
     d.sbd.a = fit.a;
     d.sbd.P = fit.P;
@@ -263,6 +296,7 @@ void assemble_opdata(int kind, double k, const double* src_xy, uint64_t n_src, c
     ci.device = o.device;
     CloseMatrixOutput co;
     build_close_matrix_gpu(ci, co);
+    plog.mark("close pairs + far field (GPU)");
     d.row_offsets = std::move(co.row_offsets);
     d.cols = std::move(co.cols);
     d.values = std::move(co.values);
@@ -280,6 +314,7 @@ void assemble_opdata(int kind, double k, const double* src_xy, uint64_t n_src, c
                 d.values[2 * i + 1] += -0.25 * bessel_j0(k * rad);
             }
         }
+        plog.mark("Helmholtz kernel values");
     }
 }
 

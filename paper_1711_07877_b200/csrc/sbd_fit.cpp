@@ -13,6 +13,9 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <functional>
 #include <numeric>
@@ -214,6 +217,7 @@ class Workspace {
 
     void ensure(int P) {
         if (P <= cap_) return;
+        const auto t0 = std::chrono::steady_clock::now();
         const int old = cap_;
         cap_ = P;
         basis_ = make_basis(bc_, H_, cap_);
@@ -234,6 +238,9 @@ class Workspace {
         gram_ = assemble_gram(basis_, a_, bc_ == 1 ? H_ : 0.0);
         chol_ = gram_;
         chol_ok_ = gpu_cholesky(chol_, cap_, device_);
+        if (std::getenv("SBD_VERBOSE"))
+            std::fprintf(stderr, "[sbd fit] ensure(P=%d) %.3f s\n", cap_,
+                         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
     }
 
     // Solves the leading P x P system; returns the validation L-inf error.
@@ -292,6 +299,7 @@ class Workspace {
             // r G'(r) = 1 for G = log(dmax r): the integral is (J0(rho a) - J0(rho)) / rho.
             return -2.0 * kPi * c * (bessel_j0(rho * a_) - bessel_j0(rho));
         }
+        if (k_.rhs_integral) return -2.0 * kPi * c * rho * k_.rhs_integral(rho, a_);
         const int panels0 = std::max(4, (int)std::ceil((1.0 - a_) * rho * 10.0 / (2.0 * kPi * 16.0)));
         const double I = integrate([&](double r) { return r * k_.deriv(r) * bessel_j1(rho * r); }, a_, 1.0,
                                    1e-12, panels0);

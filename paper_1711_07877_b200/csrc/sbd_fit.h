@@ -11,6 +11,8 @@ struct FitKernel {
     std::function<double(double)> eval, deriv;
     double oscillation_freq = 0.0;
     bool laplace_rhs = false; // r G'(r) == 1: closed-form right-hand side
+    // optional closed form of int_a^1 r G'(r) J1(rho r) dr (else adaptive GL)
+    std::function<double(double rho, double a)> rhs_integral;
 };
 
 struct SbdFit {
