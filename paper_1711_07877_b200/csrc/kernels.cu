@@ -109,7 +109,7 @@ __global__ void k_tile_keys(const double2* __restrict__ pos, uint64_t n, double 
     const double2 p = pos[k];
     const int rx = (int)ceil(p.x - half) - tg.rlo, ry = (int)ceil(p.y - half) - tg.clo;
     const int bx = rx / tg.tr, by = ry / kTileC;
-    const int sub = ((rx % tg.tr) >> 2) * (kTileC >> 2) + ((ry % kTileC) >> 2);
+    const int sub = (((rx % tg.tr) >> 2) * (kTileC >> 2) + ((ry % kTileC) >> 2)) & 31;
     keys[k] = (((uint32_t)bx * (uint32_t)tg.nby + (uint32_t)by) << 5) | (uint32_t)(sub & 31);
 }
 
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(128, TR == 16 ? 4 : 5) k_spread_tiles(WindowPo
     const int rend = tg.pitch ? tg.rhi : g.n1, cend = tg.pitch ? tg.chi : g.n2;
     const size_t pitch = tg.pitch ? (size_t)tg.pitch : (size_t)g.n2;
     const int r0 = tg.pitch ? tg.rlo : 0, c0 = tg.pitch ? tg.clo : 0;
-    if (col < cend) {
+    if (lane < kTileC && col < cend) {
 #pragma unroll
         for (int r = 0; r < TR; ++r) {
             const int row = X0 + r;
@@ -355,7 +355,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // 256 multiply-adds, which removes the instruction-issue bound of the scalar
 // version; points are sorted by 4x4 sub-tile so a group's footprint is small.
 template <int W>
-__global__ void __launch_bounds__(128) k_spread_mma(WindowPoly P, GridGeom g, TileGeom tg,
+__global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g, TileGeom tg,
                                                     const uint32_t* __restrict__ bin_start,
                                                     const double2* __restrict__ bsorted,
                                                     const double2* __restrict__ pos,
@@ -373,11 +373,12 @@ __global__ void __launch_bounds__(128) k_spread_mma(WindowPoly P, GridGeom g, Ti
     const int bx = tile / tg.nby, by = tile - (tile / tg.nby) * tg.nby;
     const int X0 = tg.rlo + bx * TR, Y0 = tg.clo + by * kTileC;
     const int gid = lane >> 2, kq = lane & 3;
-    double cr[2][4][2], ci[2][4][2];
+    constexpr int NJ = kTileC / 8;
+    double cr[2][NJ][2], ci[2][NJ][2];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+        for (int j = 0; j < NJ; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
 
     // 8 tiles x 32 list entries per warp, after all four warps' queues
     uint32_t* s_list = reinterpret_cast<uint32_t*>(smem + 4 * 96 * W) + 4 * 128 + warp * 256;
@@ -401,10 +402,10 @@ __global__ void __launch_bounds__(128) k_spread_mma(WindowPoly P, GridGeom g, Ti
             kb_taps_each<W>((iy0 - t.y) + g.half, P, [&](int i, double v) { wyp[i] = v; });
         }
         const uint32_t packed = (uint32_t)lane | ((uint32_t)(dx + 64) << 8) | ((uint32_t)(dy + 64) << 16);
-        int cnt[8];
+        int cnt[2 * NJ];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            const int i = t >> 2, j = t & 3;
+        for (int t = 0; t < 2 * NJ; ++t) {
+            const int i = t / NJ, j = t % NJ;
             const bool hit = dx < 8 * i + 8 && dx + W > 8 * i && dy < 8 * j + 8 && dy + W > 8 * j;
             const unsigned m = __ballot_sync(0xffffffffu, hit);
             if (hit) s_list[t * 32 + __popc(m & ((1u << lane) - 1u))] = packed;
@@ -412,8 +413,8 @@ __global__ void __launch_bounds__(128) k_spread_mma(WindowPoly P, GridGeom g, Ti
         }
         __syncwarp();
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-            const int i = t >> 2, j = t & 3;
+        for (int t = 0; t < 2 * NJ; ++t) {
+            const int i = t / NJ, j = t % NJ;
             for (int grp = 0; grp < cnt[t]; grp += 4) {
                 const int idx = grp + kq;
                 double a_r = 0.0, a_i = 0.0, bv = 0.0;
@@ -477,7 +478,7 @@ __global__ void __launch_bounds__(128) k_spread_mma(WindowPoly P, GridGeom g, Ti
         const int row = X0 + 8 * i + gid;
         if (row >= rend) continue;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < NJ; ++j) {
             const int col = Y0 + 8 * j + 2 * kq;
             double2* dst = grid + (size_t)(row - r0) * pitch + (col - c0);
             if (col < cend) dst[0] = make_double2(cr[i][j][0], ci[i][j][0]);

@@ -135,7 +135,7 @@ struct FftWork {
 // Spread tiles of the pruned forward path: one warp owns kTileR x kTileC
 // grid cells (lanes = columns, rows in registers).
 constexpr int kTileR = 16;
-constexpr int kTileC = 32;
+constexpr int kTileC = 16;
 struct TileGeom {
     int rlo, clo, nbx, nby;
     int tr;              // rows per tile (8 or 16)
