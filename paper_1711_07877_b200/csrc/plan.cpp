@@ -164,23 +164,36 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
         tg.pitch = 0;
         tg.rhi = rhi;
         tg.chi = chi;
-        const char* fe = std::getenv("SBD_FFT");  // dft | cufft | (default) cufft-transposed
+        // SBD_FFT: dft | dft-strict (error when the grid is unsupported) | cufft |
+        // (default) cufft-transposed; SBD_DFT_R3="r[,r]" forces the last radix
+        const char* fe = std::getenv("SBD_FFT");
         const bool want_dft = fe && fe[0] == 'd';
+        int f1 = 0, f2 = 0;
+        if (const char* r3 = std::getenv("SBD_DFT_R3")) {
+            f1 = f2 = std::atoi(r3);
+            if (const char* c2 = std::strchr(r3, ',')) f2 = std::atoi(c2 + 1);
+        }
         const int R = rhi - rlo, C = chi - clo;
-        if (want_dft && make_pruned_pass(ay.n, clo, C, R, pass1) &&
-            make_pruned_pass(ax.n, rlo, R, pass1.B, pass2)) {
+        const bool dft_ok = want_dft && make_pruned_pass(ay.n, clo, C, R, f1, pass1) &&
+                            make_pruned_pass(ax.n, rlo, R, pass1.B, f2, pass2);
+        if (want_dft && !dft_ok && std::strcmp(fe, "dft-strict") == 0)
+            throw Error(3, "pruned dft: grid " + std::to_string(ax.n) + "x" + std::to_string(ay.n) +
+                               " unsupported");
+        if (dft_ok) {
             dft = true;
             tg.pitch = C;
             pass1.in_row = C;
             pass1.in_elem = 1;
-            pass1.out_row = pass1.B;
-            pass1.out_elem = 1;
-            pass2.in_row = 1;
-            pass2.in_elem = pass1.B;
+            // pass 1 stores its band outputs column-major (T1[c][r], c < B1) so
+            // that pass 2 reads contiguous sequences too
+            pass1.out_row = 1;
+            pass1.out_elem = R;
+            pass2.in_row = R;
+            pass2.in_elem = 1;
             pass2.out_row = pass2.B;
             pass2.out_elem = 1;
-            tw1 = make_twiddles(ay.n, st);
-            tw2 = make_twiddles(ax.n, st);
+            tw1 = make_twiddles(pass1, st);
+            tw2 = make_twiddles(pass2, st);
             band1 = pass2.b;
             b1c = pass2.B;
             std::vector<double> hb(b1c);

@@ -237,3 +237,58 @@ def test_cpp_api_example():
     r = subprocess.run([exe, "20000"], capture_output=True, text=True, timeout=300)
     print(r.stdout)
     assert r.returncode == 0 and "PASS" in r.stdout
+
+
+def _grid_plan_inputs(nx, ny, tol, rng, n=20000):
+    # points in [-1, 1]^2 (X = 1, gamma = 2 / pi) and frequency half-extents S
+    # chosen so that ceil(2 sigma (gamma S + w/2 + 1)) = n_axis - 4, which
+    # next_fast_even rounds up to n_axis for the sizes used below
+    w = min(max(int(np.ceil(-np.log10(tol))) + 2, 4), 17)
+    gamma = 2.0 / np.pi
+
+    def s_for(na):
+        return ((na - 4) / 4.0 - 0.5 * w - 1.0 - 1e-3) / gamma
+
+    sx, sy = s_for(nx), s_for(ny)
+    pts = rng.uniform(-1, 1, (n, 2))
+    pts[:4] = [[-1, -1], [1, 1], [-1, 1], [1, -1]]
+    frq = np.stack([rng.uniform(-sx, sx, n + 7), rng.uniform(-sy, sy, n + 7)], 1)
+    frq[:2] = [[-sx, -sy], [sx, sy]]
+    c = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    return pts, frq, c
+
+
+@pytest.mark.parametrize("nx,ny,r3", [(2304, 2304, "9"), (2304, 2304, "3"), (7680, 12288, "16,10"),
+                                      (7680, 12288, "12,15"), (7680, 12288, "8,6"),
+                                      (7680, 12288, "4,5"), (7680, 12288, "2,2"),
+                                      (7680, 12288, ""), (4608, 4608, "18")])
+def test_band_dft_radix_variants(nx, ny, r3, monkeypatch):
+    # every k_band_dft instantiation (N = 256 R3, decimation D = n / N) against
+    # the cuFFT row/column path and the direct sum
+    rng = np.random.default_rng(nx + ny + len(r3))
+    tol = 1e-8
+    pts, frq, c = _grid_plan_inputs(nx, ny, tol, rng)
+    opts = sbd.NufftOptions(tol=tol, mode="fast")
+    for sign in (1, -1):
+        base = sbd.NufftPlan(pts, frq, sign, opts)
+        assert base._meta()[2:] == (nx, ny)
+        monkeypatch.setenv("SBD_FFT", "dft-strict")
+        if r3:
+            monkeypatch.setenv("SBD_DFT_R3", r3)
+        plan = sbd.NufftPlan(pts, frq, sign, opts)
+        monkeypatch.delenv("SBD_FFT")
+        monkeypatch.delenv("SBD_DFT_R3", raising=False)
+        got, want = plan.apply(c), base.apply(c)
+        assert rel_l2(got, want) <= 1e-13
+        sub = rng.choice(len(frq), 2000, replace=False)
+        d = sbd.ndft_direct(pts, frq[sub], c, sign)
+        assert np.max(np.abs(got[sub] - d)) <= tol * np.abs(c).sum()
+
+
+def test_band_dft_strict_rejects_unsupported_grid(monkeypatch):
+    rng = np.random.default_rng(5)
+    pts, frq, _ = _grid_plan_inputs(2304, 2304, 1e-8, rng, n=100)
+    monkeypatch.setenv("SBD_FFT", "dft-strict")
+    monkeypatch.setenv("SBD_DFT_R3", "16")  # 4096 does not divide 2304
+    with pytest.raises(sbd.SbdError, match="unsupported"):
+        sbd.NufftPlan(pts, frq, 1, sbd.NufftOptions(tol=1e-8, mode="fast"))
