@@ -775,6 +775,263 @@ __global__ void __launch_bounds__(128) k_interp_mma(WindowPoly P, GridGeom g, ui
     }
 }
 
+// ---- tile-staged tensor-core interpolation -------------------------------
+// Outputs are Z-ordered by stencil cell, so the outputs whose stencil starts
+// in one 32 x 32 cell block are contiguous ("tiles", starts built at plan
+// time). One CTA stages the block's (32 + W - 1)^2 footprint of the grid,
+// pre-multiplied by the row and column deconvolution factors, into shared
+// memory once; its warps then run the 8-output MMA groups of k_interp_mma
+// from shared memory. The grid is read from L2 once per tile instead of once
+// per 8-output group.
+constexpr int kIT = 32;  // tile edge (Morton level 5)
+
+template <int W, bool TRANS>
+struct ITile {
+    static constexpr int E = kIT + W - 1;  // footprint edge
+    static constexpr int RE = E + 7;       // rows incl. the zero rows an 8-row MMA slice may touch
+    static constexpr int CE = E + 3;       // cols incl. the zero cols a 4-col MMA slice may touch
+    // [col][row] (TRANS) or [row][col] layout, pitch chosen so the 8 x 4 cell
+    // reads of one quarter-warp hit distinct 16-byte bank groups
+    static constexpr int ext = TRANS ? RE : CE;
+    static constexpr int mod = TRANS ? 2 : 4;
+    static constexpr int P = ext + ((mod - ext % 8) + 8) % 8;
+    static constexpr int cells = (TRANS ? CE : RE) * P;
+    static constexpr size_t smem = (size_t)cells * sizeof(double2) + 2 * 4 * 32 * W * sizeof(double);
+    __device__ static int at(int r, int c) { return TRANS ? c * P + r : r * P + c; }
+};
+
+template <int W, bool TRANS, int NRT, int NCT>
+__device__ __forceinline__ void mma_group_s(const double2* __restrict__ S, int rl, int cl, int gid,
+                                            int kq, const double* wys, int nb, int jyl,
+                                            const double* wxs, int na, int jxl0, int jxl1,
+                                            double& p0r, double& p0i, double& p1r, double& p1i) {
+    using TT = ITile<W, TRANS>;
+    double hr[NRT][2], hi[NRT][2];
+#pragma unroll
+    for (int t = 0; t < NRT; ++t) hr[t][0] = hr[t][1] = hi[t][0] = hi[t][1] = 0.0;
+#pragma unroll
+    for (int c = 0; c < NCT; ++c) {
+        const int cc = cl + 4 * c + kq;
+        const int jb = cc - jyl;
+        const double b = (unsigned)jb < (unsigned)W ? wys[nb * W + jb] : 0.0;
+#pragma unroll
+        for (int t = 0; t < NRT; ++t) {
+            const double2 a = S[TT::at(rl + 8 * t + gid, cc)];
+            dmma(hr[t][0], hr[t][1], a.x, b);
+            dmma(hi[t][0], hi[t][1], a.y, b);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < NRT; ++t) {
+        const int row = rl + 8 * t + gid;
+        const int i0 = row - jxl0, i1 = row - jxl1;
+        const double w0 = (unsigned)i0 < (unsigned)W ? wxs[na * W + i0] : 0.0;
+        const double w1 = (unsigned)i1 < (unsigned)W ? wxs[(na + 1) * W + i1] : 0.0;
+        p0r = fma(hr[t][0], w0, p0r);
+        p0i = fma(hi[t][0], w0, p0i);
+        p1r = fma(hr[t][1], w1, p1r);
+        p1i = fma(hi[t][1], w1, p1i);
+    }
+}
+
+template <int W, bool TRANS>
+__global__ void __launch_bounds__(128) k_interp_tile(
+    WindowPoly P, GridGeom g, const uint32_t* __restrict__ tstart, uint32_t ntiles, int shift,
+    uint64_t out_lo, uint64_t n, const double2* __restrict__ pos, const double2* __restrict__ phase,
+    const double2* __restrict__ mult, const double* __restrict__ dxt, const double* __restrict__ dyt,
+    const double2* __restrict__ grid, const uint32_t* __restrict__ perm,
+    const double2* __restrict__ addend, double2* __restrict__ out) {
+    using TT = ITile<W, TRANS>;
+    extern __shared__ __align__(16) double sm_it[];
+    double2* S = reinterpret_cast<double2*>(sm_it);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = lane >> 2, kq = lane & 3;
+    double* wxs = sm_it + 2 * TT::cells + warp * 2 * 32 * W;
+    double* wys = wxs + 32 * W;
+    __shared__ int s_jx[4][32], s_jy[4][32];
+    __shared__ double s_fx[TT::RE], s_fy[TT::CE];
+    int* jxs = s_jx[warp];
+    int* jys = s_jy[warp];
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        // tile range in sorted order, clipped to this call's output range
+        const uint64_t t0 = tstart[tile], t1 = tstart[tile + 1];
+        const uint64_t a0 = t0 > out_lo ? t0 : out_lo, a1 = t1 < out_lo + n ? t1 : out_lo + n;
+        if (a0 >= a1) continue;
+        const double2 s0 = pos[a0 - out_lo];
+        const int X0 = (((int)ceil(s0.x - g.half) + shift) & ~(kIT - 1)) - shift;
+        const int Y0 = (((int)ceil(s0.y - g.half) + shift) & ~(kIT - 1)) - shift;
+        __syncthreads();  // previous tile's readers are done
+        // deconvolution factors of the tile's rows and columns
+        for (int i = threadIdx.x; i < TT::RE + TT::CE; i += blockDim.x) {
+            if (i < TT::RE)
+                s_fx[i] = (i < TT::E && dxt) ? __ldg(dxt + wrap_near(X0 + i, g.n1)) : 1.0;
+            else
+                s_fy[i - TT::RE] = (i - TT::RE < TT::E && dyt) ? __ldg(dyt + wrap_near(Y0 + i - TT::RE, g.n2)) : 1.0;
+        }
+        __syncthreads();
+        // footprint -> shared memory, eight loads in flight per thread
+        constexpr int kB = 8;
+        for (int ib = 0; ib < TT::cells; ib += kB * 128) {
+            double2 v[kB];
+#pragma unroll
+            for (int u = 0; u < kB; ++u) {
+                const int i = ib + u * 128 + threadIdx.x;
+                const int q = i / TT::P, rr = i - q * TT::P;
+                const int r = TRANS ? rr : q, c = TRANS ? q : rr;
+                v[u] = make_double2(0.0, 0.0);
+                if (i < TT::cells && r < TT::E && c < TT::E) {
+                    const int gr = wrap_near(X0 + r, g.n1), gc = wrap_near(Y0 + c, g.n2);
+                    v[u] = __ldg(TRANS ? grid + (size_t)gc * g.n1 + gr : grid + (size_t)gr * g.n2 + gc);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kB; ++u) {
+                const int i = ib + u * 128 + threadIdx.x;
+                if (i < TT::cells) {
+                    const int q = i / TT::P, rr = i - q * TT::P;
+                    const int r = TRANS ? rr : q, c = TRANS ? q : rr;
+                    const double f = (r < TT::RE ? s_fx[r] : 1.0) * (c < TT::CE ? s_fy[c] : 1.0);
+                    S[i] = make_double2(v[u].x * f, v[u].y * f);
+                }
+            }
+        }
+        __syncthreads();
+        for (uint64_t base = a0 + 32 * warp; base < a1; base += 128) {
+            // this lane's output: position now, epilogue operands prefetched
+            const uint64_t vmy = base + lane;
+            const bool mine = vmy < a1;
+            const uint64_t vr = mine ? vmy - out_lo : 0;
+            double2 sv = make_double2(0.0, 0.0), ph = sv, mu = make_double2(1.0, 0.0), ad = sv;
+            uint32_t dst = 0;
+            if (mine) {
+                sv = pos[vr];
+                ph = phase[vr];
+                if (mult) mu = mult[vr];
+                if (addend) ad = addend[vr];
+                dst = perm ? perm[vr] : (uint32_t)vr;
+            }
+            {
+                int jx0 = 1 << 28, jy0 = 1 << 28;
+                if (mine) {
+                    const int ix = (int)ceil(sv.x - g.half), iy = (int)ceil(sv.y - g.half);
+                    double* wxp = wxs + lane * W;
+                    double* wyp = wys + lane * W;
+                    kb_taps_each<W>((ix - sv.x) + g.half, P, [&](int i, double w) { wxp[i] = w; });
+                    kb_taps_each<W>((iy - sv.y) + g.half, P, [&](int j, double w) { wyp[j] = w; });
+                    jx0 = ix - X0;  // tile-local stencil start, in [0, 32)
+                    jy0 = iy - Y0;
+                }
+                jxs[lane] = jx0;
+                jys[lane] = jy0;
+            }
+            __syncwarp();
+            double accr = 0.0, acci = 0.0;  // this lane's output after the group loop
+#pragma unroll 1
+            for (int grp = 0; grp < 4; ++grp) {
+                const int o8 = grp * 8;
+                const int e = lane & 7;
+                const int jxe = jxs[o8 + e], jye = jys[o8 + e];
+                const bool real = jxe != (1 << 28);
+                int rmin = real ? jxe : 1 << 29, rmax = real ? jxe + W : -(1 << 29);
+                int cmin = real ? jye : 1 << 29, cmax = real ? jye + W : -(1 << 29);
+#pragma unroll
+                for (int o = 1; o <= 4; o <<= 1) {
+                    rmin = min(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
+                    rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+                    cmin = min(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+                    cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+                }
+                if (rmax < rmin) break;
+                const int nb = o8 + gid;
+                const int jyl = jys[nb];
+                const int na = o8 + 2 * kq;
+                const int jxl0 = jxs[na], jxl1 = jxs[na + 1];
+                double p0r = 0.0, p0i = 0.0, p1r = 0.0, p1i = 0.0;
+                const int nrt = (rmax - rmin + 7) >> 3, nct = (cmax - cmin + 3) >> 2;
+                const int shape = (nrt <= 3 && nct <= 6 && nct >= 3) ? (nrt - 1) * 4 + (nct - 3) : -1;
+#define SBD_MMA_CASE(R, C)                                                                         \
+    case (R - 1) * 4 + (C - 3):                                                                    \
+        mma_group_s<W, TRANS, R, C>(S, rmin, cmin, gid, kq, wys, nb, jyl, wxs, na, jxl0, jxl1, p0r, \
+                                    p0i, p1r, p1i);                                                \
+        break;
+                switch (shape) {
+                    SBD_MMA_CASE(1, 3) SBD_MMA_CASE(1, 4) SBD_MMA_CASE(1, 5) SBD_MMA_CASE(1, 6)
+                    SBD_MMA_CASE(2, 3) SBD_MMA_CASE(2, 4) SBD_MMA_CASE(2, 5) SBD_MMA_CASE(2, 6)
+                    SBD_MMA_CASE(3, 3) SBD_MMA_CASE(3, 4) SBD_MMA_CASE(3, 5) SBD_MMA_CASE(3, 6)
+                    default: {
+                        // wide group: lanes 0..7 each interpolate one output from the tile
+                        double ar = 0.0, ai = 0.0;
+                        if (lane < 8 && jxs[o8 + lane] != (1 << 28)) {
+                            const int node = o8 + lane;
+                            const int jx0 = jxs[node], jy0 = jys[node];
+                            for (int i = 0; i < W; ++i) {
+                                double rr = 0.0, ri = 0.0;
+                                for (int j = 0; j < W; ++j) {
+                                    const double2 gv = S[TT::at(jx0 + i, jy0 + j)];
+                                    const double wyj = wys[node * W + j];
+                                    rr = fma(gv.x, wyj, rr);
+                                    ri = fma(gv.y, wyj, ri);
+                                }
+                                ar = fma(rr, wxs[node * W + i], ar);
+                                ai = fma(ri, wxs[node * W + i], ai);
+                            }
+                        }
+                        // lanes 0..7 hold outputs o8 + lane: hand them to the owners
+                        ar = __shfl_sync(0xffffffffu, ar, lane & 7);
+                        ai = __shfl_sync(0xffffffffu, ai, lane & 7);
+                        if ((lane >> 3) == grp) {
+                            accr = ar;
+                            acci = ai;
+                        }
+                        break;
+                    }
+                }
+#undef SBD_MMA_CASE
+                if (shape >= 0) {
+#pragma unroll
+                    for (int o = 4; o <= 16; o <<= 1) {
+                        p0r += __shfl_xor_sync(0xffffffffu, p0r, o);
+                        p0i += __shfl_xor_sync(0xffffffffu, p0i, o);
+                        p1r += __shfl_xor_sync(0xffffffffu, p1r, o);
+                        p1i += __shfl_xor_sync(0xffffffffu, p1i, o);
+                    }
+                    // lanes kq = 0..3 now hold outputs o8 + 2 kq (+1): hand them to the owners
+                    const int src = (lane & 7) >> 1;
+                    const double r0 = __shfl_sync(0xffffffffu, p0r, src), i0 = __shfl_sync(0xffffffffu, p0i, src);
+                    const double r1 = __shfl_sync(0xffffffffu, p1r, src), i1 = __shfl_sync(0xffffffffu, p1i, src);
+                    if ((lane >> 3) == grp) {
+                        accr = (lane & 1) ? r1 : r0;
+                        acci = (lane & 1) ? i1 : i0;
+                    }
+                }
+            }
+            if (mine) {
+                double2 o2 = cmul(make_double2(accr, acci), ph);
+                if (mult) o2 = cmul(o2, mu);
+                o2.x += ad.x;
+                o2.y += ad.y;
+                out[dst] = o2;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// tile t of the Z-ordered outputs = sorted positions [start[t], start[t+1])
+__global__ void k_tile_flags(const uint32_t* __restrict__ key, uint64_t n, int bits,
+                             uint32_t* __restrict__ flag) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    flag[i] = (i == 0 || (key[i] >> bits) != (key[i - 1] >> bits)) ? 1u : 0u;
+}
+__global__ void k_tile_scatter(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ idx,
+                               uint64_t n, uint32_t* __restrict__ start) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (flag[i]) start[idx[i]] = (uint32_t)i;
+    if (i == n - 1) start[idx[i] + flag[i]] = (uint32_t)n;
+}
+
 // Direct sum (nufft.cpp:76-93): thread per output, sequential over points in
 // the caller's order (same summation order as the reference).
 __global__ void k_ndft(const double2* __restrict__ pts, uint64_t np,
@@ -973,12 +1230,36 @@ struct InterpRun {
     static void run(const WindowPoly& P, GridGeom g, uint64_t n, const double2* pos,
                     const double2* phase, const double2* mult, const double* dx, const double* dy,
                     const double2* grid, const uint32_t* perm, const double2* addend, double2* out,
-                    int acc, int cj, cudaStream_t st, bool trans) {
+                    int acc, int cj, cudaStream_t st, bool trans, const InterpTiles* tiles) {
         // tensor-core interpolation pays off when outputs are dense on the band
-        // (>= 0.25 per cell: the xi side); SBD_INTERP=mma|scalar forces a choice
+        // (>= 0.25 per cell: the xi side); SBD_INTERP=tile|mma|scalar forces a
+        // choice (tile: the shared-memory staged variant, needs the tile list)
         const char* e = getenv("SBD_INTERP");
         const double density = (double)n / ((double)g.n1 * (double)g.n2 / (trans ? 2.0 : 4.0));
-        const bool use_mma = e ? e[0] == 'm' : density >= 0.25;
+        const bool use_mma = e ? (e[0] == 'm' || e[0] == 't') : density >= 0.25;
+        const bool use_tile = use_mma && tiles && tiles->n && !(e && e[0] == 'm');
+        if (use_tile && !acc && !cj) {
+            auto go = [&](auto kern, size_t smem, size_t& attr) {
+                if (smem > attr) {
+                    ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                       "interp tile smem");
+                    attr = smem;
+                }
+                int dev = 0, sms = 148, per = 1;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 128, smem);
+                const unsigned nb = (unsigned)std::min<uint64_t>(tiles->n, (uint64_t)sms * std::max(per, 1) * 8);
+                kern<<<nb, 128, smem, st>>>(P, g, tiles->start, tiles->n, tiles->shift, tiles->out_lo, n, pos,
+                                            phase, mult, dx, dy, grid, perm, addend, out);
+            };
+            static size_t attr_t = 0, attr_n = 0;  // per W (this template)
+            if (trans)
+                go(k_interp_tile<W, true>, ITile<W, true>::smem, attr_t);
+            else
+                go(k_interp_tile<W, false>, ITile<W, false>::smem, attr_n);
+            return;
+        }
         if (use_mma && !acc && !cj) {
             const uint64_t warps = (n + 31) / 32;
             const unsigned grid_blocks = (unsigned)std::min<uint64_t>((warps + 3) / 4, 148ull * 16);
@@ -1116,12 +1397,34 @@ void launch_spread(int w, const WindowPoly& win, GridGeom g, uint64_t n, const u
 void launch_interp(int w, const WindowPoly& win, GridGeom g, uint64_t n, const double2* pos,
                    const double2* phase, const double2* mult, const double* dx, const double* dy,
                    const double2* grid, const uint32_t* perm, double2* out, int accumulate,
-                   int conj_out, cudaStream_t st, const double2* addend, bool transposed) {
+                   int conj_out, cudaStream_t st, const double2* addend, bool transposed,
+                   const InterpTiles* tiles) {
     if (!n) return;
     dispatch_w<InterpRun>(w, win, g, n, pos, phase, mult, dx, dy, grid, perm, addend, out,
-                          accumulate, conj_out, st, transposed);
+                          accumulate, conj_out, st, transposed, tiles);
     count_launch();
     ck(cudaGetLastError(), "k_interp");
+}
+
+void build_tile_starts(const uint32_t* sorted_keys, uint64_t n, int bits, DevBuf<uint32_t>& start,
+                       uint32_t& ntiles, cudaStream_t st) {
+    ntiles = 0;
+    if (!n) return;
+    DevBuf<uint32_t> flag(n), idx(n);
+    k_tile_flags<<<blocks(n, 256), 256, 0, st>>>(sorted_keys, n, bits, flag.p);
+    size_t tmp = 0;
+    ck(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag.p, idx.p, (int)n, st), "tile scan (size)");
+    DevBuf<unsigned char> t(tmp);
+    ck(cub::DeviceScan::ExclusiveSum(t.p, tmp, flag.p, idx.p, (int)n, st), "tile scan");
+    uint32_t last[2];
+    ck(cudaMemcpyAsync(&last[0], idx.p + n - 1, 4, cudaMemcpyDeviceToHost, st), "tile count");
+    ck(cudaMemcpyAsync(&last[1], flag.p + n - 1, 4, cudaMemcpyDeviceToHost, st), "tile count");
+    ck(cudaStreamSynchronize(st), "tile count");
+    ntiles = last[0] + last[1];
+    start.alloc((size_t)ntiles + 1);
+    k_tile_scatter<<<blocks(n, 256), 256, 0, st>>>(flag.p, idx.p, n, start.p);
+    count_launch(4);
+    ck(cudaStreamSynchronize(st), "tile starts");
 }
 
 void launch_ndft(const double2* pts, uint64_t np, const double2* frq, uint64_t nf,

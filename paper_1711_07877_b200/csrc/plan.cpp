@@ -144,6 +144,10 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
             const uint32_t nbins = (uint32_t)tg.nbx * (uint32_t)tg.nby;
             bin_start.alloc(nbins + 1);
             launch_bin_bounds(keys.p, n, nbins, bin_start.p, st);
+        } else {
+            // 32 x 32 blocks of the Z order (k_interp_tile)
+            out_shift = std::max(ax.n, ay.n) / 2 + w;
+            build_tile_starts(keys.p, n, 10, out_tiles, n_out_tiles, st);
         }
         ck(cudaStreamSynchronize(st), "sort side");
     };
@@ -351,6 +355,11 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
     const uint32_t* perm_p = perm_s.n ? perm_s.p + out_lo : nullptr;
     double2* out_p = perm_s.n ? out : out + out_lo;
     if (!pruned) throw Error(3, "apply_pruned on a plan without the pruned path");
+    InterpTiles otiles;
+    otiles.start = out_tiles.p;
+    otiles.n = n_out_tiles;
+    otiles.shift = out_shift;
+    otiles.out_lo = out_lo;
     ensure_work(wk, st);
     const GridGeom g{ax.n, ay.n, 0.5 * w};
     const int n2 = ay.n;
@@ -379,7 +388,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         if (tm) tm->start(tag_interp);
         const GridGeom gt{b1c, bc, 0.5 * w};
         launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx_band.p, dy_band.p, wk.bandT.p, perm_p,
-                      out_p, 0, 0, st, add_p, /*transposed=*/true);
+                      out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles);
         if (tm) tm->stop();
         return;
     }
@@ -431,7 +440,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         if (tm) tm->start(tag_interp);
         const GridGeom gt{ax.n, bc, 0.5 * w};
         launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx.p, dy_band.p, wk.bandT.p, perm_p,
-                      out_p, 0, 0, st, add_p, /*transposed=*/true);
+                      out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles);
         if (tm) tm->stop();
         return;
     }
@@ -445,7 +454,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
     if (tm) tm->start(tag_interp);
     const GridGeom gb{ax.n, bc, 0.5 * w};
     launch_interp(w, win, gb, nout, s_p, post_p, mult_p, dx.p, dy_band.p, wk.band.p, perm_p, out_p, 0,
-                  0, st, add_p);
+                  0, st, add_p, false, &otiles);
     if (tm) tm->stop();
 }
 

@@ -195,6 +195,9 @@ class Plan {
     int rlo = 0, rhi = 0, clo = 0, chi = 0; // region written by the spread tiles
     TileGeom tg{};
     DevBuf<uint32_t> bin_start;
+    DevBuf<uint32_t> out_tiles;  // Z-order block starts of the sorted outputs
+    uint32_t n_out_tiles = 0;
+    int out_shift = 0;
     int band2 = 0, bc = 0;
     DevBuf<double> dy_band;
     cufftHandle fft_row = 0, fft_colA = 0, fft_colB = 0;
@@ -283,11 +286,23 @@ void launch_spread(int w, const WindowPoly& win, GridGeom g, uint64_t n, const u
                    const double2* mult, const double* dx, const double* dy, double2* grid,
                    int conj_in, cudaStream_t st);
 // interp: out[perm?perm[k]:k] (+)= sum taps * (dx dy) * grid * phase[k] (* mult[k])
+// Z-ordered outputs grouped by 32 x 32 stencil-cell block (k_interp_tile):
+// block t = sorted positions [start[t], start[t+1]); out_lo = the absolute
+// sorted index of the call's first output
+struct InterpTiles {
+    const uint32_t* start = nullptr;
+    uint32_t n = 0;
+    int shift = 0;
+    uint64_t out_lo = 0;
+};
 void launch_interp(int w, const WindowPoly& win, GridGeom g, uint64_t n, const double2* pos,
                    const double2* phase, const double2* mult, const double* dx, const double* dy,
                    const double2* grid, const uint32_t* perm, double2* out, int accumulate,
                    int conj_out, cudaStream_t st, const double2* addend = nullptr,
-                   bool transposed = false);
+                   bool transposed = false, const InterpTiles* tiles = nullptr);
+// sorted keys -> starts of the runs of equal key >> bits
+void build_tile_starts(const uint32_t* sorted_keys, uint64_t n, int bits, DevBuf<uint32_t>& start,
+                       uint32_t& ntiles, cudaStream_t st);
 // direct sum out[v] = sum_k c_k e^{i sign z_k . f_v}
 void launch_ndft(const double2* pts, uint64_t np, const double2* frq, uint64_t nf,
                  const double2* c, int sign, double2* out, cudaStream_t st);
