@@ -103,24 +103,25 @@ __global__ void k_stencil_extent(const double2* __restrict__ pos, uint64_t n, do
 // consecutive in the sorted order are within a few cells of each other, which
 // is what makes 4-point MMA groups compact in the DMMA spread.
 __global__ void k_tile_keys(const double2* __restrict__ pos, uint64_t n, double half, TileGeom tg,
-                            uint32_t* __restrict__ keys) {
+                            uint32_t* __restrict__ keys, const uint8_t* __restrict__ tag) {
     const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (k >= n) return;
     const double2 p = pos[k];
     const int rx = (int)ceil(p.x - half) - tg.rlo, ry = (int)ceil(p.y - half) - tg.clo;
     const int bx = rx / tg.tr, by = ry / kTileC;
     const int sub = (((rx % tg.tr) >> 2) * (kTileC >> 2) + ((ry % kTileC) >> 2)) & 31;
-    keys[k] = (((uint32_t)bx * (uint32_t)tg.nby + (uint32_t)by) << 5) | (uint32_t)(sub & 31);
+    keys[k] = (((uint32_t)bx * (uint32_t)tg.nby + (uint32_t)by) << 5) | (uint32_t)(sub & 31) |
+              (tag && tag[k] ? 0x80000000u : 0u);
 }
 
 // start[b] = first sorted position with key >= b, for b in [0, nbins]
 __global__ void k_bin_bounds(const uint32_t* __restrict__ key, uint64_t n, uint32_t nbins,
-                             uint32_t* __restrict__ start) {
+                             uint32_t* __restrict__ start, uint32_t base, uint32_t mask) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i > n) return;
-    const int64_t prev = i > 0 ? (int64_t)(key[i - 1] >> 5) : -1;
-    const int64_t cur = i < n ? (int64_t)(key[i] >> 5) : (int64_t)nbins;
-    for (int64_t b = prev + 1; b <= cur; ++b) start[b] = (uint32_t)i;
+    const int64_t prev = i > 0 ? (int64_t)((key[i - 1] & mask) >> 5) : -1;
+    const int64_t cur = i < n ? (int64_t)((key[i] & mask) >> 5) : (int64_t)nbins;
+    for (int64_t b = prev + 1; b <= cur; ++b) start[b] = base + (uint32_t)i;
 }
 
 __device__ __forceinline__ uint32_t spread_bits16(uint32_t v) {
@@ -136,13 +137,15 @@ __device__ __forceinline__ uint32_t spread_bits16(uint32_t v) {
 // `shift` to be nonnegative: consecutive sorted outputs share small
 // footprints (what the 8-output MMA groups of k_interp_mma rely on).
 __global__ void k_morton_keys(const double2* __restrict__ pos, uint64_t n, double half, int shift,
-                              uint32_t* __restrict__ keys) {
+                              uint32_t* __restrict__ keys, const uint8_t* __restrict__ tag) {
     const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (k >= n) return;
     const double2 p = pos[k];
-    const int ix = min(max((int)ceil(p.x - half) + shift, 0), 65535);
-    const int iy = min(max((int)ceil(p.y - half) + shift, 0), 65535);
-    keys[k] = (spread_bits16((uint32_t)ix) << 1) | spread_bits16((uint32_t)iy);
+    const int cap = tag ? 32767 : 65535;
+    const int ix = min(max((int)ceil(p.x - half) + shift, 0), cap);
+    const int iy = min(max((int)ceil(p.y - half) + shift, 0), cap);
+    keys[k] = (spread_bits16((uint32_t)ix) << 1) | spread_bits16((uint32_t)iy) |
+              (tag && tag[k] ? 0x80000000u : 0u);
 }
 
 __global__ void k_iota(uint32_t* v, uint64_t n) {
@@ -254,7 +257,9 @@ __global__ void __launch_bounds__(128, TR == 16 ? 4 : 5) k_spread_tiles(WindowPo
                                                       const uint32_t* __restrict__ bin_start,
                                                       const double2* __restrict__ bsorted,
                                                       const double2* __restrict__ pos,
-                                                      double2* __restrict__ grid) {
+                                                      double2* __restrict__ grid,
+                                                      const uint32_t* __restrict__ bin_start2,
+                                                      const int* __restrict__ herm) {
     extern __shared__ double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // per warp: bwx[32*W] (double2), wy[32*W] (double), queue k[64], ix[32], iy[32]
@@ -297,11 +302,13 @@ __global__ void __launch_bounds__(128, TR == 16 ? 4 : 5) k_spread_tiles(WindowPo
         __syncwarp();
     };
 
-    for (int q = 0; q < 4; ++q) {
-        const int cbx = bx - (q >> 1), cby = by - (q & 1);
+    const int nq = (bin_start2 && !(herm && *herm)) ? 8 : 4;
+    for (int q = 0; q < nq; ++q) {
+        const int cbx = bx - ((q >> 1) & 1), cby = by - (q & 1);
         if (cbx < 0 || cby < 0) continue;
         const int b = cbx * tg.nby + cby;
-        const uint32_t s0 = bin_start[b], s1 = bin_start[b + 1];
+        const uint32_t* bs = q < 4 ? bin_start : bin_start2;
+        const uint32_t s0 = bs[b], s1 = bs[b + 1];
         for (uint32_t s = s0; s < s1; s += 32) {
             const uint32_t k = s + lane;
             bool take = false;
@@ -359,7 +366,9 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
                                                     const uint32_t* __restrict__ bin_start,
                                                     const double2* __restrict__ bsorted,
                                                     const double2* __restrict__ pos,
-                                                    double2* __restrict__ grid) {
+                                                    double2* __restrict__ grid,
+                                                      const uint32_t* __restrict__ bin_start2,
+                                                      const int* __restrict__ herm) {
     constexpr int TR = 16;
     extern __shared__ double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -437,11 +446,13 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
         __syncwarp();
     };
 
-    for (int q = 0; q < 4; ++q) {
-        const int cbx = bx - (q >> 1), cby = by - (q & 1);
+    const int nq = (bin_start2 && !(herm && *herm)) ? 8 : 4;
+    for (int q = 0; q < nq; ++q) {
+        const int cbx = bx - ((q >> 1) & 1), cby = by - (q & 1);
         if (cbx < 0 || cby < 0) continue;
         const int b = cbx * tg.nby + cby;
-        const uint32_t s0 = bin_start[b], s1 = bin_start[b + 1];
+        const uint32_t* bs = q < 4 ? bin_start : bin_start2;
+        const uint32_t s0 = bs[b], s1 = bs[b + 1];
         for (uint32_t s = s0; s < s1; s += 128) {
             // four independent position loads in flight per lane
             double2 tt[4];
@@ -500,9 +511,11 @@ __global__ void __launch_bounds__(256) k_interp(WindowPoly P, GridGeom g, uint64
                                                 const uint32_t* __restrict__ perm,
                                                 const double2* __restrict__ addend,
                                                 double2* __restrict__ out, int accumulate,
-                                                int conj_out) {
+                                                int conj_out, HermArgs h) {
     const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (v >= n) return;
+    const bool hon = h.flag && *h.flag;
+    if (v >= (hon && h.n < n ? h.n : n)) return;
+    if (hon && h.mult) mult = h.mult;
     const double2 s = pos[v];
     const int jx0 = (int)ceil(s.x - g.half), jy0 = (int)ceil(s.y - g.half);
     double wx[W], wy[W];
@@ -561,6 +574,7 @@ __global__ void __launch_bounds__(256) k_interp(WindowPoly P, GridGeom g, uint64
     }
     double2 o = cmul(make_double2(ar, ai), phase[v]);
     if (mult) o = cmul(o, mult[v]);
+    if (hon && h.two_re) o = make_double2(2.0 * o.x, 0.0);
     if (conj_out) o.y = -o.y;
     if (addend) {
         const double2 a = addend[v];
@@ -646,7 +660,12 @@ __global__ void __launch_bounds__(128) k_interp_mma(WindowPoly P, GridGeom g, ui
                                                     const double2* __restrict__ grid,
                                                     const uint32_t* __restrict__ perm,
                                                     const double2* __restrict__ addend,
-                                                    double2* __restrict__ out) {
+                                                    double2* __restrict__ out, HermArgs hh) {
+    const bool hon = hh.flag && *hh.flag;
+    if (hon) {
+        if (hh.n < n) n = hh.n;
+        if (hh.mult) mult = hh.mult;
+    }
     __shared__ double s_wx[4][32 * W];
     __shared__ double s_wy[4][32 * W];
     __shared__ int s_jx[4][32], s_jy[4][32];
@@ -761,6 +780,7 @@ __global__ void __launch_bounds__(128) k_interp_mma(WindowPoly P, GridGeom g, ui
                     if (v >= n) continue;
                     double2 o2 = cmul(h ? make_double2(p1r, p1i) : make_double2(p0r, p0i), phase[v]);
                     if (mult) o2 = cmul(o2, mult[v]);
+                    if (hon && hh.two_re) o2 = make_double2(2.0 * o2.x, 0.0);
                     if (addend) {
                         const double2 ad = addend[v];
                         o2.x += ad.x;
@@ -840,8 +860,13 @@ __global__ void __launch_bounds__(128) k_interp_tile(
     uint64_t out_lo, uint64_t n, const double2* __restrict__ pos, const double2* __restrict__ phase,
     const double2* __restrict__ mult, const double* __restrict__ dxt, const double* __restrict__ dyt,
     const double2* __restrict__ grid, const uint32_t* __restrict__ perm,
-    const double2* __restrict__ addend, double2* __restrict__ out) {
+    const double2* __restrict__ addend, double2* __restrict__ out, HermArgs hh) {
     using TT = ITile<W, TRANS>;
+    const bool hon = hh.flag && *hh.flag;
+    if (hon) {
+        if (hh.n < n) n = hh.n;
+        if (hh.mult) mult = hh.mult;
+    }
     extern __shared__ __align__(16) double sm_it[];
     double2* S = reinterpret_cast<double2*>(sm_it);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1008,6 +1033,7 @@ __global__ void __launch_bounds__(128) k_interp_tile(
             if (mine) {
                 double2 o2 = cmul(make_double2(accr, acci), ph);
                 if (mult) o2 = cmul(o2, mu);
+                if (hon && hh.two_re) o2 = make_double2(2.0 * o2.x, 0.0);
                 o2.x += ad.x;
                 o2.y += ad.y;
                 out[dst] = o2;
@@ -1057,10 +1083,12 @@ __global__ void k_ndft(const double2* __restrict__ pts, uint64_t np,
 // coefficients (nufft.cpp:233) and the sorted copy of f for the CSR pass.
 __global__ void k_gather_mul(const double2* __restrict__ in, const uint32_t* __restrict__ perm,
                              const double2* __restrict__ phase, double2* __restrict__ b,
-                             double2* __restrict__ raw, uint64_t n, uint64_t lo, uint64_t hi) {
+                             double2* __restrict__ raw, uint64_t n, uint64_t lo, uint64_t hi,
+                             int* __restrict__ clear) {
     const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (k >= n) return;
     const double2 c = in[perm ? perm[k] : k];
+    if (clear && c.y != 0.0) *clear = 0;
     b[k] = (k >= lo && k < hi) ? cmul(c, phase[k]) : make_double2(0.0, 0.0);
     if (raw) raw[k] = c;
 }
@@ -1196,7 +1224,8 @@ template <int W>
 struct SpreadTilesRun {
     static size_t smem() { return (size_t)4 * 32 * W * 24 + 4 * 128 * sizeof(uint32_t) + 4 * 256 * sizeof(uint32_t); }
     static void run(const WindowPoly& P, GridGeom g, TileGeom tg, const uint32_t* bs,
-                    const double2* b, const double2* pos, double2* grid, cudaStream_t st) {
+                    const double2* b, const double2* pos, double2* grid, cudaStream_t st,
+                    const uint32_t* bs2, const int* herm) {
         static bool attr = false;
         if (!attr) {
             ck(cudaFuncSetAttribute(k_spread_tiles<W, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1217,11 +1246,11 @@ struct SpreadTilesRun {
                "smem attr");
         }
         if (use_mma && tg.tr == 16)
-            k_spread_mma<W><<<(tiles + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid);
+            k_spread_mma<W><<<(tiles + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid, bs2, herm);
         else if (tg.tr == 8)
-            k_spread_tiles<W, 8><<<(tiles + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid);
+            k_spread_tiles<W, 8><<<(tiles + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid, bs2, herm);
         else
-            k_spread_tiles<W, 16><<<(tiles + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid);
+            k_spread_tiles<W, 16><<<(tiles + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid, bs2, herm);
     }
 };
 
@@ -1230,7 +1259,9 @@ struct InterpRun {
     static void run(const WindowPoly& P, GridGeom g, uint64_t n, const double2* pos,
                     const double2* phase, const double2* mult, const double* dx, const double* dy,
                     const double2* grid, const uint32_t* perm, const double2* addend, double2* out,
-                    int acc, int cj, cudaStream_t st, bool trans, const InterpTiles* tiles) {
+                    int acc, int cj, cudaStream_t st, bool trans, const InterpTiles* tiles,
+                    const HermArgs* herm) {
+        const HermArgs hh = herm ? *herm : HermArgs{};
         // tensor-core interpolation pays off when outputs are dense on the band
         // (>= 0.25 per cell: the xi side); SBD_INTERP=tile|mma|scalar forces a
         // choice (tile: the shared-memory staged variant, needs the tile list)
@@ -1251,7 +1282,7 @@ struct InterpRun {
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 128, smem);
                 const unsigned nb = (unsigned)std::min<uint64_t>(tiles->n, (uint64_t)sms * std::max(per, 1) * 8);
                 kern<<<nb, 128, smem, st>>>(P, g, tiles->start, tiles->n, tiles->shift, tiles->out_lo, n, pos,
-                                            phase, mult, dx, dy, grid, perm, addend, out);
+                                            phase, mult, dx, dy, grid, perm, addend, out, hh);
             };
             static size_t attr_t = 0, attr_n = 0;  // per W (this template)
             if (trans)
@@ -1265,19 +1296,19 @@ struct InterpRun {
             const unsigned grid_blocks = (unsigned)std::min<uint64_t>((warps + 3) / 4, 148ull * 16);
             if (trans)
                 k_interp_mma<W, true><<<grid_blocks, 128, 0, st>>>(P, g, n, pos, phase, mult, dx, dy,
-                                                                    grid, perm, addend, out);
+                                                                    grid, perm, addend, out, hh);
             else
                 k_interp_mma<W, false><<<grid_blocks, 128, 0, st>>>(P, g, n, pos, phase, mult, dx, dy,
-                                                                     grid, perm, addend, out);
+                                                                     grid, perm, addend, out, hh);
             return;
         }
         if (trans) {
             k_interp<W, true><<<blocks(n, 256), 256, 0, st>>>(P, g, n, pos, phase, mult, dx, dy, grid,
-                                                              perm, addend, out, acc, cj);
+                                                              perm, addend, out, acc, cj, hh);
             return;
         }
         k_interp<W, false><<<blocks(n, 256), 256, 0, st>>>(P, g, n, pos, phase, mult, dx, dy, grid,
-                                                           perm, addend, out, acc, cj);
+                                                           perm, addend, out, acc, cj, hh);
     }
 };
 
@@ -1321,33 +1352,34 @@ void launch_stencil_extent(const double2* pos, uint64_t n, double half, int* ext
 }
 
 void launch_tile_keys(const double2* pos, uint64_t n, double half, TileGeom tg, uint32_t* keys,
-                      cudaStream_t st) {
+                      cudaStream_t st, const uint8_t* tag) {
     if (!n) return;
-    k_tile_keys<<<blocks(n, 256), 256, 0, st>>>(pos, n, half, tg, keys);
+    k_tile_keys<<<blocks(n, 256), 256, 0, st>>>(pos, n, half, tg, keys, tag);
     count_launch();
     ck(cudaGetLastError(), "k_tile_keys");
 }
 
 void launch_bin_bounds(const uint32_t* sorted_keys, uint64_t n, uint32_t nbins, uint32_t* start,
-                       cudaStream_t st) {
-    k_bin_bounds<<<blocks(n + 1, 256), 256, 0, st>>>(sorted_keys, n, nbins, start);
+                       cudaStream_t st, uint32_t base, uint32_t mask) {
+    k_bin_bounds<<<blocks(n + 1, 256), 256, 0, st>>>(sorted_keys, n, nbins, start, base, mask);
     count_launch();
     ck(cudaGetLastError(), "k_bin_bounds");
 }
 
 void launch_spread_tiles(int w, const WindowPoly& win, GridGeom g, TileGeom tg,
                          const uint32_t* bin_start, const double2* b, const double2* pos,
-                         double2* grid, cudaStream_t st) {
+                         double2* grid, cudaStream_t st, const uint32_t* bin_start2,
+                         const int* herm) {
     if (tg.nbx * tg.nby == 0) return;
-    dispatch_w<SpreadTilesRun>(w, win, g, tg, bin_start, b, pos, grid, st);
+    dispatch_w<SpreadTilesRun>(w, win, g, tg, bin_start, b, pos, grid, st, bin_start2, herm);
     count_launch();
     ck(cudaGetLastError(), "k_spread_tiles");
 }
 
 void launch_morton_keys(const double2* pos, uint64_t n, double half, int shift, uint32_t* keys,
-                        cudaStream_t st) {
+                        cudaStream_t st, const uint8_t* tag) {
     if (!n) return;
-    k_morton_keys<<<blocks(n, 256), 256, 0, st>>>(pos, n, half, shift, keys);
+    k_morton_keys<<<blocks(n, 256), 256, 0, st>>>(pos, n, half, shift, keys, tag);
     count_launch();
     ck(cudaGetLastError(), "k_morton_keys");
 }
@@ -1398,10 +1430,10 @@ void launch_interp(int w, const WindowPoly& win, GridGeom g, uint64_t n, const d
                    const double2* phase, const double2* mult, const double* dx, const double* dy,
                    const double2* grid, const uint32_t* perm, double2* out, int accumulate,
                    int conj_out, cudaStream_t st, const double2* addend, bool transposed,
-                   const InterpTiles* tiles) {
+                   const InterpTiles* tiles, const HermArgs* herm) {
     if (!n) return;
     dispatch_w<InterpRun>(w, win, g, n, pos, phase, mult, dx, dy, grid, perm, addend, out,
-                          accumulate, conj_out, st, transposed, tiles);
+                          accumulate, conj_out, st, transposed, tiles, herm);
     count_launch();
     ck(cudaGetLastError(), "k_interp");
 }
@@ -1436,9 +1468,10 @@ void launch_ndft(const double2* pts, uint64_t np, const double2* frq, uint64_t n
 }
 
 void launch_gather_mul(const double2* in, const uint32_t* perm, const double2* phase, double2* b,
-                       double2* raw, uint64_t n, cudaStream_t st, uint64_t lo, uint64_t hi) {
+                       double2* raw, uint64_t n, cudaStream_t st, uint64_t lo, uint64_t hi,
+                       int* clear) {
     if (!n) return;
-    k_gather_mul<<<blocks(n, 256), 256, 0, st>>>(in, perm, phase, b, raw, n, lo, hi);
+    k_gather_mul<<<blocks(n, 256), 256, 0, st>>>(in, perm, phase, b, raw, n, lo, hi, clear);
     count_launch();
     ck(cudaGetLastError(), "k_gather_mul");
 }

@@ -10,6 +10,7 @@
 //   each plan carries its own tile permutation internally.
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -190,6 +191,15 @@ struct sbd_op {
     DevBuf<uint32_t> cols_s;
     DevBuf<double2> vals_s;
     DevBuf<double2> kappa, f_sorted, qs;
+    // Real-input half split: with real omega-hat and
+    // antipodally paired rings, a real f has spectrum(-xi) = conj(spectrum(xi)),
+    // so only the tag-0 half of each pair is interpolated and spread and the
+    // far field is 2 Re(.). The device flag is set per apply and cleared by the
+    // input gather when f has a nonzero imaginary part (no host round trip).
+    bool herm_ok = false;
+    uint64_t n_half = 0;           // tag-0 xi nodes (sorted positions [0, n_half))
+    DevBuf<double2> kappa_h;       // kappa with self-conjugate nodes halved
+    DevBuf<int> herm_flag;
     StageTimer tm;
     std::mutex mu;
 
@@ -208,9 +218,12 @@ struct sbd_op {
         o.direct_threshold = d.direct_threshold;
         o.max_grid_bytes = d.max_grid_bytes;
         const double* tgt = d.single ? d.src.data() : d.tgt.data();
+        std::vector<uint8_t> tag;
+        std::vector<uint64_t> halve;
+        const bool split = herm_pairs(tag, halve);
         // fwd_out = Plan(xi, tgt, +): xi take this plan's sorted order.
         fwd_out = std::make_unique<Plan>(d.freqs.data(), d.n_xi(), tgt, d.n_tgt(), +1, o, device,
-                                         true, true, stream);
+                                         true, true, stream, split ? tag.data() : nullptr);
         perm_xi = fwd_out->adopt_point_order(stream);
         std::vector<double> xi_sorted(2 * d.n_xi()), w_host(2 * d.n_xi());
         for (uint64_t i = 0; i < d.n_xi(); ++i) {
@@ -223,8 +236,14 @@ struct sbd_op {
         // fwd_in = Plan(src, xi, -): its outputs (the xi nodes, in the canonical
         // order above) get their own Z-order for the interpolation; its perm_s
         // maps back, so the spectrum is written in the canonical order.
+        std::vector<uint8_t> tag_sorted;
+        if (split) {
+            tag_sorted.resize(d.n_xi());
+            for (uint64_t i = 0; i < d.n_xi(); ++i) tag_sorted[i] = tag[perm_xi[i]];
+        }
         fwd_in = std::make_unique<Plan>(d.src.data(), d.n_src(), xi_sorted.data(), d.n_xi(), -1, o,
-                                        device, true, true, stream);
+                                        device, true, true, stream,
+                                        nullptr, split ? tag_sorted.data() : nullptr);
         w_sorted.upload(reinterpret_cast<const double2*>(w_host.data()), d.n_xi(), stream);
         w_in.alloc(std::max<uint64_t>(d.n_xi(), 1));
         if (fwd_in->perm_s.n)
@@ -239,6 +258,117 @@ struct sbd_op {
         spec.alloc(std::max<uint64_t>(d.n_xi(), 1));
         ck(cudaStreamSynchronize(stream), "operator upload");
         build_fused();
+        if (split) build_half(halve);
+    }
+
+    // Antipodal pairing of the ring quadrature (ring_quadrature.cpp:51-66: ring
+    // p holds M_p (even) nodes at angles 2 pi j / M_p, so node j + M_p/2 is -xi_j
+    // up to rounding; a one-node ring is the zero frequency). tag 0 = computed,
+    // 1 = taken as the conjugate of its partner. A pair whose rounded
+    // coordinates put the partner's stencil somewhere other than the mirror of
+    // the node's (an axis node with an even width, say: the window is 1, not 0,
+    // at its edge) is computed on both nodes instead. `halve` lists the tag-0
+    // nodes that enter 2 Re(.) with weight 1/2 (self-conjugate nodes and both
+    // nodes of such pairs). False when omega-hat is not real or the pairing
+    // does not hold to 1e-12 relative.
+    bool herm_pairs(std::vector<uint8_t>& tag, std::vector<uint64_t>& halve) const {
+        if (std::getenv("SBD_NO_HERM")) return false;
+        const uint64_t nx = d.n_xi();
+        if (nx < 2 || d.ring_offsets.size() < 2 || d.ring_offsets.front() != 0 ||
+            (uint64_t)d.ring_offsets.back() != nx)
+            return false;
+        for (uint64_t i = 0; i < nx; ++i)
+            if (d.weights[2 * i + 1] != 0.0) return false;
+        // stencil geometry of the two plans (Plan(src, xi, -), Plan(xi, tgt, +))
+        const int w = width_for_tol(d.nufft_tol);
+        const double* tgt = d.single ? d.src.data() : d.tgt.data();
+        const double* xi = d.freqs.data();
+        const Axis inx = plan_axis(d.src.data(), d.n_src(), xi, nx, 0, -1.0, w);
+        const Axis iny = plan_axis(d.src.data(), d.n_src(), xi, nx, 1, -1.0, w);
+        const Axis outx = plan_axis(xi, nx, tgt, d.n_tgt(), 0, 1.0, w);
+        const Axis outy = plan_axis(xi, nx, tgt, d.n_tgt(), 1, 1.0, w);
+        auto mirrored = [&](uint64_t j, uint64_t q) {
+            const double jx = xi[2 * j], jy = xi[2 * j + 1], qx = xi[2 * q], qy = xi[2 * q + 1];
+            const bool in_ok =
+                stencil_start_output(inx, qx, -1.0, w) == -(stencil_start_output(inx, jx, -1.0, w) + w - 1) &&
+                stencil_start_output(iny, qy, -1.0, w) == -(stencil_start_output(iny, jy, -1.0, w) + w - 1);
+            const bool out_ok =
+                stencil_start_point(outx, qx, w) == outx.n - (stencil_start_point(outx, jx, w) + w - 1) &&
+                stencil_start_point(outy, qy, w) == outy.n - (stencil_start_point(outy, jy, w) + w - 1);
+            return in_ok && out_ok;
+        };
+        tag.assign(nx, 0);
+        halve.clear();
+        for (size_t r = 0; r + 1 < d.ring_offsets.size(); ++r) {
+            const uint64_t a = (uint64_t)d.ring_offsets[r], b = (uint64_t)d.ring_offsets[r + 1];
+            const uint64_t m = b - a;
+            if (m == 1) {
+                if (xi[2 * a] != 0.0 || xi[2 * a + 1] != 0.0) return false;
+                halve.push_back(a);
+                continue;
+            }
+            if (m == 0 || (m & 1)) return false;
+            for (uint64_t j = a; j < a + m / 2; ++j) {
+                const uint64_t q = j + m / 2;
+                const double px = xi[2 * j], py = xi[2 * j + 1];
+                const double sx = px + xi[2 * q], sy = py + xi[2 * q + 1];
+                const double mag = std::sqrt(px * px + py * py);
+                if (std::sqrt(sx * sx + sy * sy) > 1e-12 * mag || d.weights[2 * j] != d.weights[2 * q])
+                    return false;
+                if (mirrored(j, q)) {
+                    tag[q] = 1;
+                } else {
+                    halve.push_back(j);
+                    halve.push_back(q);
+                }
+            }
+        }
+        return true;
+    }
+
+    void build_half(const std::vector<uint64_t>& halve) {
+        if (!fused || !fwd_out->tagged_pts || !fwd_in->tagged_out || fwd_out->n0_pts != fwd_in->n0_out) {
+            if (std::getenv("SBD_VERBOSE"))
+                std::fprintf(stderr, "[sbd] half split off: fused %d tagged %d %d n0 %llu %llu\n", (int)fused,
+                             (int)fwd_out->tagged_pts, (int)fwd_in->tagged_out,
+                             (unsigned long long)fwd_out->n0_pts, (unsigned long long)fwd_in->n0_out);
+            return;
+        }
+        const uint64_t nx = d.n_xi();
+        n_half = fwd_out->n0_pts;
+        kappa_h.alloc(nx);
+        ck(cudaMemcpyAsync(kappa_h.p, kappa.p, nx * 16, cudaMemcpyDeviceToDevice, stream), "kappa_h");
+        if (!halve.empty()) {
+            // position of each halved node in fwd_in's output order
+            std::vector<uint32_t> inv_xi(nx);
+            for (uint64_t i = 0; i < nx; ++i) inv_xi[perm_xi[i]] = (uint32_t)i;
+            std::vector<uint32_t> pos_of(nx);
+            if (fwd_in->perm_s.n) {
+                std::vector<uint32_t> ps(nx);
+                ck(cudaMemcpyAsync(ps.data(), fwd_in->perm_s.p, nx * 4, cudaMemcpyDeviceToHost, stream), "perm");
+                ck(cudaStreamSynchronize(stream), "perm");
+                for (uint64_t i = 0; i < nx; ++i) pos_of[ps[i]] = (uint32_t)i;
+            } else {
+                for (uint64_t i = 0; i < nx; ++i) pos_of[i] = (uint32_t)i;
+            }
+            std::vector<double2> kh(nx);
+            ck(cudaMemcpyAsync(kh.data(), kappa_h.p, nx * 16, cudaMemcpyDeviceToHost, stream), "kappa_h");
+            ck(cudaStreamSynchronize(stream), "kappa_h");
+            for (uint64_t f : halve) {
+                double2& v = kh[pos_of[inv_xi[f]]];
+                v.x *= 0.5;
+                v.y *= 0.5;
+            }
+            ck(cudaMemcpyAsync(kappa_h.p, kh.data(), nx * 16, cudaMemcpyHostToDevice, stream), "kappa_h");
+        }
+        if (std::getenv("SBD_VERBOSE"))
+            std::fprintf(stderr, "[sbd] half split: %zu nodes at weight 1/2\n", halve.size());
+        herm_flag.alloc(1);
+        ck(cudaStreamSynchronize(stream), "half split");
+        herm_ok = true;
+        if (std::getenv("SBD_VERBOSE"))
+            std::fprintf(stderr, "[sbd] real-input half split: %llu of %llu xi nodes\n",
+                         (unsigned long long)n_half, (unsigned long long)nx);
     }
 
     void build_fused() {
@@ -289,15 +419,26 @@ struct sbd_op {
     // conv_operator.cpp:301-309 on device buffers, one right-hand side.
     void apply_one(const double2* f, double2* q, cudaStream_t st) {
         if (fused) {
+            HermArgs hin, hout;
+            if (herm_ok) {
+                ck(cudaMemsetAsync(herm_flag.p, 1, sizeof(int), st), "half flag");
+                hin.flag = hout.flag = herm_flag.p;
+                hin.n = n_half;
+                hin.mult = kappa_h.p;
+                hin.clear = true;
+                hout.n = ~0ull;
+                hout.two_re = true;
+            }
             // spectrum_b = NUFFT-(f) * w * pre_out, with f_sorted kept for the CSR pass
             fwd_in->apply_pruned(f, false, f_sorted.p, spec.p, kappa.p, nullptr, work, st, &tm,
-                                 "spread_src", "fft_in", "interp_xi");
+                                 "spread_src", "fft_in", "interp_xi", 0, ~0ull, 0, ~0ull,
+                                 herm_ok ? &hin : nullptr);
             if (tm.on) tm.start("spmv");
             launch_spmv_vec(d.n_tgt(), ro_s.p, cols_s.p, vals_s.p, f_sorted.p, qs.p, st);
             if (tm.on) tm.stop();
             // q = NUFFT+(spectrum) + D f, scattered to the caller's target order
             fwd_out->apply_pruned(spec.p, true, nullptr, q, nullptr, qs.p, work, st, &tm, "spread_xi",
-                                  "fft_out", "interp_tgt");
+                                  "fft_out", "interp_tgt", 0, ~0ull, 0, ~0ull, herm_ok ? &hout : nullptr);
             return;
         }
         fwd_in->apply(f, spec.p, work, st, &tm, w_in.p, "spread_src", "fft_in", "interp_xi");
@@ -346,7 +487,7 @@ struct sbd_op {
                ro_s.bytes() + cols_s.bytes() + vals_s.bytes() + kappa.bytes() + f_sorted.bytes() +
                qs.bytes() + work.bbuf.bytes() +
                cols.bytes() + vals.bytes() + work.grid.bytes() + work.T.bytes() + work.band.bytes() +
-               spec.bytes() + hf.bytes() + hq.bytes();
+               spec.bytes() + hf.bytes() + hq.bytes() + kappa_h.bytes();
     }
 
     // conv_operator.cpp:338-353

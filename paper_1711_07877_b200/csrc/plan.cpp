@@ -47,8 +47,39 @@ std::vector<double> make_deconv(const Axis& a, double beta) {
 
 } // namespace
 
+Axis plan_axis(const double* pts_xy, uint64_t np, const double* frq_xy, uint64_t nf, int comp,
+               double sg, int w) {
+    Axis a;
+    double plo, phi, flo, fhi;
+    span(pts_xy, np, comp, 1.0, plo, phi);
+    span(frq_xy, nf, comp, sg, flo, fhi);
+    a.center = 0.5 * (plo + phi);
+    a.fcenter = 0.5 * (flo + fhi);
+    const double X = std::max(0.5 * (phi - plo), 1e-8 * (1.0 + std::fabs(a.center)));
+    const double S = std::max(0.5 * (fhi - flo), 1e-8 * (1.0 + std::fabs(a.fcenter)));
+    a.gamma = kSigma * X / kPi;
+    a.n = next_fast_even((int)std::ceil(2.0 * kSigma * (a.gamma * S + 0.5 * w + 1.0)));
+    a.alpha1 = kPi * w / a.n;
+    a.alpha2 = 0.5 * w / a.gamma;
+    return a;
+}
+
+int stencil_start_point(const Axis& a, double p, int w) {
+    // k_plan_points' grid coordinate, then ceil(t - w/2) (same IEEE operations)
+    const double u = (p - a.center) / a.gamma;
+    const double tt = ((u + kPi) * (double)a.n) / (2.0 * kPi);
+    return (int)std::ceil(tt - 0.5 * w);
+}
+
+int stencil_start_output(const Axis& a, double f, double sg, int w) {
+    // k_plan_outputs' mode coordinate, then ceil(s - w/2)
+    const double s = a.gamma * (sg * f - a.fcenter);
+    return (int)std::ceil(s - 0.5 * w);
+}
+
 Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf_, int sign_,
-           const NufftOpts& o, int dev, bool sort_points, bool sort_outputs, cudaStream_t st)
+           const NufftOpts& o, int dev, bool sort_points, bool sort_outputs, cudaStream_t st,
+           const uint8_t* pt_tag, const uint8_t* out_tag)
     : sign(sign_ > 0 ? 1 : -1), device(dev), np(np_), nf(nf_), opts(o) {
     const uint64_t work = np * nf;
     const bool direct = o.mode == 1 || (o.mode == 0 && work <= o.direct_threshold);
@@ -64,21 +95,8 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
     w = width_for_tol(o.tol);
     beta = 2.3562 * w;
     const double sg = (double)sign;
-    auto setup_axis = [&](Axis& a, int comp) {
-        double plo, phi, flo, fhi;
-        span(pts_xy, np, comp, 1.0, plo, phi);
-        span(frq_xy, nf, comp, sg, flo, fhi);
-        a.center = 0.5 * (plo + phi);
-        a.fcenter = 0.5 * (flo + fhi);
-        const double X = std::max(0.5 * (phi - plo), 1e-8 * (1.0 + std::fabs(a.center)));
-        const double S = std::max(0.5 * (fhi - flo), 1e-8 * (1.0 + std::fabs(a.fcenter)));
-        a.gamma = kSigma * X / kPi;
-        a.n = next_fast_even((int)std::ceil(2.0 * kSigma * (a.gamma * S + 0.5 * w + 1.0)));
-        a.alpha1 = kPi * w / a.n;
-        a.alpha2 = 0.5 * w / a.gamma;
-    };
-    setup_axis(ax, 0);
-    setup_axis(ay, 1);
+    ax = plan_axis(pts_xy, np, frq_xy, nf, 0, sg, w);
+    ay = plan_axis(pts_xy, np, frq_xy, nf, 1, sg, w);
     const uint64_t ncell = (uint64_t)ax.n * (uint64_t)ay.n;
     if (ncell * 16u > o.max_grid_bytes)
         throw Error(3, "nufft: oversampled grid exceeds the memory limit");
@@ -124,15 +142,34 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
     }
 
     // ---- sort both sides by grid tile of the stencil start
+    // tags: tag-0 entries sort first (key bit 31); needs the tile index below
+    // 2^26 (points) or stencil cells below 2^15 after the shift (outputs)
+    const int oshift = std::max(ax.n, ay.n) / 2 + w;
+    auto count0 = [](const uint8_t* tag, uint64_t n) {
+        uint64_t c = 0;
+        for (uint64_t i = 0; i < n; ++i) c += tag[i] ? 0 : 1;
+        return c;
+    };
+    if (pt_tag && pruned && (uint64_t)tg.nbx * (uint64_t)tg.nby < (1ull << 26)) {
+        tagged_pts = true;
+        n0_pts = count0(pt_tag, np);
+    }
+    if (out_tag && sort_outputs && oshift + std::max(ax.n, ay.n) / 2 + w < 32768) {
+        tagged_out = true;
+        n0_out = count0(out_tag, nf);
+    }
     auto sort_side = [&](DevBuf<double2>& pos, DevBuf<double2>& ph, DevBuf<uint32_t>& perm,
                          uint64_t n, bool tiles) {
         if (n < 1) return;
         DevBuf<uint32_t> keys(n);
         perm.alloc(n);
+        const uint8_t* htag = tiles ? (tagged_pts ? pt_tag : nullptr) : (tagged_out ? out_tag : nullptr);
+        DevBuf<uint8_t> dtag;
+        if (htag) dtag.upload(htag, n, st);
         if (tiles)
-            launch_tile_keys(pos.p, n, g.half, tg, keys.p, st);
+            launch_tile_keys(pos.p, n, g.half, tg, keys.p, st, dtag.p);
         else  // outputs: Z-order of the stencil cell (mode units, |j| <= n/2)
-            launch_morton_keys(pos.p, n, g.half, std::max(ax.n, ay.n) / 2 + w, keys.p, st);
+            launch_morton_keys(pos.p, n, g.half, oshift, keys.p, st, dtag.p);
         launch_iota(perm.p, n, st);
         sort_by_key(keys.p, perm.p, n, st);
         DevBuf<double2> a(n), b(n);
@@ -143,10 +180,18 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
         if (tiles) {
             const uint32_t nbins = (uint32_t)tg.nbx * (uint32_t)tg.nby;
             bin_start.alloc(nbins + 1);
-            launch_bin_bounds(keys.p, n, nbins, bin_start.p, st);
+            if (tagged_pts) {
+                // tag-0 points [0, n0) and tag-1 points [n0, n) binned separately
+                bin_start2.alloc(nbins + 1);
+                launch_bin_bounds(keys.p, n0_pts, nbins, bin_start.p, st);
+                launch_bin_bounds(keys.p + n0_pts, n - n0_pts, nbins, bin_start2.p, st, (uint32_t)n0_pts,
+                                  0x7fffffffu);
+            } else {
+                launch_bin_bounds(keys.p, n, nbins, bin_start.p, st);
+            }
         } else {
             // 32 x 32 blocks of the Z order (k_interp_tile)
-            out_shift = std::max(ax.n, ay.n) / 2 + w;
+            out_shift = oshift;
             build_tile_starts(keys.p, n, 10, out_tiles, n_out_tiles, st);
         }
         ck(cudaStreamSynchronize(st), "sort side");
@@ -343,7 +388,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
                         const double2* mult, const double2* addend, FftWork& wk, cudaStream_t st,
                         StageTimer* tm, const char* tag_spread, const char* tag_fft,
                         const char* tag_interp, uint64_t in_lo, uint64_t in_hi, uint64_t out_lo,
-                        uint64_t out_hi) const {
+                        uint64_t out_hi, const HermArgs* herm) const {
     out_hi = std::min<uint64_t>(out_hi, nf);
     out_lo = std::min(out_lo, out_hi);
     const uint64_t nout = out_hi - out_lo;
@@ -355,6 +400,17 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
     const uint32_t* perm_p = perm_s.n ? perm_s.p + out_lo : nullptr;
     double2* out_p = perm_s.n ? out : out + out_lo;
     if (!pruned) throw Error(3, "apply_pruned on a plan without the pruned path");
+    // real-input half split: the output count is relative to this call's range
+    HermArgs hz;
+    const HermArgs* hp = nullptr;
+    if (herm) {
+        hz = *herm;
+        hz.n = herm->n > out_lo ? std::min<uint64_t>(nout, herm->n - out_lo) : 0;
+        hp = &hz;
+    }
+    int* clear = herm && herm->clear ? herm->flag : nullptr;
+    const uint32_t* bs2 = tagged_pts ? bin_start2.p : nullptr;
+    const int* hflag = herm ? herm->flag : nullptr;
     InterpTiles otiles;
     otiles.start = out_tiles.p;
     otiles.n = n_out_tiles;
@@ -368,12 +424,12 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
     if (!in_is_b) {
         if (wk.bbuf.n < np) wk.bbuf.alloc(np);
         launch_gather_mul(in, perm_t.n ? perm_t.p : nullptr, pre.p, wk.bbuf.p, raw_sorted, np, st, in_lo,
-                          in_hi);
+                          in_hi, clear);
         b = wk.bbuf.p;
     }
     if (dft) {
         // compact support grid -> rows pass -> band-columns pass -> transposed band
-        launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, wk.grid.p, st);
+        launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, wk.grid.p, st, bs2, hflag);
         if (tm) tm->stop();
         if (tm) tm->start(tag_fft);
         launch_pruned_dft(pass1, wk.grid.p, wk.T1.p, tw1.p, st);
@@ -388,7 +444,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         if (tm) tm->start(tag_interp);
         const GridGeom gt{b1c, bc, 0.5 * w};
         launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx_band.p, dy_band.p, wk.bandT.p, perm_p,
-                      out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles);
+                      out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles, hp);
         if (tm) tm->stop();
         return;
     }
@@ -396,7 +452,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         zero_rect_minus(wk.grid.p, n2, wk.gr0, wk.gr1, wk.gc0, wk.gc1, rlo, rhi, clo, chi, st);
     else if (wk.g_pitch)  // written by a plan of another grid size: clear all of it
         zero_rect_minus(wk.grid.p, wk.g_pitch, wk.gr0, wk.gr1, wk.gc0, wk.gc1, 0, 0, 0, 0, st);
-    launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, wk.grid.p, st);
+    launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, wk.grid.p, st, bs2, hflag);
     wk.gr0 = rlo;
     wk.gr1 = rhi;
     wk.gc0 = clo;
@@ -440,7 +496,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         if (tm) tm->start(tag_interp);
         const GridGeom gt{ax.n, bc, 0.5 * w};
         launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx.p, dy_band.p, wk.bandT.p, perm_p,
-                      out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles);
+                      out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles, hp);
         if (tm) tm->stop();
         return;
     }
@@ -454,7 +510,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
     if (tm) tm->start(tag_interp);
     const GridGeom gb{ax.n, bc, 0.5 * w};
     launch_interp(w, win, gb, nout, s_p, post_p, mult_p, dx.p, dy_band.p, wk.band.p, perm_p, out_p, 0,
-                  0, st, add_p, false, &otiles);
+                  0, st, add_p, false, &otiles, hp);
     if (tm) tm->stop();
 }
 

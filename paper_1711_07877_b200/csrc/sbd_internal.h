@@ -92,6 +92,14 @@ struct Axis {
     double alpha1 = 0.0, alpha2 = 0.0;
 };
 
+// Plan geometry of one axis (nufft.cpp:127-154), exactly as Plan computes it,
+// and the stencil start ceil(c - w/2) of a point / an output on that axis as
+// k_plan_points / k_plan_outputs + the spread / interpolation compute it.
+Axis plan_axis(const double* pts_xy, uint64_t np, const double* frq_xy, uint64_t nf, int comp,
+               double sg, int w);
+int stencil_start_point(const Axis& a, double p, int w);
+int stencil_start_output(const Axis& a, double f, double sg, int w);
+
 struct NufftOpts {
     double tol = 1e-9;
     int mode = 0; // 0 auto, 1 direct, 2 fast
@@ -160,10 +168,15 @@ struct PrunedPass {
 // ("s": gather in apply, spread in apply_transpose) are stored in a sorted
 // order chosen for locality; perm_* map sorted position -> caller index (empty
 // when the caller's order is kept).
+struct HermArgs;
+
 class Plan {
   public:
+    // pt_tag / out_tag (optional, caller order, 0/1): sort tag-0 entries before
+    // tag-1 entries on that side (the real-input half split, op.cpp)
     Plan(const double* pts_xy, uint64_t np, const double* frq_xy, uint64_t nf, int sign,
-         const NufftOpts& opts, int device, bool sort_points, bool sort_outputs, cudaStream_t st);
+         const NufftOpts& opts, int device, bool sort_points, bool sort_outputs, cudaStream_t st,
+         const uint8_t* pt_tag = nullptr, const uint8_t* out_tag = nullptr);
     ~Plan();
     Plan(const Plan&) = delete;
     Plan& operator=(const Plan&) = delete;
@@ -195,6 +208,11 @@ class Plan {
     int rlo = 0, rhi = 0, clo = 0, chi = 0; // region written by the spread tiles
     TileGeom tg{};
     DevBuf<uint32_t> bin_start;
+    // tagged sides: tag-0 entries are sorted positions [0, n0_*); the points'
+    // tile bins of the tag-1 entries are in bin_start2
+    bool tagged_pts = false, tagged_out = false;
+    uint64_t n0_pts = 0, n0_out = 0;
+    DevBuf<uint32_t> bin_start2;
     DevBuf<uint32_t> out_tiles;  // Z-order block starts of the sorted outputs
     uint32_t n_out_tiles = 0;
     int out_shift = 0;
@@ -222,11 +240,13 @@ class Plan {
     //           order (else b is formed from caller-order `in`, and the sorted
     //           copy of `in` is written to raw_sorted when given);
     //  addend:  per sorted output, added after mult before the scatter.
+    //  herm:    real-input half split (HermArgs), nullptr = off
     void apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, double2* out,
                       const double2* mult, const double2* addend, FftWork& wk, cudaStream_t st,
                       StageTimer* tm, const char* tag_spread, const char* tag_fft,
                       const char* tag_interp, uint64_t in_lo = 0, uint64_t in_hi = ~0ull,
-                      uint64_t out_lo = 0, uint64_t out_hi = ~0ull) const;
+                      uint64_t out_lo = 0, uint64_t out_hi = ~0ull,
+                      const HermArgs* herm = nullptr) const;
     void apply_transpose(const double2* in, double2* out, FftWork& wk, cudaStream_t st,
                          StageTimer* tm, const double2* mult = nullptr, int conj_in = 0,
                          int conj_out = 0) const;
@@ -238,6 +258,20 @@ class Plan {
     // data in this plan's sorted order from now on. Returns the permutation
     // (sorted position -> caller index) on the host.
     std::vector<uint32_t> adopt_point_order(cudaStream_t st);
+};
+
+// Real-input half split (op.cpp): when the device flag is nonzero at kernel
+// time, the xi-side interpolation computes only the first `n` sorted outputs
+// (the tag-0 half of the antipodal pairs) with multiplier `mult`, the xi-side
+// spread reads only the tag-0 points, and the target-side interpolation
+// returns 2 Re(.). `clear`: the input gather zeroes the flag when an input has
+// a nonzero imaginary part.
+struct HermArgs {
+    int* flag = nullptr;
+    uint64_t n = 0;
+    const double2* mult = nullptr;
+    bool two_re = false;
+    bool clear = false;
 };
 
 // ---------------------------------------------------------------- kernels
@@ -256,22 +290,29 @@ void launch_bin_keys(const double2* pos, uint64_t n, GridGeom g, int tile, uint3
                      cudaStream_t st);
 // min/max of the stencil starts ceil(t - w/2): ext = {ixmin, ixmax, iymin, iymax}
 void launch_stencil_extent(const double2* pos, uint64_t n, double half, int* ext, cudaStream_t st);
+// tag (optional, 0/1 per entry) becomes key bit 31 (Morton keys then use 15
+// bits per axis)
 void launch_morton_keys(const double2* pos, uint64_t n, double half, int shift, uint32_t* keys,
-                        cudaStream_t st);
+                        cudaStream_t st, const uint8_t* tag = nullptr);
 void launch_tile_keys(const double2* pos, uint64_t n, double half, TileGeom tg, uint32_t* keys,
-                      cudaStream_t st);
+                      cudaStream_t st, const uint8_t* tag = nullptr);
+// start[b] = base + first i with ((key[i] & mask) >> 5) >= b
 void launch_bin_bounds(const uint32_t* sorted_keys, uint64_t n, uint32_t nbins, uint32_t* start,
-                       cudaStream_t st);
+                       cudaStream_t st, uint32_t base = 0, uint32_t mask = 0xffffffffu);
 // Tile-owned spread: writes every cell of the tiles (no atomics, no memset).
+// bin_start2 (optional): a second bin set over the same tiles (tag-1 points),
+// skipped when *herm is nonzero
 void launch_spread_tiles(int w, const WindowPoly& win, GridGeom g, TileGeom tg,
                          const uint32_t* bin_start, const double2* b, const double2* pos,
-                         double2* grid, cudaStream_t st);
+                         double2* grid, cudaStream_t st, const uint32_t* bin_start2 = nullptr,
+                         const int* herm = nullptr);
 void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int B, double2* Tt,
                            int n1, cudaStream_t st);
 // b[k] = in[perm[k]] phase[k] for k in [lo, hi) (zero elsewhere); raw[k] = in[perm[k]].
+// clear (optional): set to 0 when some in[k] has a nonzero imaginary part.
 void launch_gather_mul(const double2* in, const uint32_t* perm, const double2* phase, double2* b,
                        double2* raw, uint64_t n, cudaStream_t st, uint64_t lo = 0,
-                       uint64_t hi = ~0ull);
+                       uint64_t hi = ~0ull, int* clear = nullptr);
 void launch_spmv_vec(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double2* vals,
                      const double2* f, double2* qs, cudaStream_t st);
 void sort_by_key(uint32_t* keys, uint32_t* vals, uint64_t n, cudaStream_t st);
@@ -299,7 +340,8 @@ void launch_interp(int w, const WindowPoly& win, GridGeom g, uint64_t n, const d
                    const double2* phase, const double2* mult, const double* dx, const double* dy,
                    const double2* grid, const uint32_t* perm, double2* out, int accumulate,
                    int conj_out, cudaStream_t st, const double2* addend = nullptr,
-                   bool transposed = false, const InterpTiles* tiles = nullptr);
+                   bool transposed = false, const InterpTiles* tiles = nullptr,
+                   const HermArgs* herm = nullptr);
 // sorted keys -> starts of the runs of equal key >> bits
 void build_tile_starts(const uint32_t* sorted_keys, uint64_t n, int bits, DevBuf<uint32_t>& start,
                        uint32_t& ntiles, cudaStream_t st);

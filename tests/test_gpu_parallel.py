@@ -16,9 +16,15 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("name", ["lap_disk_n1000", "helm_disk_n800", "lap_two_clouds",
                                   "lap_star_n1500"])
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
-def test_sharded_halves_reproduce_apply(name, world):
+def test_sharded_halves_reproduce_apply(name, world, monkeypatch):
     path, g = golden(name)
+    # the sharded halves compute every xi node: compare with the full-path
+    # operator bitwise-closely, and with the default one (which may take the
+    # real-input half split) to the half split's own agreement
+    monkeypatch.setenv("SBD_NO_HERM", "1")
     op = sbd.CompressedOperator.load(path)
+    monkeypatch.delenv("SBD_NO_HERM")
+    op_default = sbd.CompressedOperator.load(path)
     be = DeviceBackend(op)
     f = torch.from_numpy(np.ascontiguousarray(g["f"], dtype=np.complex128).view(np.float64)).cuda()
     ranks = [ShardedApply(be, r, world, allreduce=lambda t: None) for r in range(world)]
@@ -33,4 +39,6 @@ def test_sharded_halves_reproduce_apply(name, world):
     torch.cuda.synchronize()
     qh = q.cpu().numpy().view(np.complex128)
     assert rel_l2(qh, op.apply(g["f"])) <= 1e-13
+    qd = op_default.apply(g["f"])
+    assert rel_l2(qh.real, qd.real) <= 1e-13 and rel_l2(qh, qd) <= 5e-10
     assert rel_l2(qh, g["q"]) <= 1e-9

@@ -188,11 +188,14 @@ def test_nufft_auto_direct_and_guards():
 def test_fused_and_unfused_paths_agree(name, monkeypatch):
     # The fused forward path (renumbered D, kappa-weighted xi interpolation)
     # against the plain stage-by-stage path on the same operator file.
+    # (The real-input half split is off here: it is compared in its own test.)
     path, g = golden(name)
+    monkeypatch.setenv("SBD_NO_HERM", "1")
     fused = sbd.CompressedOperator.load(path)
     monkeypatch.setenv("SBD_NO_FUSED", "1")
     plain = sbd.CompressedOperator.load(path)
     monkeypatch.delenv("SBD_NO_FUSED")
+    monkeypatch.delenv("SBD_NO_HERM")
     assert rel_l2(fused.apply(g["f"]), plain.apply(g["f"])) <= 1e-13
     assert rel_l2(plain.apply(g["f"]), g["q"]) <= PARITY
 
@@ -292,3 +295,71 @@ def test_band_dft_strict_rejects_unsupported_grid(monkeypatch):
     monkeypatch.setenv("SBD_DFT_R3", "16")  # 4096 does not divide 2304
     with pytest.raises(sbd.SbdError, match="unsupported"):
         sbd.NufftPlan(pts, frq, 1, sbd.NufftOptions(tol=1e-8, mode="fast"))
+
+
+# ------------------------------------------------------- real-input half split
+def _close_times(op, f):
+    # D f on the host from the operator's own close matrix (row k = target k)
+    m = op.close_matrix()
+    rows = np.repeat(np.arange(len(m.row_offsets) - 1), np.diff(m.row_offsets.astype(np.int64)))
+    out = np.zeros(len(m.row_offsets) - 1, dtype=np.complex128)
+    np.add.at(out, rows, m.values * f[m.cols.astype(np.int64)])
+    return out
+
+
+# Laplace cases whose two NUFFTs are both gridded (the fused path)
+HALF_CASES = ["lap_disk_n1000", "lap_star_n1500", "lap_two_clouds"]
+
+
+@pytest.mark.parametrize("name", HALF_CASES)
+def test_real_input_half_split(ops, oracle, name, monkeypatch):
+    # real omega-hat, antipodal rings, real f: only half of the xi nodes are
+    # interpolated / spread and the far field is 2 Re(.) (op.cpp herm_pairs);
+    # the result must match the full computation and the reference
+    path, g = golden(name)
+    rng = np.random.default_rng(77)
+    f = rng.standard_normal(len(g["f"])) + 0j
+    q = ops[name].apply(f)
+    # the 2 Re(.) path ran: Im q is exactly Im(D f) (D itself carries the
+    # reference far field's rounding-level imaginary parts); the full path
+    # adds the NUFFT's ~1e-11 asymmetry on top
+    df = _close_times(ops[name], f)
+    assert np.abs(q.imag - df.imag).max() <= 1e-14 * np.abs(q).max()
+    monkeypatch.setenv("SBD_NO_HERM", "1")
+    full = sbd.CompressedOperator.load(path)
+    monkeypatch.delenv("SBD_NO_HERM")
+    qf = full.apply(f)
+    if name != "lap_two_clouds":  # (its full-path asymmetry is at rounding level)
+        assert np.abs(qf.imag - df.imag).max() > 1e-14 * np.abs(qf).max()
+    # real parts agree to rounding; the full path's (and the reference's)
+    # imaginary far field is the window truncation's asymmetry (~1e-10
+    # relative), which the half split does not reproduce
+    assert rel_l2(q.real, qf.real) <= 1e-13
+    assert rel_l2(q, qf) <= 5e-10
+    assert rel_l2(q, oracle.op(path).apply(f)) <= PARITY
+    # a complex right-hand side on the same operator takes the full path
+    fc = f + 1e-3j * rng.standard_normal(len(f))
+    assert rel_l2(ops[name].apply(fc), full.apply(fc)) <= 1e-13
+
+
+def test_real_input_half_split_batched_mixed(ops):
+    # per-RHS decision: real and complex columns in one batched call
+    _, g = golden("lap_disk_n1000")
+    rng = np.random.default_rng(8)
+    n = len(g["f"])
+    F = np.stack([rng.standard_normal(n) + 0j, rng.standard_normal(n) + 1j * rng.standard_normal(n),
+                  rng.standard_normal(n) + 0j])
+    Q = ops["lap_disk_n1000"].apply(F)
+    for r in range(3):
+        assert rel_l2(Q[r], ops["lap_disk_n1000"].apply(F[r])) <= 1e-13
+    for r in (0, 2):
+        df = _close_times(ops["lap_disk_n1000"], F[r])
+        assert np.abs(Q[r].imag - df.imag).max() <= 1e-14 * np.abs(Q[r]).max()
+
+
+def test_helmholtz_real_input_takes_full_path(ops, oracle):
+    # complex omega-hat (the J0 ring): no half split even for real f
+    path, g = golden("helm_disk_n800")
+    f = np.random.default_rng(9).standard_normal(len(g["f"])) + 0j
+    q = ops["helm_disk_n800"].apply(f)
+    assert rel_l2(q, oracle.op(path).apply(f)) <= PARITY
