@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
                                                     const double2* __restrict__ pos,
                                                     double2* __restrict__ grid,
                                                       const uint32_t* __restrict__ bin_start2,
-                                                      const int* __restrict__ herm) {
+                                                      const int* __restrict__ herm, SpreadOut so) {
     constexpr int TR = 16;
     extern __shared__ double smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -378,8 +378,9 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
     int* s_ix = reinterpret_cast<int*>(s_q + 64);
     int* s_iy = s_ix + 32;
     const int tile = blockIdx.x * 4 + warp;
-    if (tile >= tg.nbx * tg.nby) return;
-    const int bx = tile / tg.nby, by = tile - (tile / tg.nby) * tg.nby;
+    const int nrun = so.nby_run;  // tile columns run (a prefix of the tg.nby columns)
+    if (tile >= tg.nbx * nrun) return;
+    const int bx = tile / nrun, by = tile - (tile / nrun) * nrun;
     const int X0 = tg.rlo + bx * TR, Y0 = tg.clo + by * kTileC;
     const int gid = lane >> 2, kq = lane & 3;
     constexpr int NJ = kTileC / 8;
@@ -398,10 +399,11 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
     auto flush = [&](int n) {
         int dx = -4 * W, dy = -4 * W;
         if (lane < n) {
-            const uint32_t k = s_q[lane];
-            const double2 t = pos[k];
+            const uint32_t e = s_q[lane];
+            const uint32_t k = e & 0x7fffffffu;  // bit 31: second point set
+            const double2 t = (e >> 31) ? so.pos2[k] : pos[k];
             const int ix0 = (int)ceil(t.x - g.half), iy0 = (int)ceil(t.y - g.half);
-            const double2 b2 = bsorted[k];
+            const double2 b2 = (e >> 31) ? so.b2[k] : bsorted[k];
             dx = ix0 - X0;
             dy = iy0 - Y0;
             double2* bw = s_bwx + lane * W;
@@ -453,13 +455,16 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
         const int b = cbx * tg.nby + cby;
         const uint32_t* bs = q < 4 ? bin_start : bin_start2;
         const uint32_t s0 = bs[b], s1 = bs[b + 1];
+        const bool second = q >= 4 && so.pos2;
+        const double2* P2 = second ? so.pos2 : pos;
+        const uint32_t tagbit = second ? 0x80000000u : 0u;
         for (uint32_t s = s0; s < s1; s += 128) {
             // four independent position loads in flight per lane
             double2 tt[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint32_t k = s + 32 * u + lane;
-                tt[u] = k < s1 ? pos[k] : make_double2(-1e30, -1e30);
+                tt[u] = k < s1 ? P2[k] : make_double2(-1e30, -1e30);
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -468,7 +473,7 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
                 const bool take = k < s1 && ix0 < X0 + TR && ix0 + W > X0 && iy0 < Y0 + kTileC &&
                                   iy0 + W > Y0;
                 const unsigned m = __ballot_sync(0xffffffffu, take);
-                if (take) s_q[queued + __popc(m & ((1u << lane) - 1u))] = k;
+                if (take) s_q[queued + __popc(m & ((1u << lane) - 1u))] = k | tagbit;
                 queued += __popc(m);
                 __syncwarp();
                 if (queued >= 32) {
@@ -481,19 +486,24 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
         }
     }
     if (queued) flush(queued);
-    const int rend = tg.pitch ? tg.rhi : g.n1, cend = tg.pitch ? tg.chi : g.n2;
-    const size_t pitch = tg.pitch ? (size_t)tg.pitch : (size_t)g.n2;
-    const int r0 = tg.pitch ? tg.rlo : 0, c0 = tg.pitch ? tg.clo : 0;
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
         const int row = X0 + 8 * i + gid;
-        if (row >= rend) continue;
+        if (row >= so.rend) continue;
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
             const int col = Y0 + 8 * j + 2 * kq;
-            double2* dst = grid + (size_t)(row - r0) * pitch + (col - c0);
-            if (col < cend) dst[0] = make_double2(cr[i][j][0], ci[i][j][0]);
-            if (col + 1 < cend) dst[1] = make_double2(cr[i][j][1], ci[i][j][1]);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (col + h >= so.cend) continue;
+                const double re = cr[i][j][h], im = ci[i][j][h];
+                if (so.mode == 0)
+                    grid[(size_t)(row - so.r0) * so.pitch + (col + h - so.c0)] = make_double2(re, im);
+                else if (so.mode == 1)  // real grid rows (the imaginary part is zero)
+                    so.rgrid[(size_t)(row - so.r0) * so.pitch + (col + h - so.c0)] = re;
+                else  // transposed: column-major, full-length columns
+                    grid[(size_t)(col + h - so.c0) * so.pitch + (row - so.r0)] = make_double2(re, im);
+            }
         }
     }
 }
@@ -795,6 +805,56 @@ __global__ void __launch_bounds__(128) k_interp_mma(WindowPoly P, GridGeom g, ui
     }
 }
 
+// Interpolation from a real band grid (the Hermitian-FFT mode's output,
+// row-major [r][c] with pitch g.n2): one thread per output, the real part of
+// sum * phase, plus the addend. Same taps and order as k_interp.
+template <int W>
+__global__ void __launch_bounds__(256) k_interp_real(WindowPoly P, GridGeom g, uint64_t n,
+                                                     const double2* __restrict__ pos,
+                                                     const double2* __restrict__ phase,
+                                                     const double* __restrict__ dxt,
+                                                     const double* __restrict__ dyt,
+                                                     const double* __restrict__ grid,
+                                                     const uint32_t* __restrict__ perm,
+                                                     const double2* __restrict__ addend,
+                                                     double2* __restrict__ out) {
+    const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const double2 s = pos[v];
+    const int jx0 = (int)ceil(s.x - g.half), jy0 = (int)ceil(s.y - g.half);
+    double wx[W], wy[W];
+    kb_taps<W>((jx0 - s.x) + g.half, P, wx);
+    kb_taps<W>((jy0 - s.y) + g.half, P, wy);
+    const int mx0 = wrap_base(jx0, g.n1), my0 = wrap_base(jy0, g.n2);
+    int myj[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        int my = my0 + j;
+        if (my >= g.n2) my -= g.n2;
+        myj[j] = my;
+        if (dyt) wy[j] *= dyt[my];
+    }
+    double ar = 0.0;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        int mx = mx0 + i;
+        if (mx >= g.n1) mx -= g.n1;
+        const double* row = grid + (size_t)mx * g.n2;
+        double rr = 0.0;
+#pragma unroll
+        for (int j = 0; j < W; ++j) rr = fma(__ldg(row + myj[j]), wy[j], rr);
+        ar = fma(rr, dxt ? wx[i] * dxt[mx] : wx[i], ar);
+    }
+    const double2 ph = phase[v];
+    double2 o = make_double2(ar * ph.x, 0.0);
+    if (addend) {
+        const double2 a = addend[v];
+        o.x += a.x;
+        o.y += a.y;
+    }
+    out[perm ? perm[v] : v] = o;
+}
+
 // ---- tile-staged tensor-core interpolation -------------------------------
 // Outputs are Z-ordered by stencil cell, so the outputs whose stencil starts
 // in one 32 x 32 cell block are contiguous ("tiles", starts built at plan
@@ -867,6 +927,7 @@ __global__ void __launch_bounds__(128) k_interp_tile(
         if (hh.n < n) n = hh.n;
         if (hh.mult) mult = hh.mult;
     }
+    const int hcols = hon ? hh.hcols : 0;
     extern __shared__ __align__(16) double sm_it[];
     double2* S = reinterpret_cast<double2*>(sm_it);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -906,7 +967,13 @@ __global__ void __launch_bounds__(128) k_interp_tile(
                 v[u] = make_double2(0.0, 0.0);
                 if (i < TT::cells && r < TT::E && c < TT::E) {
                     const int gr = wrap_near(X0 + r, g.n1), gc = wrap_near(Y0 + c, g.n2);
-                    v[u] = __ldg(TRANS ? grid + (size_t)gc * g.n1 + gr : grid + (size_t)gr * g.n2 + gc);
+                    if (TRANS && hcols && gc >= hcols) {
+                        // negative column: conjugate of the mirrored stored cell
+                        const double2 m = __ldg(grid + (size_t)(g.n2 - gc) * g.n1 + (gr ? g.n1 - gr : 0));
+                        v[u] = make_double2(m.x, -m.y);
+                    } else {
+                        v[u] = __ldg(TRANS ? grid + (size_t)gc * g.n1 + gr : grid + (size_t)gr * g.n2 + gc);
+                    }
                 }
             }
 #pragma unroll
@@ -1034,6 +1101,7 @@ __global__ void __launch_bounds__(128) k_interp_tile(
                 double2 o2 = cmul(make_double2(accr, acci), ph);
                 if (mult) o2 = cmul(o2, mu);
                 if (hon && hh.two_re) o2 = make_double2(2.0 * o2.x, 0.0);
+                if (hon && hh.out2) hh.out2[hh.perm2[vr]] = make_double2(o2.x, -o2.y);
                 o2.x += ad.x;
                 o2.y += ad.y;
                 out[dst] = o2;
@@ -1129,7 +1197,8 @@ __global__ void __launch_bounds__(256) k_spmv_vec(uint64_t rows, const uint64_t*
 // are coalesced.
 __global__ void __launch_bounds__(256) k_band_transpose(const double2* __restrict__ T, int n2,
                                                         int r0, int r1, int b, int B,
-                                                        double2* __restrict__ Tt, int n1) {
+                                                        double2* __restrict__ Tt, int n1, int rin0,
+                                                        int conj_out) {
     __shared__ double2 tile[32][33];
     const int cb = blockIdx.x * 32, rb = r0 + blockIdx.y * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
@@ -1138,15 +1207,50 @@ __global__ void __launch_bounds__(256) k_band_transpose(const double2* __restric
         const int r = rb + ty + q, c = cb + tx;
         if (r < r1 && c < B) {
             const int m = c <= b ? c : n2 - B + c;
-            tile[ty + q][tx] = T[(size_t)r * n2 + m];
+            tile[ty + q][tx] = T[(size_t)(r - rin0) * n2 + m];
         }
     }
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < 32; q += 8) {
         const int c = cb + ty + q, r = rb + tx;
-        if (r < r1 && c < B) Tt[(size_t)c * n1 + r] = tile[tx][ty + q];
+        if (r < r1 && c < B) {
+            double2 v = tile[tx][ty + q];
+            if (conj_out) v.y = -v.y;
+            Tt[(size_t)c * n1 + r] = v;
+        }
     }
+}
+
+// Mirrored grid coordinates t' = n - t: the image of a point under the grid
+// reflection m -> -m (mod n). The image's stencil must be exactly the mirror
+// of the point's (start n - s - w + 1 for start s = ceil(t - w/2)); when
+// rounding puts ceil(t' - w/2) one cell off (t - w/2 within an ulp of an
+// integer), t' is nudged by ulps, which moves the taps by rounding only.
+__device__ __forceinline__ double mirror_coord(double t, int n, int w) {
+    const double h = 0.5 * w;
+    const int want = n - (int)ceil(t - h) - w + 1;
+    double m = (double)n - t;
+    for (int it = 0; it < 8 && (int)ceil(m - h) > want; ++it) m = nextafter(m, -1e300);
+    for (int it = 0; it < 8 && (int)ceil(m - h) < want; ++it) m = nextafter(m, 1e300);
+    return m;
+}
+
+__global__ void k_mirror_points(const double2* __restrict__ t, uint64_t n, int n1, int n2, int w,
+                                double2* __restrict__ out) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double2 p = t[k];
+    out[k] = make_double2(mirror_coord(p.x, n1, w), mirror_coord(p.y, n2, w));
+}
+
+// *flag |= (some im(x[k]) != 0)
+__global__ void k_any_imag(const double2* __restrict__ x, uint64_t n, int* __restrict__ flag) {
+    int any = 0;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
+         k += (uint64_t)gridDim.x * blockDim.x)
+        any |= x[k].y != 0.0;
+    if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
 __global__ void k_mul(double2* x, const double2* __restrict__ m, uint64_t n) {
@@ -1225,7 +1329,7 @@ struct SpreadTilesRun {
     static size_t smem() { return (size_t)4 * 32 * W * 24 + 4 * 128 * sizeof(uint32_t) + 4 * 256 * sizeof(uint32_t); }
     static void run(const WindowPoly& P, GridGeom g, TileGeom tg, const uint32_t* bs,
                     const double2* b, const double2* pos, double2* grid, cudaStream_t st,
-                    const uint32_t* bs2, const int* herm) {
+                    const uint32_t* bs2, const int* herm, const SpreadOut* out) {
         static bool attr = false;
         if (!attr) {
             ck(cudaFuncSetAttribute(k_spread_tiles<W, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1245,8 +1349,22 @@ struct SpreadTilesRun {
                                     (int)smem()),
                "smem attr");
         }
+        SpreadOut so;
+        if (out) {
+            so = *out;
+        } else {
+            so.mode = 0;
+            so.rend = tg.pitch ? tg.rhi : g.n1;
+            so.cend = tg.pitch ? tg.chi : g.n2;
+            so.pitch = tg.pitch ? (size_t)tg.pitch : (size_t)g.n2;
+            so.r0 = tg.pitch ? tg.rlo : 0;
+            so.c0 = tg.pitch ? tg.clo : 0;
+            so.nby_run = tg.nby;
+        }
+        if (out && !(use_mma && tg.tr == 16)) throw Error(3, "spread output modes need the DMMA spread");
         if (use_mma && tg.tr == 16)
-            k_spread_mma<W><<<(tiles + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid, bs2, herm);
+            k_spread_mma<W><<<(tg.nbx * so.nby_run + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid, bs2,
+                                                                               herm, so);
         else if (tg.tr == 8)
             k_spread_tiles<W, 8><<<(tiles + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid, bs2, herm);
         else
@@ -1268,7 +1386,8 @@ struct InterpRun {
         const char* e = getenv("SBD_INTERP");
         const double density = (double)n / ((double)g.n1 * (double)g.n2 / (trans ? 2.0 : 4.0));
         const bool use_mma = e ? (e[0] == 'm' || e[0] == 't') : density >= 0.25;
-        const bool use_tile = use_mma && tiles && tiles->n && !(e && e[0] == 'm');
+        const bool use_tile = (use_mma && tiles && tiles->n && !(e && e[0] == 'm')) || hh.hcols;
+        if (hh.hcols && !(tiles && tiles->n)) throw Error(3, "Hermitian band needs the staged interpolation");
         if (use_tile && !acc && !cj) {
             auto go = [&](auto kern, size_t smem, size_t& attr) {
                 if (smem > attr) {
@@ -1369,9 +1488,9 @@ void launch_bin_bounds(const uint32_t* sorted_keys, uint64_t n, uint32_t nbins, 
 void launch_spread_tiles(int w, const WindowPoly& win, GridGeom g, TileGeom tg,
                          const uint32_t* bin_start, const double2* b, const double2* pos,
                          double2* grid, cudaStream_t st, const uint32_t* bin_start2,
-                         const int* herm) {
+                         const int* herm, const SpreadOut* out) {
     if (tg.nbx * tg.nby == 0) return;
-    dispatch_w<SpreadTilesRun>(w, win, g, tg, bin_start, b, pos, grid, st, bin_start2, herm);
+    dispatch_w<SpreadTilesRun>(w, win, g, tg, bin_start, b, pos, grid, st, bin_start2, herm, out);
     count_launch();
     ck(cudaGetLastError(), "k_spread_tiles");
 }
@@ -1438,6 +1557,24 @@ void launch_interp(int w, const WindowPoly& win, GridGeom g, uint64_t n, const d
     ck(cudaGetLastError(), "k_interp");
 }
 
+template <int W>
+struct InterpRealRun {
+    static void run(const WindowPoly& P, GridGeom g, uint64_t n, const double2* pos, const double2* phase,
+                    const double* dx, const double* dy, const double* grid, const uint32_t* perm,
+                    const double2* addend, double2* out, cudaStream_t st) {
+        k_interp_real<W><<<blocks(n, 256), 256, 0, st>>>(P, g, n, pos, phase, dx, dy, grid, perm, addend, out);
+    }
+};
+
+void launch_interp_real(int w, const WindowPoly& win, GridGeom g, uint64_t n, const double2* pos,
+                        const double2* phase, const double* dx, const double* dy, const double* grid,
+                        const uint32_t* perm, const double2* addend, double2* out, cudaStream_t st) {
+    if (!n) return;
+    dispatch_w<InterpRealRun>(w, win, g, n, pos, phase, dx, dy, grid, perm, addend, out, st);
+    count_launch();
+    ck(cudaGetLastError(), "k_interp_real");
+}
+
 void build_tile_starts(const uint32_t* sorted_keys, uint64_t n, int bits, DevBuf<uint32_t>& start,
                        uint32_t& ntiles, cudaStream_t st) {
     ntiles = 0;
@@ -1485,12 +1622,28 @@ void launch_spmv_vec(uint64_t rows, const uint64_t* ro, const uint32_t* cols, co
 }
 
 void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int B, double2* Tt,
-                           int n1, cudaStream_t st) {
+                           int n1, cudaStream_t st, int rin0, int conj_out) {
     if (r1 <= r0) return;
     dim3 grid((unsigned)((B + 31) / 32), (unsigned)((r1 - r0 + 31) / 32));
-    k_band_transpose<<<grid, 256, 0, st>>>(T, n2, r0, r1, b, B, Tt, n1);
+    k_band_transpose<<<grid, 256, 0, st>>>(T, n2, r0, r1, b, B, Tt, n1, rin0, conj_out);
     count_launch();
     ck(cudaGetLastError(), "k_band_transpose");
+}
+
+void launch_mirror_points(const double2* t, uint64_t n, int n1, int n2, int w, double2* out,
+                          cudaStream_t st) {
+    if (!n) return;
+    k_mirror_points<<<blocks(n, 256), 256, 0, st>>>(t, n, n1, n2, w, out);
+    count_launch();
+    ck(cudaGetLastError(), "k_mirror_points");
+}
+
+void launch_any_imag(const double2* x, uint64_t n, int* flag, cudaStream_t st) {
+    ck(cudaMemsetAsync(flag, 0, sizeof(int), st), "imag flag");
+    if (!n) return;
+    k_any_imag<<<(unsigned)std::min<uint64_t>(blocks(n, 256), 148 * 8), 256, 0, st>>>(x, n, flag);
+    count_launch();
+    ck(cudaGetLastError(), "k_any_imag");
 }
 
 void launch_mul(double2* x, const double2* m, uint64_t n, cudaStream_t st) {

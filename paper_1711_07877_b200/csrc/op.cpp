@@ -200,6 +200,13 @@ struct sbd_op {
     uint64_t n_half = 0;           // tag-0 xi nodes (sorted positions [0, n_half))
     DevBuf<double2> kappa_h;       // kappa with self-conjugate nodes halved
     DevBuf<int> herm_flag;
+    // Hermitian-FFT mode on top of the half split (Plan::enable_hfft): needs
+    // the host to know f is real (host buffers are scanned, device buffers
+    // checked with one reduction + sync)
+    bool hfft_ok = false;
+    DevBuf<double2> spec_v;        // conj spectrum at the mirror images (fwd_out order)
+    DevBuf<uint32_t> perm_v;       // fwd_in tag-0 output position -> mirror-image position
+    DevBuf<int> imag_flag;
     StageTimer tm;
     std::mutex mu;
 
@@ -259,6 +266,44 @@ struct sbd_op {
         ck(cudaStreamSynchronize(stream), "operator upload");
         build_fused();
         if (split) build_half(halve);
+        if (herm_ok) build_hfft();
+    }
+
+    void build_hfft() {
+        if (std::getenv("SBD_NO_HFFT")) return;
+        if (!fwd_in->enable_hfft(1, stream)) return;
+        if (!fwd_out->enable_hfft(2, stream)) {
+            fwd_in->hrole = 0;
+            return;
+        }
+        const uint64_t nx = d.n_xi(), n0 = n_half;
+        std::vector<uint32_t> ps(nx), of(n0), pv(n0);
+        if (fwd_in->perm_s.n)
+            ck(cudaMemcpyAsync(ps.data(), fwd_in->perm_s.p, nx * 4, cudaMemcpyDeviceToHost, stream), "perm");
+        else
+            for (uint64_t i = 0; i < nx; ++i) ps[i] = (uint32_t)i;
+        ck(cudaMemcpyAsync(of.data(), fwd_out->hv_of.p, n0 * 4, cudaMemcpyDeviceToHost, stream), "perm");
+        ck(cudaStreamSynchronize(stream), "perm");
+        for (uint64_t v = 0; v < n0; ++v) {
+            if (ps[v] >= n0) return;  // tag-0 outputs must map to tag-0 nodes
+            pv[v] = of[ps[v]];
+        }
+        perm_v.upload(pv.data(), n0, stream);
+        spec_v.alloc(n0);
+        imag_flag.alloc(1);
+        ck(cudaStreamSynchronize(stream), "hfft");
+        hfft_ok = true;
+        if (std::getenv("SBD_VERBOSE")) std::fprintf(stderr, "[sbd] Hermitian FFT mode on\n");
+    }
+
+    // 1 if f (n entries, device) is real; one reduction and a stream sync
+    int device_real(const double2* f, uint64_t n, cudaStream_t st) {
+        if (!imag_flag.n) imag_flag.alloc(1);
+        launch_any_imag(f, n, imag_flag.p, st);
+        int any = 1;
+        ck(cudaMemcpyAsync(&any, imag_flag.p, sizeof(int), cudaMemcpyDeviceToHost, st), "imag flag");
+        ck(cudaStreamSynchronize(st), "imag flag");
+        return any ? 0 : 1;
     }
 
     // Antipodal pairing of the ring quadrature (ring_quadrature.cpp:51-66: ring
@@ -417,9 +462,12 @@ struct sbd_op {
     }
 
     // conv_operator.cpp:301-309 on device buffers, one right-hand side.
-    void apply_one(const double2* f, double2* q, cudaStream_t st) {
+    // real_hint: 1 = f is real, 0 = complex, -1 = unknown (checked on the
+    // device when the Hermitian-FFT mode could use it)
+    void apply_one(const double2* f, double2* q, cudaStream_t st, int real_hint = -1) {
         if (fused) {
             HermArgs hin, hout;
+            const bool hfft_now = hfft_ok && (real_hint == 1 || (real_hint < 0 && device_real(f, d.n_src(), st)));
             if (herm_ok) {
                 ck(cudaMemsetAsync(herm_flag.p, 1, sizeof(int), st), "half flag");
                 hin.flag = hout.flag = herm_flag.p;
@@ -428,6 +476,12 @@ struct sbd_op {
                 hin.clear = true;
                 hout.n = ~0ull;
                 hout.two_re = true;
+                if (hfft_now) {
+                    hin.hfft = hout.hfft = true;
+                    hin.hcols = fwd_in->hcols;
+                    hin.out2 = hout.out2 = spec_v.p;
+                    hin.perm2 = perm_v.p;
+                }
             }
             // spectrum_b = NUFFT-(f) * w * pre_out, with f_sorted kept for the CSR pass
             fwd_in->apply_pruned(f, false, f_sorted.p, spec.p, kappa.p, nullptr, work, st, &tm,
@@ -676,18 +730,23 @@ int sbd_op_get(const sbd_op* op, int which, void* dst, uint64_t* count) {
     });
 }
 
+static void apply_device_rhs(sbd_op* op, const double* d_f, double* d_q, int nrhs, cudaStream_t st,
+                             const int* real_hint) {
+    std::lock_guard<std::mutex> lk(op->mu);
+    DeviceGuard g(op->device);
+    op->tm.stream = st;
+    const auto* f = reinterpret_cast<const double2*>(d_f);
+    auto* q = reinterpret_cast<double2*>(d_q);
+    for (int r = 0; r < nrhs; ++r)
+        op->apply_one(f + (size_t)r * op->d.n_src(), q + (size_t)r * op->d.n_tgt(), st,
+                      real_hint ? real_hint[r] : -1);
+    ck(cudaGetLastError(), "apply");
+}
+
 int sbd_op_apply_device(sbd_op* op, const double* d_f, double* d_q, int nrhs, void* stream) {
     return guarded([&] {
         if (!op || !d_f || !d_q || nrhs < 1) throw Error(SBD_ERR_INVALID_ARGUMENT, "apply: bad argument");
-        std::lock_guard<std::mutex> lk(op->mu);
-        DeviceGuard g(op->device);
-        cudaStream_t st = (cudaStream_t)stream;
-        op->tm.stream = st;
-        const auto* f = reinterpret_cast<const double2*>(d_f);
-        auto* q = reinterpret_cast<double2*>(d_q);
-        for (int r = 0; r < nrhs; ++r)
-            op->apply_one(f + (size_t)r * op->d.n_src(), q + (size_t)r * op->d.n_tgt(), st);
-        ck(cudaGetLastError(), "apply");
+        apply_device_rhs(op, d_f, d_q, nrhs, (cudaStream_t)stream, nullptr);
     });
 }
 
@@ -754,9 +813,21 @@ static int host_apply(sbd_op* op, const double* in, double* out, int nrhs, bool 
             if (op->hq.n < nout * nrhs) op->hq.alloc(nout * nrhs);
             ck(cudaMemcpyAsync(op->hf.p, in, nin * nrhs * 16, cudaMemcpyHostToDevice, op->stream), "H2D f");
         }
-        const int rc = adjoint ? sbd_op_apply_adjoint_device(op, (double*)op->hf.p, (double*)op->hq.p, nrhs, op->stream)
-                               : sbd_op_apply_device(op, (double*)op->hf.p, (double*)op->hq.p, nrhs, op->stream);
-        if (rc) throw Error(rc, g_err);
+        if (adjoint) {
+            const int rc = sbd_op_apply_adjoint_device(op, (double*)op->hf.p, (double*)op->hq.p, nrhs, op->stream);
+            if (rc) throw Error(rc, g_err);
+        } else {
+            // real right-hand sides, decided on the host copy (no device round trip)
+            std::vector<int> real(nrhs, 1);
+            for (int r = 0; r < nrhs; ++r) {
+                const double* x = in + (size_t)r * nin * 2;
+                int any = 0;
+#pragma omp parallel for reduction(| : any) schedule(static)
+                for (int64_t i = 0; i < (int64_t)nin; ++i) any |= x[2 * i + 1] != 0.0;
+                real[r] = !any;
+            }
+            apply_device_rhs(op, (double*)op->hf.p, (double*)op->hq.p, nrhs, op->stream, real.data());
+        }
         std::lock_guard<std::mutex> lk(op->mu);
         DeviceGuard g(op->device);
         ck(cudaMemcpyAsync(out, op->hq.p, nout * nrhs * 16, cudaMemcpyDeviceToHost, op->stream), "D2H q");

@@ -8,6 +8,7 @@
 // with the same operation order. Points and outputs are stored sorted by grid
 // tile for locality.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -274,6 +275,84 @@ Plan::~Plan() {
     if (fft_colA) cufftDestroy(fft_colA);
     if (fft_colB) cufftDestroy(fft_colB);
     if (fft_colT) cufftDestroy(fft_colT);
+    if (hp1) cufftDestroy(hp1);
+    if (hp2) cufftDestroy(hp2);
+}
+
+bool Plan::enable_hfft(int role, cudaStream_t st) {
+    if (!fast || !pruned || dft) return false;
+    const int n1 = ax.n, n2 = ay.n, R = rhi - rlo;
+    const int h2 = n2 / 2 + 1;
+    if (role == 1) {
+        // the spread grid is real only when the prephase is (fcenter exactly 0)
+        if (!tagged_out || !n_out_tiles || ax.fcenter != 0.0 || ay.fcenter != 0.0) return false;
+        hcols = band2 + 1;
+        hreal.alloc((size_t)R * n2);
+        ck(cudaMemsetAsync(hreal.p, 0, hreal.bytes(), st), "hfft zero");
+        hA.alloc((size_t)R * h2);
+        hB.alloc((size_t)hcols * n1);
+        ck(cudaMemsetAsync(hB.p, 0, hB.bytes(), st), "hfft zero");
+        hC.alloc((size_t)hcols * n1);
+        int nr[1] = {n2}, ni[1] = {n2}, no[1] = {h2}, nc[1] = {n1};
+        ckfft(cufftPlanMany(&hp1, 1, nr, ni, 1, n2, no, 1, h2, CUFFT_D2Z, R), "hfft D2Z rows");
+        ckfft(cufftPlanMany(&hp2, 1, nc, nc, 1, n1, nc, 1, n1, CUFFT_Z2Z, hcols), "hfft Z2Z cols");
+    } else if (role == 2) {
+        if (!tagged_pts || !n0_pts) return false;
+        const GridGeom g{n1, n2, 0.5 * w};
+        hv_t.alloc(n0_pts);
+        launch_mirror_points(t.p, n0_pts, n1, n2, w, hv_t.p, st);
+        // the mirror images must fall inside this plan's spread tiles
+        DevBuf<int> ext(4);
+        const int init[4] = {INT_MAX, INT_MIN, INT_MAX, INT_MIN};
+        ck(cudaMemcpyAsync(ext.p, init, sizeof(init), cudaMemcpyHostToDevice, st), "extent init");
+        launch_stencil_extent(hv_t.p, n0_pts, g.half, ext.p, st);
+        int he[4];
+        ck(cudaMemcpyAsync(he, ext.p, sizeof(he), cudaMemcpyDeviceToHost, st), "extent D2H");
+        ck(cudaStreamSynchronize(st), "extent");
+        if (he[0] < rlo || he[1] + w > rhi || he[2] < clo || he[3] + w > chi || clo > n2 / 2) {
+            hv_t = DevBuf<double2>();
+            return false;
+        }
+        // sort the mirror images by spread tile, keep both directions of the map
+        DevBuf<uint32_t> keys(n0_pts), src(n0_pts);
+        launch_tile_keys(hv_t.p, n0_pts, g.half, tg, keys.p, st);
+        launch_iota(src.p, n0_pts, st);
+        sort_by_key(keys.p, src.p, n0_pts, st);
+        DevBuf<double2> sorted(n0_pts);
+        launch_gather(hv_t.p, src.p, sorted.p, n0_pts, st);
+        hv_t = std::move(sorted);
+        const uint32_t nbins = (uint32_t)tg.nbx * (uint32_t)tg.nby;
+        hv_bins.alloc(nbins + 1);
+        launch_bin_bounds(keys.p, n0_pts, nbins, hv_bins.p, st);
+        std::vector<uint32_t> hs(n0_pts), inv(n0_pts);
+        ck(cudaMemcpyAsync(hs.data(), src.p, n0_pts * 4, cudaMemcpyDeviceToHost, st), "mirror map");
+        ck(cudaStreamSynchronize(st), "mirror map");
+        for (uint64_t i = 0; i < n0_pts; ++i) inv[hs[i]] = (uint32_t)i;
+        hv_of.upload(inv.data(), n0_pts, st);
+        // columns m2 in [clo, n2/2] of the Hermitian grid, as full-length columns
+        hnm = n2 / 2 - clo + 1;
+        hnby = std::min(tg.nby, (n2 / 2 + 1 - clo + kTileC - 1) / kTileC);
+        hb1 = n1 / 4;
+        hB1 = 2 * hb1 + 1;
+        hA.alloc((size_t)hnm * n1);
+        ck(cudaMemsetAsync(hA.p, 0, hA.bytes(), st), "hfft zero");
+        hB.alloc((size_t)hnm * n1);
+        hC.alloc((size_t)hB1 * h2);
+        hreal.alloc((size_t)hB1 * n2);
+        std::vector<double> hx(n1), hb(hB1);
+        ck(cudaMemcpyAsync(hx.data(), dx.p, n1 * sizeof(double), cudaMemcpyDeviceToHost, st), "deconv");
+        ck(cudaStreamSynchronize(st), "deconv");
+        for (int r = 0; r < hB1; ++r) hb[r] = hx[r <= hb1 ? r : n1 + r - hB1];
+        hdx_band.upload(hb.data(), hB1, st);
+        int nc[1] = {n1}, nr[1] = {n2}, ni[1] = {h2};
+        ckfft(cufftPlanMany(&hp1, 1, nc, nc, 1, n1, nc, 1, n1, CUFFT_Z2Z, hnm), "hfft Z2Z cols");
+        ckfft(cufftPlanMany(&hp2, 1, nr, ni, 1, h2, nr, 1, n2, CUFFT_Z2D, hB1), "hfft Z2D rows");
+    } else {
+        return false;
+    }
+    ck(cudaStreamSynchronize(st), "hfft setup");
+    hrole = role;
+    return true;
 }
 
 void FftWork::ensure(int n1_, int n2_, int bc_, cudaStream_t st) {
@@ -426,6 +505,72 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         launch_gather_mul(in, perm_t.n ? perm_t.p : nullptr, pre.p, wk.bbuf.p, raw_sorted, np, st, in_lo,
                           in_hi, clear);
         b = wk.bbuf.p;
+    }
+    if (herm && herm->hfft && hrole == 1) {
+        // real grid -> D2Z rows -> conj band transpose (columns 0..n2/4) -> Z2Z columns
+        SpreadOut so;
+        so.mode = 1;
+        so.rgrid = hreal.p;
+        so.pitch = (size_t)n2;
+        so.r0 = rlo;
+        so.c0 = 0;
+        so.rend = rhi;
+        so.cend = chi;
+        so.nby_run = tg.nby;
+        launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, nullptr, st, bs2, hflag, &so);
+        if (tm) tm->stop();
+        if (tm) tm->start(tag_fft);
+        ckfft(cufftSetStream(hp1, st), "cufftSetStream");
+        ckfft(cufftExecD2Z(hp1, hreal.p, reinterpret_cast<cufftDoubleComplex*>(hA.p)), "hfft D2Z");
+        // D2Z is the e^{-} transform: conjugating gives the e^{+} one of a real row
+        launch_band_transpose(hA.p, n2 / 2 + 1, rlo, rhi, band2, hcols, hB.p, ax.n, st, rlo, 1);
+        ckfft(cufftSetStream(hp2, st), "cufftSetStream");
+        ckfft(cufftExecZ2Z(hp2, reinterpret_cast<cufftDoubleComplex*>(hB.p),
+                           reinterpret_cast<cufftDoubleComplex*>(hC.p), CUFFT_INVERSE),
+              "hfft Z2Z");
+        count_launch(4);
+        if (tm) tm->stop();
+        if (tm) tm->start(tag_interp);
+        const GridGeom gt{ax.n, bc, 0.5 * w};
+        launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx.p, dy_band.p, hC.p, perm_p, out_p, 0, 0, st,
+                      add_p, /*transposed=*/true, &otiles, hp);
+        if (tm) tm->stop();
+        return;
+    }
+    if (herm && herm->hfft && hrole == 2) {
+        // tag-0 points + mirror images -> Hermitian grid columns m2 <= n2/2
+        // (transposed) -> Z2Z columns -> band rows -> Z2D rows -> real band
+        SpreadOut so;
+        so.mode = 2;
+        so.pitch = (size_t)ax.n;
+        so.r0 = 0;
+        so.c0 = clo;
+        so.rend = rhi;
+        so.cend = clo + hnm;
+        so.nby_run = hnby;
+        so.pos2 = hv_t.p;
+        so.b2 = herm->out2;
+        launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, hA.p, st, hv_bins.p, nullptr, &so);
+        if (tm) tm->stop();
+        if (tm) tm->start(tag_fft);
+        const int h2 = n2 / 2 + 1;
+        ckfft(cufftSetStream(hp1, st), "cufftSetStream");
+        ckfft(cufftExecZ2Z(hp1, reinterpret_cast<cufftDoubleComplex*>(hA.p),
+                           reinterpret_cast<cufftDoubleComplex*>(hB.p), CUFFT_INVERSE),
+              "hfft Z2Z cols");
+        // the C2R input is clobbered by cuFFT: re-zero the columns left of the support
+        ck(cudaMemset2DAsync(hC.p, (size_t)h2 * sizeof(double2), 0, (size_t)clo * sizeof(double2), hB1, st),
+           "hfft zero");
+        launch_band_transpose(hB.p, ax.n, 0, hnm, hb1, hB1, hC.p + clo, h2, st);
+        ckfft(cufftSetStream(hp2, st), "cufftSetStream");
+        ckfft(cufftExecZ2D(hp2, reinterpret_cast<cufftDoubleComplex*>(hC.p), hreal.p), "hfft Z2D");
+        count_launch(4);
+        if (tm) tm->stop();
+        if (tm) tm->start(tag_interp);
+        const GridGeom gr{hB1, n2, 0.5 * w};
+        launch_interp_real(w, win, gr, nout, s_p, post_p, hdx_band.p, dy.p, hreal.p, perm_p, add_p, out_p, st);
+        if (tm) tm->stop();
+        return;
     }
     if (dft) {
         // compact support grid -> rows pass -> band-columns pass -> transposed band

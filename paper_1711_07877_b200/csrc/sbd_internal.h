@@ -226,6 +226,24 @@ class Plan {
     DevBuf<double2> tw1, tw2;  // e^{+2 pi i q / n} tables for the two axes
     PrunedPass pass1{}, pass2{};
 
+    // Hermitian-FFT mode for a real input (op.cpp). Role 1 (fwd_in): the
+    // spread grid is real: real rows -> D2Z rows -> conjugated band transpose
+    // (columns 0..n2/4 only) -> Z2Z columns; the xi interpolation reads the
+    // negative columns by conjugate symmetry. Role 2 (fwd_out): the tag-0
+    // points plus their mirror images (conjugate values) make the spread grid
+    // Hermitian; only the columns m2 <= n2/2 are spread (transposed), then Z2Z
+    // columns -> band-row transpose -> Z2D rows give the real band, and the
+    // target interpolation reads it.
+    int hrole = 0;
+    cufftHandle hp1 = 0, hp2 = 0;
+    mutable DevBuf<double> hreal;
+    mutable DevBuf<double2> hA, hB, hC;
+    int hnm = 0, hnby = 0, hb1 = 0, hB1 = 0, hcols = 0;
+    DevBuf<double2> hv_t;             // role 2: mirrored tag-0 points, sorted by tile
+    DevBuf<uint32_t> hv_bins, hv_of;  // their bins; tag-0 sorted position -> mirrored position
+    DevBuf<double> hdx_band;          // role 2: deconvolution of the band rows
+    bool enable_hfft(int role, cudaStream_t st);
+
     uint64_t cells() const { return fast ? (uint64_t)ax.n * (uint64_t)ay.n : 0; }
     size_t device_bytes() const;
 
@@ -272,6 +290,28 @@ struct HermArgs {
     const double2* mult = nullptr;
     bool two_re = false;
     bool clear = false;
+    // Hermitian-FFT mode (Plan::enable_hfft): the xi interpolation reads a
+    // band stored for columns [0, hcols) only (the rest by conjugate symmetry)
+    // and also writes conj(value) to out2[perm2[v]] (the mirrored spread's input)
+    int hcols = 0;
+    double2* out2 = nullptr;
+    const uint32_t* perm2 = nullptr;
+    bool hfft = false;  // take the Hermitian-FFT pipelines in apply_pruned
+};
+
+// Output of the tile-owned spread: mode 0 = complex grid[(row-r0)*pitch +
+// col-c0]; 1 = real parts into rgrid rows (same indexing); 2 = transposed
+// complex grid[(col-c0)*pitch + row-r0]. Rows < rend and columns < cend are
+// written; only the first nby_run tile columns run. pos2/b2: the point
+// arrays of the second bin set (nullptr: the first set's arrays).
+struct SpreadOut {
+    int mode = 0;
+    double* rgrid = nullptr;
+    size_t pitch = 0;
+    int r0 = 0, c0 = 0, rend = 0, cend = 0;
+    int nby_run = 0;
+    const double2* pos2 = nullptr;
+    const double2* b2 = nullptr;
 };
 
 // ---------------------------------------------------------------- kernels
@@ -305,9 +345,20 @@ void launch_bin_bounds(const uint32_t* sorted_keys, uint64_t n, uint32_t nbins, 
 void launch_spread_tiles(int w, const WindowPoly& win, GridGeom g, TileGeom tg,
                          const uint32_t* bin_start, const double2* b, const double2* pos,
                          double2* grid, cudaStream_t st, const uint32_t* bin_start2 = nullptr,
-                         const int* herm = nullptr);
+                         const int* herm = nullptr, const SpreadOut* out = nullptr);
+// Tt[c * n1 + r] = T[(r - rin0) * n2 + m(c)] for r in [r0, r1), c < B,
+// m(c) = c (c <= b) else n2 - B + c
 void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int B, double2* Tt,
-                           int n1, cudaStream_t st);
+                           int n1, cudaStream_t st, int rin0 = 0, int conj_out = 0);
+void launch_mirror_points(const double2* t, uint64_t n, int n1, int n2, int w, double2* out,
+                          cudaStream_t st);
+// *flag = 1 if some x[k] has a nonzero imaginary part, else 0
+void launch_any_imag(const double2* x, uint64_t n, int* flag, cudaStream_t st);
+// interpolation from a real band grid (row-major [r][c], pitch g.n2):
+// out[perm?perm[k]:k] = Re(sum taps * dx dy * grid * phase[k]) + addend[k]
+void launch_interp_real(int w, const WindowPoly& win, GridGeom g, uint64_t n, const double2* pos,
+                        const double2* phase, const double* dx, const double* dy, const double* grid,
+                        const uint32_t* perm, const double2* addend, double2* out, cudaStream_t st);
 // b[k] = in[perm[k]] phase[k] for k in [lo, hi) (zero elsewhere); raw[k] = in[perm[k]].
 // clear (optional): set to 0 when some in[k] has a nonzero imaginary part.
 void launch_gather_mul(const double2* in, const uint32_t* perm, const double2* phase, double2* b,

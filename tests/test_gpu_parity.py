@@ -363,3 +363,24 @@ def test_helmholtz_real_input_takes_full_path(ops, oracle):
     f = np.random.default_rng(9).standard_normal(len(g["f"])) + 0j
     q = ops["helm_disk_n800"].apply(f)
     assert rel_l2(q, oracle.op(path).apply(f)) <= PARITY
+
+
+@pytest.mark.parametrize("name", HALF_CASES)
+def test_hermitian_fft_mode_device_and_host_agree(ops, name, monkeypatch):
+    # Real f: the Hermitian-FFT pipelines (real-grid D2Z, mirrored spread +
+    # Z2D) are chosen by a host scan (sbd_op_apply) or a device check
+    # (sbd_op_apply_device); both must equal the half split without them.
+    import torch
+    path, g = golden(name)
+    f = np.random.default_rng(31).standard_normal(len(g["f"])) + 0j
+    q = ops[name].apply(f)
+    fd = torch.from_numpy(f.view(np.float64).copy()).cuda()
+    qd = torch.zeros(2 * len(q), dtype=torch.float64, device="cuda")
+    ops[name].apply_device(fd.data_ptr(), qd.data_ptr(), 1, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert rel_l2(qd.cpu().numpy().view(np.complex128), q) <= 1e-14
+    monkeypatch.setenv("SBD_NO_HFFT", "1")
+    plain = sbd.CompressedOperator.load(path)
+    monkeypatch.delenv("SBD_NO_HFFT")
+    qp = plain.apply(f)
+    assert rel_l2(q.real, qp.real) <= 1e-13 and rel_l2(q, qp) <= 1e-13
