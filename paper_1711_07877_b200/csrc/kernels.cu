@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
                     if ((unsigned)cc < (unsigned)W) bv = s_wy[node * W + cc];
                 }
                 dmma(cr[i][j][0], cr[i][j][1], a_r, bv);
-                dmma(ci[i][j][0], ci[i][j][1], a_i, bv);
+                if (so.mode != 1) dmma(ci[i][j][0], ci[i][j][1], a_i, bv);  // mode 1: real grid
             }
         }
         __syncwarp();

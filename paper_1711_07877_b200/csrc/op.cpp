@@ -361,7 +361,9 @@ struct sbd_op {
                 if (std::sqrt(sx * sx + sy * sy) > 1e-12 * mag || d.weights[2 * j] != d.weights[2 * q])
                     return false;
                 if (mirrored(j, q)) {
-                    tag[q] = 1;
+                    // compute the node with xi_y <= 0: the source-side NUFFT (sign -1)
+                    // then reads mostly the stored, non-negative band columns
+                    tag[xi[2 * j + 1] > 0.0 ? j : q] = 1;
                 } else {
                     halve.push_back(j);
                     halve.push_back(q);
