@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
                     if ((unsigned)cc < (unsigned)W) bv = s_wy[node * W + cc];
                 }
                 dmma(cr[i][j][0], cr[i][j][1], a_r, bv);
-                if (so.mode != 1) dmma(ci[i][j][0], ci[i][j][1], a_i, bv);  // mode 1: real grid
+                if (so.mode < 3) dmma(ci[i][j][0], ci[i][j][1], a_i, bv);  // mode 3: real grid
             }
         }
         __syncwarp();
@@ -501,6 +501,9 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
                     grid[(size_t)(row - so.r0) * so.pitch + (col + h - so.c0)] = make_double2(re, im);
                 else if (so.mode == 1)  // real grid rows (the imaginary part is zero)
                     so.rgrid[(size_t)(row - so.r0) * so.pitch + (col + h - so.c0)] = re;
+                else if (so.mode == 3)  // real rows packed in pairs: row 2k -> .x, 2k+1 -> .y of row k
+                    so.rgrid[2 * ((size_t)((row - so.r0) >> 1) * so.pitch + (col + h - so.c0)) +
+                             ((row - so.r0) & 1)] = re;
                 else  // transposed: column-major, full-length columns
                     grid[(size_t)(col + h - so.c0) * so.pitch + (row - so.r0)] = make_double2(re, im);
             }
@@ -839,10 +842,11 @@ __global__ void __launch_bounds__(256) k_interp_real(WindowPoly P, GridGeom g, u
     for (int i = 0; i < W; ++i) {
         int mx = mx0 + i;
         if (mx >= g.n1) mx -= g.n1;
-        const double* row = grid + (size_t)mx * g.n2;
+        // rows packed in pairs: row mx is component (mx & 1) of complex row mx >> 1
+        const double* row = grid + 2 * (size_t)(mx >> 1) * g.n2 + (mx & 1);
         double rr = 0.0;
 #pragma unroll
-        for (int j = 0; j < W; ++j) rr = fma(__ldg(row + myj[j]), wy[j], rr);
+        for (int j = 0; j < W; ++j) rr = fma(__ldg(row + 2 * myj[j]), wy[j], rr);
         ar = fma(rr, dxt ? wx[i] * dxt[mx] : wx[i], ar);
     }
     const double2 ph = phase[v];
@@ -1253,6 +1257,74 @@ __global__ void k_any_imag(const double2* __restrict__ x, uint64_t n, int* __res
     if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
+// Packed real rows (row 2k in Re, 2k+1 in Im of row k of T, transformed with
+// e^{+}): untangle Z_a(j) = (Z(j) + conj Z(-j))/2, Z_b(j) = (Z(j) - conj Z(-j))/(2i)
+// for columns j in [0, B) and write them transposed: Tt[j * n1 + r0 + r].
+__global__ void __launch_bounds__(256) k_untangle_transpose(const double2* __restrict__ T, int n2, int nr,
+                                                            int B, double2* __restrict__ Tt, int n1,
+                                                            int r0) {
+    __shared__ double2 sa[16][33], sb[16][33];
+    const int cb = blockIdx.x * 32, kb = blockIdx.y * 16;  // 32 columns x 16 packed rows
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+#pragma unroll
+    for (int q = 0; q < 16; q += 8) {
+        const int k = kb + ty + q, c = cb + tx;
+        if (k < nr && c < B) {
+            sa[ty + q][tx] = T[(size_t)k * n2 + c];
+            sb[ty + q][tx] = T[(size_t)k * n2 + (c ? n2 - c : 0)];
+        }
+    }
+    __syncthreads();
+    // output: 32 columns x 32 real rows (two per packed row)
+#pragma unroll
+    for (int q = 0; q < 32; q += 8) {
+        const int c = cb + ty + q, rr = tx;  // rr: real row within the block
+        const int k = kb + (rr >> 1);
+        if (k < nr && c < B) {
+            const double2 a = sa[rr >> 1][ty + q], b = sb[rr >> 1][ty + q];
+            double2 v;
+            if (rr & 1)
+                v = make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x));
+            else
+                v = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+            Tt[(size_t)c * n1 + r0 + 2 * k + (rr & 1)] = v;
+        }
+    }
+}
+
+// Pack pairs of Hermitian band rows for one complex transform each: band row
+// c (mode j1(c)) has half-spectrum X_c[m] = Y[(m - m0) * n1 + j1(c)] for m in
+// [m0, n2/2] (zero below m0); row k of Z (full length n2, m in [m0, n2 - m0])
+// = X_{2k}(m) + i X_{2k+1}(m) with X(m) = conj X(n2 - m) for m > n2/2.
+__global__ void __launch_bounds__(256) k_pack_rows(const double2* __restrict__ Y, int n1, int m0,
+                                                   int n2, int b1, int B1, double2* __restrict__ Z) {
+    __shared__ double2 sy[32][33];  // [m][band row]
+    const int mb = m0 + blockIdx.x * 32, cb = blockIdx.y * 32;  // 32 source columns m x 32 band rows
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int mhi = n2 / 2;
+#pragma unroll
+    for (int q = 0; q < 32; q += 8) {
+        const int m = mb + ty + q, c = cb + tx;
+        double2 v = make_double2(0.0, 0.0);
+        if (m <= mhi && c < B1) v = Y[(size_t)(m - m0) * n1 + (c <= b1 ? c : n1 - B1 + c)];
+        sy[ty + q][tx] = v;
+    }
+    __syncthreads();
+    // each source column m feeds output columns m and (if m < n2/2, m > 0) n2 - m (conjugated)
+#pragma unroll
+    for (int q = 0; q < 16; q += 8) {
+        const int kk = ty + q;  // packed row within the block (16 per block)
+        const int k = (cb >> 1) + kk;
+        const int m = mb + tx;
+        if (m > mhi || 2 * k >= B1) continue;
+        const double2 a = sy[tx][2 * kk];
+        const double2 b = (2 * k + 1 < B1) ? sy[tx][2 * kk + 1] : make_double2(0.0, 0.0);
+        // a + i b, and for the mirrored column conj(a) + i conj(b)
+        Z[(size_t)k * n2 + m] = make_double2(a.x - b.y, a.y + b.x);
+        if (m > 0 && m < mhi) Z[(size_t)k * n2 + (n2 - m)] = make_double2(a.x + b.y, -a.y + b.x);
+    }
+}
+
 __global__ void k_mul(double2* x, const double2* __restrict__ m, uint64_t n) {
     const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (k < n) x[k] = cmul(x[k], m[k]);
@@ -1628,6 +1700,24 @@ void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int 
     k_band_transpose<<<grid, 256, 0, st>>>(T, n2, r0, r1, b, B, Tt, n1, rin0, conj_out);
     count_launch();
     ck(cudaGetLastError(), "k_band_transpose");
+}
+
+void launch_untangle_transpose(const double2* T, int n2, int nr, int B, double2* Tt, int n1, int r0,
+                               cudaStream_t st) {
+    if (nr <= 0 || B <= 0) return;
+    dim3 grid((unsigned)((B + 31) / 32), (unsigned)((nr + 15) / 16));
+    k_untangle_transpose<<<grid, 256, 0, st>>>(T, n2, nr, B, Tt, n1, r0);
+    count_launch();
+    ck(cudaGetLastError(), "k_untangle_transpose");
+}
+
+void launch_pack_rows(const double2* Y, int n1, int m0, int n2, int b1, int B1, double2* Z, cudaStream_t st) {
+    const int nm = n2 / 2 - m0 + 1;
+    if (nm <= 0) return;
+    dim3 grid((unsigned)((nm + 31) / 32), (unsigned)((B1 + 31) / 32));
+    k_pack_rows<<<grid, 256, 0, st>>>(Y, n1, m0, n2, b1, B1, Z);
+    count_launch();
+    ck(cudaGetLastError(), "k_pack_rows");
 }
 
 void launch_mirror_points(const double2* t, uint64_t n, int n1, int n2, int w, double2* out,

@@ -282,19 +282,19 @@ Plan::~Plan() {
 bool Plan::enable_hfft(int role, cudaStream_t st) {
     if (!fast || !pruned || dft) return false;
     const int n1 = ax.n, n2 = ay.n, R = rhi - rlo;
-    const int h2 = n2 / 2 + 1;
     if (role == 1) {
         // the spread grid is real only when the prephase is (fcenter exactly 0)
         if (!tagged_out || !n_out_tiles || ax.fcenter != 0.0 || ay.fcenter != 0.0) return false;
+        // real rows packed in pairs into R/2 complex rows (R is a multiple of 16)
         hcols = band2 + 1;
-        hreal.alloc((size_t)R * n2);
-        ck(cudaMemsetAsync(hreal.p, 0, hreal.bytes(), st), "hfft zero");
-        hA.alloc((size_t)R * h2);
+        hA.alloc((size_t)(R / 2) * n2);
+        ck(cudaMemsetAsync(hA.p, 0, hA.bytes(), st), "hfft zero");
+        hD.alloc((size_t)(R / 2) * n2);
         hB.alloc((size_t)hcols * n1);
         ck(cudaMemsetAsync(hB.p, 0, hB.bytes(), st), "hfft zero");
         hC.alloc((size_t)hcols * n1);
-        int nr[1] = {n2}, ni[1] = {n2}, no[1] = {h2}, nc[1] = {n1};
-        ckfft(cufftPlanMany(&hp1, 1, nr, ni, 1, n2, no, 1, h2, CUFFT_D2Z, R), "hfft D2Z rows");
+        int nr[1] = {n2}, nc[1] = {n1};
+        ckfft(cufftPlanMany(&hp1, 1, nr, nr, 1, n2, nr, 1, n2, CUFFT_Z2Z, R / 2), "hfft Z2Z rows");
         ckfft(cufftPlanMany(&hp2, 1, nc, nc, 1, n1, nc, 1, n1, CUFFT_Z2Z, hcols), "hfft Z2Z cols");
     } else if (role == 2) {
         if (!tagged_pts || !n0_pts) return false;
@@ -337,16 +337,18 @@ bool Plan::enable_hfft(int role, cudaStream_t st) {
         hA.alloc((size_t)hnm * n1);
         ck(cudaMemsetAsync(hA.p, 0, hA.bytes(), st), "hfft zero");
         hB.alloc((size_t)hnm * n1);
-        hC.alloc((size_t)hB1 * h2);
-        hreal.alloc((size_t)hB1 * n2);
+        const int K = (hB1 + 1) / 2;  // band rows packed in pairs
+        hC.alloc((size_t)K * n2);
+        ck(cudaMemsetAsync(hC.p, 0, hC.bytes(), st), "hfft zero");
+        hD.alloc((size_t)K * n2);
         std::vector<double> hx(n1), hb(hB1);
         ck(cudaMemcpyAsync(hx.data(), dx.p, n1 * sizeof(double), cudaMemcpyDeviceToHost, st), "deconv");
         ck(cudaStreamSynchronize(st), "deconv");
         for (int r = 0; r < hB1; ++r) hb[r] = hx[r <= hb1 ? r : n1 + r - hB1];
         hdx_band.upload(hb.data(), hB1, st);
-        int nc[1] = {n1}, nr[1] = {n2}, ni[1] = {h2};
+        int nc[1] = {n1}, nr[1] = {n2};
         ckfft(cufftPlanMany(&hp1, 1, nc, nc, 1, n1, nc, 1, n1, CUFFT_Z2Z, hnm), "hfft Z2Z cols");
-        ckfft(cufftPlanMany(&hp2, 1, nr, ni, 1, h2, nr, 1, n2, CUFFT_Z2D, hB1), "hfft Z2D rows");
+        ckfft(cufftPlanMany(&hp2, 1, nr, nr, 1, n2, nr, 1, n2, CUFFT_Z2Z, K), "hfft Z2Z rows");
     } else {
         return false;
     }
@@ -507,10 +509,11 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         b = wk.bbuf.p;
     }
     if (herm && herm->hfft && hrole == 1) {
-        // real grid -> D2Z rows -> conj band transpose (columns 0..n2/4) -> Z2Z columns
+        // real rows packed in pairs -> Z2Z rows -> untangle + band transpose
+        // (columns 0..n2/4) -> Z2Z columns
         SpreadOut so;
-        so.mode = 1;
-        so.rgrid = hreal.p;
+        so.mode = 3;
+        so.rgrid = reinterpret_cast<double*>(hA.p);
         so.pitch = (size_t)n2;
         so.r0 = rlo;
         so.c0 = 0;
@@ -521,9 +524,10 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         if (tm) tm->stop();
         if (tm) tm->start(tag_fft);
         ckfft(cufftSetStream(hp1, st), "cufftSetStream");
-        ckfft(cufftExecD2Z(hp1, hreal.p, reinterpret_cast<cufftDoubleComplex*>(hA.p)), "hfft D2Z");
-        // D2Z is the e^{-} transform: conjugating gives the e^{+} one of a real row
-        launch_band_transpose(hA.p, n2 / 2 + 1, rlo, rhi, band2, hcols, hB.p, ax.n, st, rlo, 1);
+        ckfft(cufftExecZ2Z(hp1, reinterpret_cast<cufftDoubleComplex*>(hA.p),
+                           reinterpret_cast<cufftDoubleComplex*>(hD.p), CUFFT_INVERSE),
+              "hfft Z2Z rows");
+        launch_untangle_transpose(hD.p, n2, (rhi - rlo) / 2, hcols, hB.p, ax.n, rlo, st);
         ckfft(cufftSetStream(hp2, st), "cufftSetStream");
         ckfft(cufftExecZ2Z(hp2, reinterpret_cast<cufftDoubleComplex*>(hB.p),
                            reinterpret_cast<cufftDoubleComplex*>(hC.p), CUFFT_INVERSE),
@@ -553,22 +557,23 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, hA.p, st, hv_bins.p, nullptr, &so);
         if (tm) tm->stop();
         if (tm) tm->start(tag_fft);
-        const int h2 = n2 / 2 + 1;
         ckfft(cufftSetStream(hp1, st), "cufftSetStream");
         ckfft(cufftExecZ2Z(hp1, reinterpret_cast<cufftDoubleComplex*>(hA.p),
                            reinterpret_cast<cufftDoubleComplex*>(hB.p), CUFFT_INVERSE),
               "hfft Z2Z cols");
-        // the C2R input is clobbered by cuFFT: re-zero the columns left of the support
-        ck(cudaMemset2DAsync(hC.p, (size_t)h2 * sizeof(double2), 0, (size_t)clo * sizeof(double2), hB1, st),
-           "hfft zero");
-        launch_band_transpose(hB.p, ax.n, 0, hnm, hb1, hB1, hC.p + clo, h2, st);
+        // two Hermitian band rows per complex row: their transforms are the
+        // real and imaginary parts of one e^{+} transform
+        launch_pack_rows(hB.p, ax.n, clo, n2, hb1, hB1, hC.p, st);
         ckfft(cufftSetStream(hp2, st), "cufftSetStream");
-        ckfft(cufftExecZ2D(hp2, reinterpret_cast<cufftDoubleComplex*>(hC.p), hreal.p), "hfft Z2D");
+        ckfft(cufftExecZ2Z(hp2, reinterpret_cast<cufftDoubleComplex*>(hC.p),
+                           reinterpret_cast<cufftDoubleComplex*>(hD.p), CUFFT_INVERSE),
+              "hfft Z2Z rows");
         count_launch(4);
         if (tm) tm->stop();
         if (tm) tm->start(tag_interp);
         const GridGeom gr{hB1, n2, 0.5 * w};
-        launch_interp_real(w, win, gr, nout, s_p, post_p, hdx_band.p, dy.p, hreal.p, perm_p, add_p, out_p, st);
+        launch_interp_real(w, win, gr, nout, s_p, post_p, hdx_band.p, dy.p,
+                           reinterpret_cast<const double*>(hD.p), perm_p, add_p, out_p, st);
         if (tm) tm->stop();
         return;
     }

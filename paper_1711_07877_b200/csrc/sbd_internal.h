@@ -227,17 +227,16 @@ class Plan {
     PrunedPass pass1{}, pass2{};
 
     // Hermitian-FFT mode for a real input (op.cpp). Role 1 (fwd_in): the
-    // spread grid is real: real rows -> D2Z rows -> conjugated band transpose
-    // (columns 0..n2/4 only) -> Z2Z columns; the xi interpolation reads the
-    // negative columns by conjugate symmetry. Role 2 (fwd_out): the tag-0
-    // points plus their mirror images (conjugate values) make the spread grid
-    // Hermitian; only the columns m2 <= n2/2 are spread (transposed), then Z2Z
-    // columns -> band-row transpose -> Z2D rows give the real band, and the
-    // target interpolation reads it.
+    // spread grid is real; its rows are packed in pairs into complex rows ->
+    // Z2Z rows -> untangle + transpose of the columns 0..n2/4 -> Z2Z columns;
+    // the xi interpolation reads the negative columns by conjugate symmetry.
+    // Role 2 (fwd_out): the tag-0 points plus their mirror images (conjugate
+    // values) make the spread grid Hermitian; only the columns m2 <= n2/2 are
+    // spread (transposed) -> Z2Z columns -> band rows, two per complex row ->
+    // Z2Z rows give the real band for the target interpolation.
     int hrole = 0;
     cufftHandle hp1 = 0, hp2 = 0;
-    mutable DevBuf<double> hreal;
-    mutable DevBuf<double2> hA, hB, hC;
+    mutable DevBuf<double2> hA, hB, hC, hD;
     int hnm = 0, hnby = 0, hb1 = 0, hB1 = 0, hcols = 0;
     DevBuf<double2> hv_t;             // role 2: mirrored tag-0 points, sorted by tile
     DevBuf<uint32_t> hv_bins, hv_of;  // their bins; tag-0 sorted position -> mirrored position
@@ -305,7 +304,7 @@ struct HermArgs {
 // written; only the first nby_run tile columns run. pos2/b2: the point
 // arrays of the second bin set (nullptr: the first set's arrays).
 struct SpreadOut {
-    int mode = 0;
+    int mode = 0;  // 3 = real rows packed in pairs (row 2k -> Re, 2k+1 -> Im of row k)
     double* rgrid = nullptr;
     size_t pitch = 0;
     int r0 = 0, c0 = 0, rend = 0, cend = 0;
@@ -354,7 +353,13 @@ void launch_mirror_points(const double2* t, uint64_t n, int n1, int n2, int w, d
                           cudaStream_t st);
 // *flag = 1 if some x[k] has a nonzero imaginary part, else 0
 void launch_any_imag(const double2* x, uint64_t n, int* flag, cudaStream_t st);
-// interpolation from a real band grid (row-major [r][c], pitch g.n2):
+// packed real rows -> untangled, transposed half band (see kernels.cu)
+void launch_untangle_transpose(const double2* T, int n2, int nr, int B, double2* Tt, int n1, int r0,
+                               cudaStream_t st);
+// Hermitian band rows from half-plane columns -> pairs packed into full rows
+void launch_pack_rows(const double2* Y, int n1, int m0, int n2, int b1, int B1, double2* Z, cudaStream_t st);
+// interpolation from a real band grid whose rows are packed in pairs (row r =
+// component r & 1 of complex row r >> 1, complex pitch g.n2):
 // out[perm?perm[k]:k] = Re(sum taps * dx dy * grid * phase[k]) + addend[k]
 void launch_interp_real(int w, const WindowPoly& win, GridGeom g, uint64_t n, const double2* pos,
                         const double2* phase, const double* dx, const double* dy, const double* grid,
