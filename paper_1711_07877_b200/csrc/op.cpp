@@ -210,7 +210,14 @@ struct sbd_op {
     StageTimer tm;
     std::mutex mu;
 
+    // optional second stream for the CSR pass (SBD_OVERLAP, see apply_one)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_f = nullptr, ev_qs = nullptr;
+
     ~sbd_op() {
+        if (ev_f) cudaEventDestroy(ev_f);
+        if (ev_qs) cudaEventDestroy(ev_qs);
+        if (side) cudaStreamDestroy(side);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -489,12 +496,32 @@ struct sbd_op {
             fwd_in->apply_pruned(f, false, f_sorted.p, spec.p, kappa.p, nullptr, work, st, &tm,
                                  "spread_src", "fft_in", "interp_xi", 0, ~0ull, 0, ~0ull,
                                  herm_ok ? &hin : nullptr);
-            if (tm.on) tm.start("spmv");
-            launch_spmv_vec(d.n_tgt(), ro_s.p, cols_s.p, vals_s.p, f_sorted.p, qs.p, st);
-            if (tm.on) tm.stop();
+            cudaEvent_t wait = nullptr;
+            // SBD_OVERLAP=1 runs the CSR pass on a second stream beside the xi
+            // spread and the second FFT (measured: no gain on config 4 -- the
+            // overlapped kernels slow down by the CSR pass's time)
+            static const bool overlap = std::getenv("SBD_OVERLAP") != nullptr;
+            if (!overlap) {
+                if (tm.on) tm.start("spmv");
+                launch_spmv_vec(d.n_tgt(), ro_s.p, cols_s.p, vals_s.p, f_sorted.p, qs.p, st);
+                if (tm.on) tm.stop();
+            } else {
+                if (!side) {
+                    ck(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "stream");
+                    ck(cudaEventCreateWithFlags(&ev_f, cudaEventDisableTiming), "event");
+                    ck(cudaEventCreateWithFlags(&ev_qs, cudaEventDisableTiming), "event");
+                }
+                ck(cudaEventRecord(ev_f, st), "event");
+                ck(cudaStreamWaitEvent(side, ev_f, 0), "wait");
+                if (tm.on) tm.start("spmv", side);
+                launch_spmv_vec(d.n_tgt(), ro_s.p, cols_s.p, vals_s.p, f_sorted.p, qs.p, side);
+                if (tm.on) tm.stop(side);
+                ck(cudaEventRecord(ev_qs, side), "event");
+                wait = ev_qs;
+            }
             // q = NUFFT+(spectrum) + D f, scattered to the caller's target order
             fwd_out->apply_pruned(spec.p, true, nullptr, q, nullptr, qs.p, work, st, &tm, "spread_xi",
-                                  "fft_out", "interp_tgt", 0, ~0ull, 0, ~0ull, herm_ok ? &hout : nullptr);
+                                  "fft_out", "interp_tgt", 0, ~0ull, 0, ~0ull, herm_ok ? &hout : nullptr, wait);
             return;
         }
         fwd_in->apply(f, spec.p, work, st, &tm, w_in.p, "spread_src", "fft_in", "interp_xi");

@@ -469,7 +469,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
                         const double2* mult, const double2* addend, FftWork& wk, cudaStream_t st,
                         StageTimer* tm, const char* tag_spread, const char* tag_fft,
                         const char* tag_interp, uint64_t in_lo, uint64_t in_hi, uint64_t out_lo,
-                        uint64_t out_hi, const HermArgs* herm) const {
+                        uint64_t out_hi, const HermArgs* herm, cudaEvent_t before_interp) const {
     out_hi = std::min<uint64_t>(out_hi, nf);
     out_lo = std::min(out_lo, out_hi);
     const uint64_t nout = out_hi - out_lo;
@@ -534,6 +534,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
               "hfft Z2Z");
         count_launch(4);
         if (tm) tm->stop();
+        if (before_interp) ck(cudaStreamWaitEvent(st, before_interp, 0), "wait");
         if (tm) tm->start(tag_interp);
         const GridGeom gt{ax.n, bc, 0.5 * w};
         launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx.p, dy_band.p, hC.p, perm_p, out_p, 0, 0, st,
@@ -570,6 +571,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
               "hfft Z2Z rows");
         count_launch(4);
         if (tm) tm->stop();
+        if (before_interp) ck(cudaStreamWaitEvent(st, before_interp, 0), "wait");
         if (tm) tm->start(tag_interp);
         const GridGeom gr{hB1, n2, 0.5 * w};
         launch_interp_real(w, win, gr, nout, s_p, post_p, hdx_band.p, dy.p,
@@ -591,6 +593,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         wk.gc0 = 0;
         wk.gc1 = wk.n2;
         wk.g_pitch = wk.n2;
+        if (before_interp) ck(cudaStreamWaitEvent(st, before_interp, 0), "wait");
         if (tm) tm->start(tag_interp);
         const GridGeom gt{b1c, bc, 0.5 * w};
         launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx_band.p, dy_band.p, wk.bandT.p, perm_p,
@@ -643,6 +646,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         ckfft(cufftExecZ2Z(fft_colT, Tt, BT, CUFFT_INVERSE), "fft cols T");
         count_launch(2);
         if (tm) tm->stop();
+        if (before_interp) ck(cudaStreamWaitEvent(st, before_interp, 0), "wait");
         if (tm) tm->start(tag_interp);
         const GridGeom gt{ax.n, bc, 0.5 * w};
         launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx.p, dy_band.p, wk.bandT.p, perm_p,
@@ -657,7 +661,8 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
     ckfft(cufftExecZ2Z(fft_colB, T + (n2 - band2), B + (band2 + 1), CUFFT_INVERSE), "fft cols B");
     count_launch(3);
     if (tm) tm->stop();
-    if (tm) tm->start(tag_interp);
+    if (before_interp) ck(cudaStreamWaitEvent(st, before_interp, 0), "wait");
+        if (tm) tm->start(tag_interp);
     const GridGeom gb{ax.n, bc, 0.5 * w};
     launch_interp(w, win, gb, nout, s_p, post_p, mult_p, dx.p, dy_band.p, wk.band.p, perm_p, out_p, 0,
                   0, st, add_p, false, &otiles, hp);
@@ -734,19 +739,19 @@ void StageTimer::reset() {
     end.clear();
     names.clear();
 }
-void StageTimer::start(const char* name) {
+void StageTimer::start(const char* name, cudaStream_t on_stream) {
     if (!on) return;
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    cudaEventRecord(a, stream);
+    cudaEventRecord(a, on_stream ? on_stream : stream);
     begin.push_back(a);
     end.push_back(b);
     names.emplace_back(name);
 }
-void StageTimer::stop() {
+void StageTimer::stop(cudaStream_t on_stream) {
     if (!on || end.empty()) return;
-    cudaEventRecord(end.back(), stream);
+    cudaEventRecord(end.back(), on_stream ? on_stream : stream);
 }
 int StageTimer::read(double* ms, const char** nm, int cap) {
     const int n = (int)names.size();

@@ -117,8 +117,8 @@ struct StageTimer {
     std::vector<std::string> names;
     std::vector<cudaEvent_t> begin, end;
     void reset();
-    void start(const char* name);
-    void stop();
+    void start(const char* name, cudaStream_t on_stream = nullptr);  // nullptr: `stream`
+    void stop(cudaStream_t on_stream = nullptr);
     int read(double* ms, const char** nm, int cap);
     ~StageTimer();
 };
@@ -258,12 +258,13 @@ class Plan {
     //           copy of `in` is written to raw_sorted when given);
     //  addend:  per sorted output, added after mult before the scatter.
     //  herm:    real-input half split (HermArgs), nullptr = off
+    //  before_interp: the interpolation waits for this event (work on another stream)
     void apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, double2* out,
                       const double2* mult, const double2* addend, FftWork& wk, cudaStream_t st,
                       StageTimer* tm, const char* tag_spread, const char* tag_fft,
                       const char* tag_interp, uint64_t in_lo = 0, uint64_t in_hi = ~0ull,
                       uint64_t out_lo = 0, uint64_t out_hi = ~0ull,
-                      const HermArgs* herm = nullptr) const;
+                      const HermArgs* herm = nullptr, cudaEvent_t before_interp = nullptr) const;
     void apply_transpose(const double2* in, double2* out, FftWork& wk, cudaStream_t st,
                          StageTimer* tm, const double2* mult = nullptr, int conj_in = 0,
                          int conj_out = 0) const;
