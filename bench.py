@@ -218,7 +218,7 @@ def run_reference(args, w):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per_round * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": per_round * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
         "config": {"workload": w["desc"], "parallelism": f"host threads x{threads}"},
         "cpu_baseline": {
@@ -357,7 +357,7 @@ def run_b200(args, w):
         line = {
             "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded clouds/RHS of the BASELINE.json shape)",
             "config": {"workload": w["desc"], "N": n, "n_xi": info["n_xi"], "nnz": info["nnz"],
