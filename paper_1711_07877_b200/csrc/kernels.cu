@@ -868,6 +868,7 @@ __global__ void __launch_bounds__(256) k_interp_real(WindowPoly P, GridGeom g, u
 // from shared memory. The grid is read from L2 once per tile instead of once
 // per 8-output group.
 constexpr int kIT = 32;  // tile edge (Morton level 5)
+constexpr int kITW = 6;  // warps per CTA sharing one staged block
 
 template <int W, bool TRANS>
 struct ITile {
@@ -880,7 +881,7 @@ struct ITile {
     static constexpr int mod = TRANS ? 2 : 4;
     static constexpr int P = ext + ((mod - ext % 8) + 8) % 8;
     static constexpr int cells = (TRANS ? CE : RE) * P;
-    static constexpr size_t smem = (size_t)cells * sizeof(double2) + 2 * 4 * 32 * W * sizeof(double);
+    static constexpr size_t smem = (size_t)cells * sizeof(double2) + 2 * kITW * 32 * W * sizeof(double);
     __device__ static int at(int r, int c) { return TRANS ? c * P + r : r * P + c; }
 };
 
@@ -919,7 +920,7 @@ __device__ __forceinline__ void mma_group_s(const double2* __restrict__ S, int r
 }
 
 template <int W, bool TRANS>
-__global__ void __launch_bounds__(128) k_interp_tile(
+__global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
     WindowPoly P, GridGeom g, const uint32_t* __restrict__ tstart, uint32_t ntiles, int shift,
     uint64_t out_lo, uint64_t n, const double2* __restrict__ pos, const double2* __restrict__ phase,
     const double2* __restrict__ mult, const double* __restrict__ dxt, const double* __restrict__ dyt,
@@ -938,7 +939,7 @@ __global__ void __launch_bounds__(128) k_interp_tile(
     const int gid = lane >> 2, kq = lane & 3;
     double* wxs = sm_it + 2 * TT::cells + warp * 2 * 32 * W;
     double* wys = wxs + 32 * W;
-    __shared__ int s_jx[4][32], s_jy[4][32];
+    __shared__ int s_jx[kITW][32], s_jy[kITW][32];
     __shared__ double s_fx[TT::RE], s_fy[TT::CE];
     int* jxs = s_jx[warp];
     int* jys = s_jy[warp];
@@ -961,11 +962,11 @@ __global__ void __launch_bounds__(128) k_interp_tile(
         __syncthreads();
         // footprint -> shared memory, eight loads in flight per thread
         constexpr int kB = 8;
-        for (int ib = 0; ib < TT::cells; ib += kB * 128) {
+        for (int ib = 0; ib < TT::cells; ib += kB * kITW * 32) {
             double2 v[kB];
 #pragma unroll
             for (int u = 0; u < kB; ++u) {
-                const int i = ib + u * 128 + threadIdx.x;
+                const int i = ib + u * kITW * 32 + threadIdx.x;
                 const int q = i / TT::P, rr = i - q * TT::P;
                 const int r = TRANS ? rr : q, c = TRANS ? q : rr;
                 v[u] = make_double2(0.0, 0.0);
@@ -982,7 +983,7 @@ __global__ void __launch_bounds__(128) k_interp_tile(
             }
 #pragma unroll
             for (int u = 0; u < kB; ++u) {
-                const int i = ib + u * 128 + threadIdx.x;
+                const int i = ib + u * kITW * 32 + threadIdx.x;
                 if (i < TT::cells) {
                     const int q = i / TT::P, rr = i - q * TT::P;
                     const int r = TRANS ? rr : q, c = TRANS ? q : rr;
@@ -992,7 +993,7 @@ __global__ void __launch_bounds__(128) k_interp_tile(
             }
         }
         __syncthreads();
-        for (uint64_t base = a0 + 32 * warp; base < a1; base += 128) {
+        for (uint64_t base = a0 + 32 * warp; base < a1; base += 32 * kITW) {
             // this lane's output: position now, epilogue operands prefetched
             const uint64_t vmy = base + lane;
             const bool mine = vmy < a1;
@@ -1470,9 +1471,9 @@ struct InterpRun {
                 int dev = 0, sms = 148, per = 1;
                 cudaGetDevice(&dev);
                 cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 128, smem);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kITW * 32, smem);
                 const unsigned nb = (unsigned)std::min<uint64_t>(tiles->n, (uint64_t)sms * std::max(per, 1) * 8);
-                kern<<<nb, 128, smem, st>>>(P, g, tiles->start, tiles->n, tiles->shift, tiles->out_lo, n, pos,
+                kern<<<nb, kITW * 32, smem, st>>>(P, g, tiles->start, tiles->n, tiles->shift, tiles->out_lo, n, pos,
                                             phase, mult, dx, dy, grid, perm, addend, out, hh);
             };
             static size_t attr_t = 0, attr_n = 0;  // per W (this template)
