@@ -57,7 +57,8 @@ os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
 open(os.path.join(ROOT, "profiles", f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
 json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
 
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-units", "base"],
+                     capture_output=True, text=True).stdout
 r = list(csv.reader(raw.splitlines()))
 h = r[0]
 want = [("gpu__time_duration.sum", "duration (ms)"),
@@ -81,6 +82,10 @@ for row in r[2:]:
         v = d.get(k, "")
         try:
             f = float(v.replace(",", ""))
+            if k == "gpu__time_duration.sum":
+                f *= 1e-6  # ns -> ms
+            elif k.startswith("dram__bytes"):
+                f *= 1e-9  # B -> GB
             vals.append(f"{f:.3g}")
         except ValueError:
             vals.append(v)
