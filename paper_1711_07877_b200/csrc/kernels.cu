@@ -859,6 +859,84 @@ __global__ void __launch_bounds__(256) k_interp_real(WindowPoly P, GridGeom g, u
     out[perm ? perm[v] : v] = o;
 }
 
+// Staged variant of k_interp_real for Z-ordered outputs: one CTA per 32x32
+// block of stencil cells stages the block's (32 + W - 1)^2 footprint of the
+// real band (deconvolution folded in) in shared memory; each thread then
+// interpolates one output of the block from shared memory. The band is read
+// from L2 once per block instead of W^2 times per output.
+template <int W>
+__global__ void __launch_bounds__(128) k_interp_real_tile(
+    WindowPoly P, GridGeom g, const uint32_t* __restrict__ tstart, uint32_t ntiles, int shift,
+    uint64_t out_lo, uint64_t n, const double2* __restrict__ pos, const double2* __restrict__ phase,
+    const double* __restrict__ dxt, const double* __restrict__ dyt, const double* __restrict__ grid,
+    const uint32_t* __restrict__ perm, const double2* __restrict__ addend, double2* __restrict__ out) {
+    constexpr int E = 32 + W - 1;
+    constexpr int PE = E | 1;  // odd pitch (in doubles): rows start on different banks
+    __shared__ double S[E * PE];
+    __shared__ double s_fx[E], s_fy[E];
+    for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t t0 = tstart[tile], t1 = tstart[tile + 1];
+        const uint64_t a0 = t0 > out_lo ? t0 : out_lo, a1 = t1 < out_lo + n ? t1 : out_lo + n;
+        if (a0 >= a1) continue;
+        const double2 s0 = pos[a0 - out_lo];
+        const int X0 = (((int)ceil(s0.x - g.half) + shift) & ~31) - shift;
+        const int Y0 = (((int)ceil(s0.y - g.half) + shift) & ~31) - shift;
+        __syncthreads();  // previous block's readers are done
+        for (int i = threadIdx.x; i < 2 * E; i += blockDim.x) {
+            if (i < E)
+                s_fx[i] = dxt ? __ldg(dxt + wrap_near(X0 + i, g.n1)) : 1.0;
+            else
+                s_fy[i - E] = dyt ? __ldg(dyt + wrap_near(Y0 + i - E, g.n2)) : 1.0;
+        }
+        __syncthreads();
+        constexpr int kB = 8;
+        for (int ib = 0; ib < E * E; ib += kB * 128) {
+            double v[kB];
+#pragma unroll
+            for (int u = 0; u < kB; ++u) {
+                const int i = ib + u * 128 + threadIdx.x;
+                v[u] = 0.0;
+                if (i < E * E) {
+                    const int r = i / E, c = i - (i / E) * E;
+                    const int gr = wrap_near(X0 + r, g.n1), gc = wrap_near(Y0 + c, g.n2);
+                    // rows packed in pairs (component gr & 1 of complex row gr >> 1)
+                    v[u] = __ldg(grid + 2 * ((size_t)(gr >> 1) * g.n2 + gc) + (gr & 1));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kB; ++u) {
+                const int i = ib + u * 128 + threadIdx.x;
+                if (i < E * E) {
+                    const int r = i / E, c = i - (i / E) * E;
+                    S[r * PE + c] = v[u] * s_fx[r] * s_fy[c];
+                }
+            }
+        }
+        __syncthreads();
+        for (uint64_t va = a0 + threadIdx.x; va < a1; va += blockDim.x) {
+            const uint64_t v = va - out_lo;
+            const double2 sv = pos[v];
+            const double2 ph = phase[v];
+            const double2 ad = addend ? addend[v] : make_double2(0.0, 0.0);
+            const uint32_t dst = perm ? perm[v] : (uint32_t)v;
+            const int ix = (int)ceil(sv.x - g.half), iy = (int)ceil(sv.y - g.half);
+            double wx[W], wy[W];
+            kb_taps<W>((ix - sv.x) + g.half, P, wx);
+            kb_taps<W>((iy - sv.y) + g.half, P, wy);
+            const double* base = S + (ix - X0) * PE + (iy - Y0);
+            double ar = 0.0;
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                double rr = 0.0;
+#pragma unroll
+                for (int j = 0; j < W; ++j) rr = fma(base[i * PE + j], wy[j], rr);
+                ar = fma(rr, wx[i], ar);
+            }
+            out[dst] = make_double2(ar * ph.x + ad.x, ad.y);
+        }
+    }
+}
+
 // ---- tile-staged tensor-core interpolation -------------------------------
 // Outputs are Z-ordered by stencil cell, so the outputs whose stencil starts
 // in one 32 x 32 cell block are contiguous ("tiles", starts built at plan
@@ -1634,16 +1712,28 @@ template <int W>
 struct InterpRealRun {
     static void run(const WindowPoly& P, GridGeom g, uint64_t n, const double2* pos, const double2* phase,
                     const double* dx, const double* dy, const double* grid, const uint32_t* perm,
-                    const double2* addend, double2* out, cudaStream_t st) {
+                    const double2* addend, double2* out, cudaStream_t st, const InterpTiles* tiles) {
+        static const bool staged = !(getenv("SBD_INTERP") && getenv("SBD_INTERP")[0] == 's');
+        if (staged && tiles && tiles->n) {
+            int dev = 0, sms = 148, per = 1;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_interp_real_tile<W>, 128, 0);
+            const unsigned nb = (unsigned)std::min<uint64_t>(tiles->n, (uint64_t)sms * std::max(per, 1) * 8);
+            k_interp_real_tile<W><<<nb, 128, 0, st>>>(P, g, tiles->start, tiles->n, tiles->shift, tiles->out_lo,
+                                                       n, pos, phase, dx, dy, grid, perm, addend, out);
+            return;
+        }
         k_interp_real<W><<<blocks(n, 256), 256, 0, st>>>(P, g, n, pos, phase, dx, dy, grid, perm, addend, out);
     }
 };
 
 void launch_interp_real(int w, const WindowPoly& win, GridGeom g, uint64_t n, const double2* pos,
                         const double2* phase, const double* dx, const double* dy, const double* grid,
-                        const uint32_t* perm, const double2* addend, double2* out, cudaStream_t st) {
+                        const uint32_t* perm, const double2* addend, double2* out, cudaStream_t st,
+                        const InterpTiles* tiles) {
     if (!n) return;
-    dispatch_w<InterpRealRun>(w, win, g, n, pos, phase, dx, dy, grid, perm, addend, out, st);
+    dispatch_w<InterpRealRun>(w, win, g, n, pos, phase, dx, dy, grid, perm, addend, out, st, tiles);
     count_launch();
     ck(cudaGetLastError(), "k_interp_real");
 }

@@ -575,7 +575,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         if (tm) tm->start(tag_interp);
         const GridGeom gr{hB1, n2, 0.5 * w};
         launch_interp_real(w, win, gr, nout, s_p, post_p, hdx_band.p, dy.p,
-                           reinterpret_cast<const double*>(hD.p), perm_p, add_p, out_p, st);
+                           reinterpret_cast<const double*>(hD.p), perm_p, add_p, out_p, st, &otiles);
         if (tm) tm->stop();
         return;
     }

@@ -364,7 +364,8 @@ void launch_pack_rows(const double2* Y, int n1, int m0, int n2, int b1, int B1, 
 // out[perm?perm[k]:k] = Re(sum taps * dx dy * grid * phase[k]) + addend[k]
 void launch_interp_real(int w, const WindowPoly& win, GridGeom g, uint64_t n, const double2* pos,
                         const double2* phase, const double* dx, const double* dy, const double* grid,
-                        const uint32_t* perm, const double2* addend, double2* out, cudaStream_t st);
+                        const uint32_t* perm, const double2* addend, double2* out, cudaStream_t st,
+                        const struct InterpTiles* tiles = nullptr);
 // b[k] = in[perm[k]] phase[k] for k in [lo, hi) (zero elsewhere); raw[k] = in[perm[k]].
 // clear (optional): set to 0 when some in[k] has a nonzero imaginary part.
 void launch_gather_mul(const double2* in, const uint32_t* perm, const double2* phase, double2* b,
