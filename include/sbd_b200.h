@@ -117,6 +117,13 @@ int sbd_op_apply_adjoint_device(sbd_op* op, const double* d_u, double* d_q, int 
  * operator's internal xi order and already carries omega-hat and the
  * second NUFFT's prephase. Requires both NUFFTs on the gridded path. */
 int sbd_op_shard_bounds(const sbd_op* op, int side, int nshards, uint64_t* bounds);
+/* Number n of leading spectrum entries that sbd_op_forward_spectrum writes
+ * and sbd_op_backward_targets reads for this (device) f: n_xi, or, for a real
+ * f on an operator with real omega-hat and antipodally paired rings, the
+ * computed half of the pairs (the real-input half split; the all-reduce then
+ * moves n complex values). Runs one reduction over f and syncs `stream`; the
+ * decision is kept for the following forward/backward calls on this f. */
+int sbd_op_spectrum_length(sbd_op* op, const double* d_f, void* stream, uint64_t* n);
 int sbd_op_forward_spectrum(sbd_op* op, const double* d_f, uint64_t src_lo, uint64_t src_hi,
                             double* d_spec, void* stream);
 int sbd_op_backward_targets(sbd_op* op, const double* d_spec, const double* d_f, uint64_t tgt_lo,

@@ -68,6 +68,7 @@ _sig("sbd_op_set_profiling", _int, _vp, _int)
 _sig("sbd_op_shard_bounds", _int, _vp, _int, _int, ctypes.POINTER(_u64))
 _sig("sbd_op_forward_spectrum", _int, _vp, _vp, _u64, _u64, _vp, _vp)
 _sig("sbd_op_backward_targets", _int, _vp, _vp, _vp, _u64, _u64, _vp, _vp)
+_sig("sbd_op_spectrum_length", _int, _vp, _vp, _vp, ctypes.POINTER(_u64))
 _sig("sbd_op_stage_times", _int, _vp, _dp, ctypes.POINTER(ctypes.c_char_p), _int)
 _sig("sbd_op_stage_times_reset", _int, _vp)
 _sig("sbd_cloud_diameter", ctypes.c_double, _dp, _u64)
@@ -94,7 +95,7 @@ EXPORTED = [
     "sbd_nufft_create", "sbd_nufft_apply", "sbd_nufft_apply_transpose", "sbd_nufft_info",
     "sbd_nufft_destroy", "sbd_ndft_direct", "sbd_choose_parameters", "sbd_kernel_launch_count",
     "sbd_window_fit_error", "sbd_bessel", "sbd_op_shard_bounds", "sbd_op_forward_spectrum",
-    "sbd_op_backward_targets",
+    "sbd_op_backward_targets", "sbd_op_spectrum_length",
 ]
 
 

@@ -1327,6 +1327,15 @@ __global__ void k_mirror_points(const double2* __restrict__ t, uint64_t n, int n
     out[k] = make_double2(mirror_coord(p.x, n1, w), mirror_coord(p.y, n2, w));
 }
 
+// out[idx[k]] = conj(in[k])
+__global__ void k_conj_scatter(const double2* __restrict__ in, uint64_t n, const uint32_t* __restrict__ idx,
+                               double2* __restrict__ out) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double2 v = in[k];
+    out[idx[k]] = make_double2(v.x, -v.y);
+}
+
 // *flag |= (some im(x[k]) != 0)
 __global__ void k_any_imag(const double2* __restrict__ x, uint64_t n, int* __restrict__ flag) {
     int any = 0;
@@ -1809,6 +1818,13 @@ void launch_pack_rows(const double2* Y, int n1, int m0, int n2, int b1, int B1, 
     k_pack_rows<<<grid, 256, 0, st>>>(Y, n1, m0, n2, b1, B1, Z);
     count_launch();
     ck(cudaGetLastError(), "k_pack_rows");
+}
+
+void launch_conj_scatter(const double2* in, uint64_t n, const uint32_t* idx, double2* out, cudaStream_t st) {
+    if (!n) return;
+    k_conj_scatter<<<blocks(n, 256), 256, 0, st>>>(in, n, idx, out);
+    count_launch();
+    ck(cudaGetLastError(), "k_conj_scatter");
 }
 
 void launch_mirror_points(const double2* t, uint64_t n, int n1, int n2, int w, double2* out,

@@ -534,11 +534,43 @@ struct sbd_op {
     // Sharded forward half (multi-GPU): the kappa-weighted
     // spectrum of the sources in sorted range [lo, hi). Summing it over a
     // partition of the sources gives exactly the single-device spectrum.
+    // The real-input half split applies to the sharded halves too: for a real
+    // f only the computed half of the spectrum ([0, n_half) in this order) is
+    // formed, reduced and read. shard_real keeps the decision for the
+    // backward half (same f on every rank, so every rank decides alike).
+    int shard_real = 0;
+
+    uint64_t spectrum_length(const double2* f, cudaStream_t st) {
+        shard_real = herm_ok ? device_real(f, d.n_src(), st) : 0;
+        return shard_real ? n_half : d.n_xi();
+    }
+
+    HermArgs shard_herm(bool forward, cudaStream_t st) {
+        HermArgs h;
+        ck(cudaMemsetAsync(herm_flag.p, 1, sizeof(int), st), "half flag");
+        h.flag = herm_flag.p;
+        h.hfft = hfft_ok;
+        if (forward) {
+            h.n = n_half;
+            h.mult = kappa_h.p;
+            h.clear = true;
+            if (hfft_ok) h.hcols = fwd_in->hcols;  // conjugates are rebuilt after the reduction
+        } else {
+            h.n = ~0ull;
+            h.two_re = true;
+            h.out2 = hfft_ok ? spec_v.p : nullptr;
+        }
+        return h;
+    }
+
     void forward_spectrum(const double2* f, uint64_t lo, uint64_t hi, double2* spec_out,
                           cudaStream_t st) {
         if (!fused) throw Error(SBD_ERR_RUNTIME, "sharded apply needs both NUFFTs on the gridded path");
+        spectrum_length(f, st);
+        HermArgs h;
+        if (shard_real) h = shard_herm(true, st);
         fwd_in->apply_pruned(f, false, f_sorted.p, spec_out, kappa.p, nullptr, work, st, &tm,
-                             "spread_src", "fft_in", "interp_xi", lo, hi);
+                             "spread_src", "fft_in", "interp_xi", lo, hi, 0, ~0ull, shard_real ? &h : nullptr);
     }
 
     // Sharded backward half: q at the targets in sorted range [lo, hi)
@@ -552,8 +584,14 @@ struct sbd_op {
         if (tm.on) tm.start("spmv");
         launch_spmv_vec(hi - lo, ro_s.p + lo, cols_s.p, vals_s.p, f_sorted.p, qs.p + lo, st);
         if (tm.on) tm.stop();
+        HermArgs h;
+        if (shard_real) {
+            h = shard_herm(false, st);
+            // the mirror images' values: conjugates of the reduced spectrum
+            if (hfft_ok) launch_conj_scatter(spec_in, n_half, fwd_out->hv_of.p, spec_v.p, st);
+        }
         fwd_out->apply_pruned(spec_in, true, nullptr, q, nullptr, qs.p, work, st, &tm, "spread_xi",
-                              "fft_out", "interp_tgt", 0, ~0ull, lo, hi);
+                              "fft_out", "interp_tgt", 0, ~0ull, lo, hi, shard_real ? &h : nullptr);
     }
 
     // conv_operator.cpp:311-324
@@ -801,6 +839,15 @@ int sbd_op_shard_bounds(const sbd_op* op, int side, int nshards, uint64_t* bound
             throw Error(SBD_ERR_INVALID_ARGUMENT, "shard_bounds: bad argument");
         const uint64_t n = side == 0 ? op->d.n_src() : op->d.n_tgt();
         for (int i = 0; i <= nshards; ++i) bounds[i] = n * (uint64_t)i / (uint64_t)nshards;
+    });
+}
+
+int sbd_op_spectrum_length(sbd_op* op, const double* d_f, void* stream, uint64_t* n) {
+    return guarded([&] {
+        if (!op || !d_f || !n) throw Error(SBD_ERR_INVALID_ARGUMENT, "spectrum_length: null argument");
+        std::lock_guard<std::mutex> lk(op->mu);
+        DeviceGuard g(op->device);
+        *n = op->spectrum_length(reinterpret_cast<const double2*>(d_f), (cudaStream_t)stream);
     });
 }
 

@@ -352,6 +352,8 @@ void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int 
                            int n1, cudaStream_t st, int rin0 = 0, int conj_out = 0);
 void launch_mirror_points(const double2* t, uint64_t n, int n1, int n2, int w, double2* out,
                           cudaStream_t st);
+// out[idx[k]] = conj(in[k]) for k < n
+void launch_conj_scatter(const double2* in, uint64_t n, const uint32_t* idx, double2* out, cudaStream_t st);
 // *flag = 1 if some x[k] has a nonzero imaginary part, else 0
 void launch_any_imag(const double2* x, uint64_t n, int* flag, cudaStream_t st);
 // packed real rows -> untangled, transposed half band (see kernels.cu)

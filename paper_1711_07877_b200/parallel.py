@@ -6,7 +6,8 @@ over G ranks:
   1. sources sharded: rank r forms the omega-hat-weighted xi spectrum of its
      source shard only (sbd_op_forward_spectrum); the spectrum is linear in f,
   2. one all-reduce (sum) of the n_xi complex spectrum -- the only data-path
-     collective, because it is the path's only real exchange step,
+     collective, because it is the path's only real exchange step (for a
+     real f on a half-split operator only the computed half: n_xi / 2),
   3. targets and near-field rows sharded: rank r evaluates the second NUFFT at
      its target shard and adds its rows of D f (sbd_op_backward_targets); f is
      replicated (all-gathered) on every rank.
@@ -48,6 +49,15 @@ class DeviceBackend:
         check(lib.sbd_op_forward_spectrum(self.op._h, ctypes.c_void_p(f.data_ptr()), lo, hi,
                                           ctypes.c_void_p(spec.data_ptr()), ctypes.c_void_p(s)))
 
+    def spectrum_length(self, f):
+        """Leading spectrum entries formed / reduced / read for this f
+        (sbd_op_spectrum_length: the computed half for a real f)."""
+        n = ctypes.c_uint64()
+        s = self.torch.cuda.current_stream().cuda_stream
+        check(lib.sbd_op_spectrum_length(self.op._h, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(s),
+                                         ctypes.byref(n)))
+        return int(n.value)
+
     def backward_targets(self, spec, f, lo, hi, q):
         s = self.torch.cuda.current_stream().cuda_stream
         check(lib.sbd_op_backward_targets(self.op._h, ctypes.c_void_p(spec.data_ptr()),
@@ -78,7 +88,10 @@ class ShardedApply:
 
     def apply(self, f, q):
         r = self.rank
+        # a real f on a half-split operator only forms (and reduces) the
+        # computed half of the spectrum
+        n = self.b.spectrum_length(f) if hasattr(self.b, "spectrum_length") else self.b.n_xi
         self.b.forward_spectrum(f, self.src[r], self.src[r + 1], self.spec)
-        self.allreduce(self.spec)
+        self.allreduce(self.spec[: 2 * n])
         self.b.backward_targets(self.spec, f, self.tgt[r], self.tgt[r + 1], q)
         return self.target_range()
