@@ -511,6 +511,252 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
     }
 }
 
+// CTA-cooperative DMMA spread (default). One CTA owns a 32 x 32 cell region:
+// four 16 x 16 warp tiles with the accumulators of k_spread_mma in registers.
+// Against the per-warp kernel it
+//  * scans the 3 x 3 bins that can reach the region once per CTA, as one
+//    flattened candidate stream (the two point sets and all nine bins in
+//    128-candidate chunks), compacting the hits into a shared ring in block
+//    prefix order (deterministic: applies stay bitwise reproducible);
+//  * evaluates each queued point's taps once for all four warps (a point is
+//    staged (1 + (W-1)/32)^2 ~ 1.7 times instead of (1 + (W-1)/16)^2 ~ 2.6),
+//    two threads per point (x taps times the coefficient, y taps);
+//  * stores the taps in zero-padded rows (7 zeros, W taps, 7 zeros) and
+//    gives every (point, 8 x 8 sub-tile) list entry the row offsets of its
+//    fragments, so the MMA loop is a list load, two fragment loads and the
+//    DMMAs -- no bounds checks (lists are padded to a multiple of 4 with an
+//    all-zero point).
+constexpr int kSCB = 64;   // points per staged batch
+constexpr int kSCQ = 256;  // candidate ring (>= kSCB - 1 + 128)
+constexpr int kSCS = 18;   // scan segments: 2 point sets x 3 x 3 bins
+
+template <int W>
+struct SCta {
+    static constexpr int L = W + 14;     // padded tap row
+    static constexpr int NP = kSCB + 1;  // staged points + the zero point
+    static constexpr int LS = kSCB + 4;  // list stride (room for the padding)
+    static constexpr size_t smem = (size_t)NP * L * (sizeof(double2) + sizeof(double)) +
+                                   (size_t)kSCQ * 2 * sizeof(double2) + (size_t)16 * LS * 4 +
+                                   (size_t)2 * kSCB * 4;
+};
+
+template <int W, bool CPLX>
+__global__ void __launch_bounds__(128, 4) k_spread_cta(WindowPoly P, GridGeom g, TileGeom tg,
+                                                     const uint32_t* __restrict__ bin_start,
+                                                     const double2* __restrict__ bsorted,
+                                                     const double2* __restrict__ pos,
+                                                     double2* __restrict__ grid,
+                                                     const uint32_t* __restrict__ bin_start2,
+                                                     const int* __restrict__ herm, SpreadOut so) {
+    using S = SCta<W>;
+    constexpr int L = S::L;
+    extern __shared__ __align__(16) double smem_sc[];
+    double2* sA = reinterpret_cast<double2*>(smem_sc);  // [NP][L]: b * x taps
+    double2* sQt = sA + S::NP * L;                       // queued positions (16-byte aligned)
+    double2* sQb = sQt + kSCQ;                           // queued coefficients
+    double* sB = reinterpret_cast<double*>(sQb + kSCQ);  // [NP][L]: y taps
+    uint32_t* sL = reinterpret_cast<uint32_t*>(sB + S::NP * L);  // [4 warps][4 sub-tiles][LS]
+    int* sDX = reinterpret_cast<int*>(sL + 16 * S::LS);  // region-relative stencil starts
+    int* sDY = sDX + kSCB;
+    __shared__ int sCnt[4];
+    __shared__ uint32_t sSeg[kSCS], sPre[kSCS + 1];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int gid = lane >> 2, kq = lane & 3;
+    const int nrun = so.nby_run;
+    const int ncy = (nrun + 1) >> 1;
+    const int cx = blockIdx.x / ncy, cy = blockIdx.x - (blockIdx.x / ncy) * ncy;
+    const int X0 = tg.rlo + cx * 32, Y0 = tg.clo + cy * kTileC * 2;
+    // warp w owns the 8 x 8 sub-tiles (wr + 2p, wc + 2q), p, q in {0, 1}, of the
+    // region's 4 x 4: every stencil (>= 2 sub-tiles wide) feeds all four warps,
+    // so a batch of neighbouring points loads them evenly
+    const int wr = warp >> 1, wc = warp & 1;
+    const unsigned lt = (1u << lane) - 1u;
+
+    for (int i = tid; i < S::NP * L; i += 128) {
+        sA[i] = make_double2(0.0, 0.0);
+        sB[i] = 0.0;
+    }
+    // scan segments: (set, bin) -> [first sorted position, size), prefix sums
+    if (warp == 0) {
+        uint32_t k0 = 0, sz = 0;
+        const bool use2 = bin_start2 && !(herm && *herm);
+        if (lane < kSCS) {
+            const int set = lane / 9, qb = lane % 9;
+            const int cbx = 2 * cx - 1 + qb / 3, cby = 2 * cy - 1 + qb % 3;
+            if ((set == 0 || use2) && cbx >= 0 && cby >= 0 && cbx < tg.nbx && cby < tg.nby) {
+                const uint32_t* bs = set ? bin_start2 : bin_start;
+                const uint32_t b = (uint32_t)cbx * (uint32_t)tg.nby + (uint32_t)cby;
+                k0 = bs[b];
+                sz = bs[b + 1] - k0;
+            }
+            const bool second = set && so.pos2;
+            sSeg[lane] = k0 | (second ? 0x80000000u : 0u);
+        }
+        uint32_t inc = sz;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        if (lane < kSCS) sPre[lane + 1] = inc;
+        if (lane == 0) sPre[0] = 0;
+    }
+    double cr[2][2][2], ci[2][2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    __syncthreads();
+
+    uint32_t head = 0, tail = 0;  // ring positions (uniform across the CTA)
+    auto flush = [&](int n) {
+        // 1. taps: thread -> (point, axis)
+        {
+            const int p = tid & (kSCB - 1);
+            if (p < n) {
+                const double2 t = sQt[(head + p) & (kSCQ - 1)];
+                if (tid < kSCB) {
+                    const double2 b2 = sQb[(head + p) & (kSCQ - 1)];
+                    const int ix0 = (int)ceil(t.x - g.half);
+                    sDX[p] = ix0 - X0;
+                    double wt[W];
+                    kb_taps<W>((ix0 - t.x) + g.half, P, wt);
+                    double2* a = sA + p * L + 7;
+#pragma unroll
+                    for (int i = 0; i < W; ++i) a[i] = make_double2(b2.x * wt[i], b2.y * wt[i]);
+                } else {
+                    const int iy0 = (int)ceil(t.y - g.half);
+                    sDY[p] = iy0 - Y0;
+                    double* bb = sB + p * L + 7;
+                    kb_taps_each<W>((iy0 - t.y) + g.half, P, [&](int i, double v) { bb[i] = v; });
+                }
+            }
+        }
+        __syncthreads();
+        // 2. this warp's four sub-tile lists: fragment row offsets per entry
+        uint32_t* lst = sL + warp * 4 * S::LS;
+        int cnt[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int h = 0; h < kSCB / 32; ++h) {
+            const int p = h * 32 + lane;
+            int dx = 1 << 20, dy = 1 << 20;
+            if (p < n) {
+                dx = sDX[p] - 8 * wr;
+                dy = sDY[p] - 8 * wc;
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int i = 2 * (t >> 1), j = 2 * (t & 1);  // sub-tile origin: 8 (wr + i), 8 (wc + j)
+                const bool hit = dx < 8 * i + 8 && dx + W > 8 * i && dy < 8 * j + 8 && dy + W > 8 * j;
+                const unsigned m = __ballot_sync(0xffffffffu, hit);
+                if (hit)
+                    lst[t * S::LS + cnt[t] + __popc(m & lt)] =
+                        (uint32_t)(p * L + 8 * i - dx + 7) | ((uint32_t)(p * L + 8 * j - dy + 7) << 16);
+                cnt[t] += __popc(m);
+            }
+        }
+        constexpr uint32_t zero = (uint32_t)(kSCB * L) | ((uint32_t)(kSCB * L) << 16);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            if (lane < ((-cnt[t]) & 3)) lst[t * S::LS + cnt[t] + lane] = zero;
+            cnt[t] = (cnt[t] + 3) & ~3;
+        }
+        __syncwarp();
+        // 3. G[8 x 8] += A[8 x 4] B[4 x 8] per sub-tile, 4 listed points at a time
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int i = t >> 1, j = t & 1;
+            const uint32_t* lt4 = lst + t * S::LS + kq;
+            for (int grp = 0; grp < cnt[t]; grp += 4) {
+                const uint32_t e = lt4[grp];
+                const double2 a = sA[(e & 0xffffu) + gid];
+                const double bv = sB[(e >> 16) + gid];
+                dmma(cr[i][j][0], cr[i][j][1], a.x, bv);
+                if (CPLX) dmma(ci[i][j][0], ci[i][j][1], a.y, bv);
+            }
+        }
+        __syncthreads();  // staged rows, starts and lists are rewritten next batch
+    };
+
+    const uint32_t total = sPre[kSCS];
+    constexpr int kU = 4;  // candidate loads in flight per thread
+    int seg = 0;           // segment of the current sub-chunk's first candidate (uniform)
+    for (uint32_t s = 0; s < total; s += 128 * kU) {
+        double2 tt[kU], tb[kU];
+        uint32_t ent[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t i = s + u * 128 + tid;
+            ent[u] = 0xffffffffu;
+            tt[u] = make_double2(-1e30, -1e30);
+            while (seg < kSCS - 1 && s + u * 128 >= sPre[seg + 1]) ++seg;
+            if (i < total) {
+                int sg = seg;
+                while (i >= sPre[sg + 1]) ++sg;
+                const uint32_t e0 = sSeg[sg];
+                const uint32_t k = (e0 & 0x7fffffffu) + (i - sPre[sg]);
+                tt[u] = (e0 >> 31) ? so.pos2[k] : pos[k];
+                tb[u] = (e0 >> 31) ? so.b2[k] : bsorted[k];
+                ent[u] = k | (e0 & 0x80000000u);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            if (s + u * 128 >= total) break;  // uniform
+            const int ix0 = (int)ceil(tt[u].x - g.half), iy0 = (int)ceil(tt[u].y - g.half);
+            const bool take = ent[u] != 0xffffffffu && ix0 < X0 + 32 && ix0 + W > X0 && iy0 < Y0 + 32 &&
+                              iy0 + W > Y0;
+            const unsigned m = __ballot_sync(0xffffffffu, take);
+            if (lane == 0) sCnt[warp] = __popc(m);
+            __syncthreads();
+            int off = 0, tot = 0;
+#pragma unroll
+            for (int w2 = 0; w2 < 4; ++w2) {
+                const int c = sCnt[w2];
+                off += w2 < warp ? c : 0;
+                tot += c;
+            }
+            if (take) {
+                const uint32_t slot = (tail + off + __popc(m & lt)) & (kSCQ - 1);
+                sQt[slot] = tt[u];
+                sQb[slot] = tb[u];
+            }
+            tail += tot;
+            __syncthreads();
+            while (tail - head >= (uint32_t)kSCB) {
+                flush(kSCB);
+                head += kSCB;
+            }
+        }
+    }
+    if (tail != head) flush((int)(tail - head));
+
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int row = X0 + 8 * (wr + 2 * i) + gid;
+        if (row >= so.rend || 2 * cx + i >= tg.nbx) continue;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            if (2 * cy + j >= nrun) continue;
+            const int col = Y0 + 8 * (wc + 2 * j) + 2 * kq;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (col + h >= so.cend) continue;
+                const double re = cr[i][j][h], im = CPLX ? ci[i][j][h] : 0.0;
+                if (so.mode == 0)
+                    grid[(size_t)(row - so.r0) * so.pitch + (col + h - so.c0)] = make_double2(re, im);
+                else if (so.mode == 1)
+                    so.rgrid[(size_t)(row - so.r0) * so.pitch + (col + h - so.c0)] = re;
+                else if (so.mode == 3)
+                    so.rgrid[2 * ((size_t)((row - so.r0) >> 1) * so.pitch + (col + h - so.c0)) +
+                             ((row - so.r0) & 1)] = re;
+                else
+                    grid[(size_t)(col + h - so.c0) * so.pitch + (row - so.r0)] = make_double2(re, im);
+            }
+        }
+    }
+}
+
 // Interp (nufft.cpp:254-283): one thread per output; deconvolution folded
 // into the taps (exact: stencils never leave the band).
 template <int W, bool TRANS>
@@ -1501,12 +1747,19 @@ struct SpreadTilesRun {
             attr = true;
         }
         const int tiles = tg.nbx * tg.nby;
-        static int use_mma = -1;
+        static int use_mma = -1, use_cta = 0;
         if (use_mma < 0) {
             const char* e = getenv("SBD_SPREAD");
             use_mma = !(e && e[0] == 's');
+            use_cta = !(e && (e[0] == 's' || e[0] == 'w'));
             ck(cudaFuncSetAttribute(k_spread_mma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem()),
+               "smem attr");
+            ck(cudaFuncSetAttribute(k_spread_cta<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)SCta<W>::smem),
+               "smem attr");
+            ck(cudaFuncSetAttribute(k_spread_cta<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)SCta<W>::smem),
                "smem attr");
         }
         SpreadOut so;
@@ -1522,7 +1775,13 @@ struct SpreadTilesRun {
             so.nby_run = tg.nby;
         }
         if (out && !(use_mma && tg.tr == 16)) throw Error(3, "spread output modes need the DMMA spread");
-        if (use_mma && tg.tr == 16)
+        if (use_cta && tg.tr == 16) {
+            const int nblk = ((tg.nbx + 1) / 2) * ((so.nby_run + 1) / 2);
+            if (so.mode == 0 || so.mode == 2)
+                k_spread_cta<W, true><<<nblk, 128, SCta<W>::smem, st>>>(P, g, tg, bs, b, pos, grid, bs2, herm, so);
+            else
+                k_spread_cta<W, false><<<nblk, 128, SCta<W>::smem, st>>>(P, g, tg, bs, b, pos, grid, bs2, herm, so);
+        } else if (use_mma && tg.tr == 16)
             k_spread_mma<W><<<(tg.nbx * so.nby_run + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid, bs2,
                                                                                herm, so);
         else if (tg.tr == 8)
