@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
 //    fragments, so the MMA loop is a list load, two fragment loads and the
 //    DMMAs -- no bounds checks (lists are padded to a multiple of 4 with an
 //    all-zero point).
-constexpr int kSCB = 64;   // points per staged batch
+constexpr int kSCB = 48;   // points per staged batch (<= 64)
 constexpr int kSCQ = 256;  // candidate ring (>= kSCB - 1 + 128)
 constexpr int kSCS = 18;   // scan segments: 2 point sets x 3 x 3 bins
 
@@ -541,7 +541,7 @@ struct SCta {
 };
 
 template <int W, bool CPLX>
-__global__ void __launch_bounds__(128, 4) k_spread_cta(WindowPoly P, GridGeom g, TileGeom tg,
+__global__ void __launch_bounds__(128, 5) k_spread_cta(WindowPoly P, GridGeom g, TileGeom tg,
                                                      const uint32_t* __restrict__ bin_start,
                                                      const double2* __restrict__ bsorted,
                                                      const double2* __restrict__ pos,
@@ -556,7 +556,9 @@ __global__ void __launch_bounds__(128, 4) k_spread_cta(WindowPoly P, GridGeom g,
     double2* sQb = sQt + kSCQ;                           // queued coefficients
     double* sB = reinterpret_cast<double*>(sQb + kSCQ);  // [NP][L]: y taps
     uint32_t* sL = reinterpret_cast<uint32_t*>(sB + S::NP * L);  // [4 warps][4 sub-tiles][LS]
-    int* sDX = reinterpret_cast<int*>(sL + 16 * S::LS);  // region-relative stencil starts
+    // per staged point: fragment row base << 4 | mask of the region's 4
+    // sub-tile rows (x) / columns (y) its stencil covers
+    int* sDX = reinterpret_cast<int*>(sL + 16 * S::LS);
     int* sDY = sDX + kSCB;
     __shared__ int sCnt[4];
     __shared__ uint32_t sSeg[kSCS], sPre[kSCS + 1];
@@ -612,13 +614,15 @@ __global__ void __launch_bounds__(128, 4) k_spread_cta(WindowPoly P, GridGeom g,
     auto flush = [&](int n) {
         // 1. taps: thread -> (point, axis)
         {
-            const int p = tid & (kSCB - 1);
+            const int p = tid & 63;
             if (p < n) {
                 const double2 t = sQt[(head + p) & (kSCQ - 1)];
-                if (tid < kSCB) {
+                if (tid < 64) {
                     const double2 b2 = sQb[(head + p) & (kSCQ - 1)];
                     const int ix0 = (int)ceil(t.x - g.half);
-                    sDX[p] = ix0 - X0;
+                    const int dx = ix0 - X0;  // in [1 - W, 32)
+                    const int r0 = max(0, ((dx + 64) >> 3) - 8), r1 = min(3, ((dx + W - 1 + 64) >> 3) - 8);
+                    sDX[p] = ((p * L - dx + 7) << 4) | (((2 << r1) - 1) & ~((1 << r0) - 1));
                     double wt[W];
                     kb_taps<W>((ix0 - t.x) + g.half, P, wt);
                     double2* a = sA + p * L + 7;
@@ -626,7 +630,9 @@ __global__ void __launch_bounds__(128, 4) k_spread_cta(WindowPoly P, GridGeom g,
                     for (int i = 0; i < W; ++i) a[i] = make_double2(b2.x * wt[i], b2.y * wt[i]);
                 } else {
                     const int iy0 = (int)ceil(t.y - g.half);
-                    sDY[p] = iy0 - Y0;
+                    const int dy = iy0 - Y0;
+                    const int c0 = max(0, ((dy + 64) >> 3) - 8), c1 = min(3, ((dy + W - 1 + 64) >> 3) - 8);
+                    sDY[p] = ((p * L - dy + 7) << 4) | (((2 << c1) - 1) & ~((1 << c0) - 1));
                     double* bb = sB + p * L + 7;
                     kb_taps_each<W>((iy0 - t.y) + g.half, P, [&](int i, double v) { bb[i] = v; });
                 }
@@ -637,21 +643,23 @@ __global__ void __launch_bounds__(128, 4) k_spread_cta(WindowPoly P, GridGeom g,
         uint32_t* lst = sL + warp * 4 * S::LS;
         int cnt[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int h = 0; h < kSCB / 32; ++h) {
+        for (int h = 0; h < (kSCB + 31) / 32; ++h) {
             const int p = h * 32 + lane;
-            int dx = 1 << 20, dy = 1 << 20;
+            int ex = 0, ey = 0;
             if (p < n) {
-                dx = sDX[p] - 8 * wr;
-                dy = sDY[p] - 8 * wc;
+                ex = sDX[p] >> wr;  // row mask bit 0 = sub-tile row wr
+                ey = sDY[p] >> wc;
+                ex = (ex & 0xf) | ((sDX[p] >> 4) + 8 * wr) << 4;
+                ey = (ey & 0xf) | ((sDY[p] >> 4) + 8 * wc) << 4;
             }
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
-                const int i = 2 * (t >> 1), j = 2 * (t & 1);  // sub-tile origin: 8 (wr + i), 8 (wc + j)
-                const bool hit = dx < 8 * i + 8 && dx + W > 8 * i && dy < 8 * j + 8 && dy + W > 8 * j;
+                const int i = 2 * (t >> 1), j = 2 * (t & 1);  // sub-tile (wr + i, wc + j)
+                const bool hit = (ex >> i) & (ey >> j) & 1;
                 const unsigned m = __ballot_sync(0xffffffffu, hit);
                 if (hit)
                     lst[t * S::LS + cnt[t] + __popc(m & lt)] =
-                        (uint32_t)(p * L + 8 * i - dx + 7) | ((uint32_t)(p * L + 8 * j - dy + 7) << 16);
+                        (uint32_t)((ex >> 4) + 8 * i) | ((uint32_t)((ey >> 4) + 8 * j) << 16);
                 cnt[t] += __popc(m);
             }
         }
@@ -679,7 +687,7 @@ __global__ void __launch_bounds__(128, 4) k_spread_cta(WindowPoly P, GridGeom g,
     };
 
     const uint32_t total = sPre[kSCS];
-    constexpr int kU = 4;  // candidate loads in flight per thread
+    constexpr int kU = 2;  // candidate loads in flight per thread
     int seg = 0;           // segment of the current sub-chunk's first candidate (uniform)
     for (uint32_t s = 0; s < total; s += 128 * kU) {
         double2 tt[kU], tb[kU];
