@@ -343,6 +343,17 @@ __global__ void __launch_bounds__(128, TR == 16 ? 4 : 5) k_spread_tiles(WindowPo
     }
 }
 
+// coefficient of mirror image k (second point set): conj of its tag-0
+// partner's coefficient when the partner map is given, else stored
+__device__ __forceinline__ double2 mirror_coef(const SpreadOut& so, const double2* __restrict__ b,
+                                               uint32_t k) {
+    if (so.src2) {
+        const double2 v = b[so.src2[k]];
+        return make_double2(v.x, -v.y);
+    }
+    return so.b2[k];
+}
+
 // fp64 tensor-core MMA: D(8x8) = A(8x4) B(4x8) + C (mma.sync m8n8k4 f64; SASS
 // DMMA.8x8x4). Fragments: a = A[lane/4][lane%4], b = B[lane%4][lane/4],
 // c = {C[lane/4][2(lane%4)], C[lane/4][2(lane%4)+1]}.
@@ -403,7 +414,7 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
             const uint32_t k = e & 0x7fffffffu;  // bit 31: second point set
             const double2 t = (e >> 31) ? so.pos2[k] : pos[k];
             const int ix0 = (int)ceil(t.x - g.half), iy0 = (int)ceil(t.y - g.half);
-            const double2 b2 = (e >> 31) ? so.b2[k] : bsorted[k];
+            const double2 b2 = (e >> 31) ? mirror_coef(so, bsorted, k) : bsorted[k];
             dx = ix0 - X0;
             dy = iy0 - Y0;
             double2* bw = s_bwx + lane * W;
@@ -704,7 +715,7 @@ __global__ void __launch_bounds__(128, 5) k_spread_cta(WindowPoly P, GridGeom g,
                 const uint32_t e0 = sSeg[sg];
                 const uint32_t k = (e0 & 0x7fffffffu) + (i - sPre[sg]);
                 tt[u] = (e0 >> 31) ? so.pos2[k] : pos[k];
-                tb[u] = (e0 >> 31) ? so.b2[k] : bsorted[k];
+                tb[u] = (e0 >> 31) ? mirror_coef(so, bsorted, k) : bsorted[k];
                 ent[u] = k | (e0 & 0x80000000u);
             }
         }
@@ -1272,7 +1283,6 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
     double* wxs = sm_it + 2 * TT::cells + warp * 2 * 32 * W;
     double* wys = wxs + 32 * W;
     __shared__ int s_jx[kITW][32], s_jy[kITW][32];
-    __shared__ double s_fx[TT::RE], s_fy[TT::CE];
     int* jxs = s_jx[warp];
     int* jys = s_jy[warp];
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -1284,24 +1294,19 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
         const int X0 = (((int)ceil(s0.x - g.half) + shift) & ~(kIT - 1)) - shift;
         const int Y0 = (((int)ceil(s0.y - g.half) + shift) & ~(kIT - 1)) - shift;
         __syncthreads();  // previous tile's readers are done
-        // deconvolution factors of the tile's rows and columns
-        for (int i = threadIdx.x; i < TT::RE + TT::CE; i += blockDim.x) {
-            if (i < TT::RE)
-                s_fx[i] = (i < TT::E && dxt) ? __ldg(dxt + wrap_near(X0 + i, g.n1)) : 1.0;
-            else
-                s_fy[i - TT::RE] = (i - TT::RE < TT::E && dyt) ? __ldg(dyt + wrap_near(Y0 + i - TT::RE, g.n2)) : 1.0;
-        }
-        __syncthreads();
-        // footprint -> shared memory, eight loads in flight per thread
+        // footprint -> shared memory times the deconvolution factors of its
+        // row and column (L1-resident tables), eight loads in flight per thread
         constexpr int kB = 8;
         for (int ib = 0; ib < TT::cells; ib += kB * kITW * 32) {
             double2 v[kB];
+            double f[kB];
 #pragma unroll
             for (int u = 0; u < kB; ++u) {
                 const int i = ib + u * kITW * 32 + threadIdx.x;
                 const int q = i / TT::P, rr = i - q * TT::P;
                 const int r = TRANS ? rr : q, c = TRANS ? q : rr;
                 v[u] = make_double2(0.0, 0.0);
+                f[u] = 0.0;
                 if (i < TT::cells && r < TT::E && c < TT::E) {
                     const int gr = wrap_near(X0 + r, g.n1), gc = wrap_near(Y0 + c, g.n2);
                     if (TRANS && hcols && gc >= hcols) {
@@ -1311,17 +1316,13 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
                     } else {
                         v[u] = __ldg(TRANS ? grid + (size_t)gc * g.n1 + gr : grid + (size_t)gr * g.n2 + gc);
                     }
+                    f[u] = (dxt ? __ldg(dxt + gr) : 1.0) * (dyt ? __ldg(dyt + gc) : 1.0);
                 }
             }
 #pragma unroll
             for (int u = 0; u < kB; ++u) {
                 const int i = ib + u * kITW * 32 + threadIdx.x;
-                if (i < TT::cells) {
-                    const int q = i / TT::P, rr = i - q * TT::P;
-                    const int r = TRANS ? rr : q, c = TRANS ? q : rr;
-                    const double f = (r < TT::RE ? s_fx[r] : 1.0) * (c < TT::CE ? s_fy[c] : 1.0);
-                    S[i] = make_double2(v[u].x * f, v[u].y * f);
-                }
+                if (i < TT::cells) S[i] = make_double2(v[u].x * f[u], v[u].y * f[u]);
             }
         }
         __syncthreads();
@@ -1388,13 +1389,15 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
                     SBD_MMA_CASE(2, 3) SBD_MMA_CASE(2, 4) SBD_MMA_CASE(2, 5) SBD_MMA_CASE(2, 6)
                     SBD_MMA_CASE(3, 3) SBD_MMA_CASE(3, 4) SBD_MMA_CASE(3, 5) SBD_MMA_CASE(3, 6)
                     default: {
-                        // wide group: lanes 0..7 each interpolate one output from the tile
+                        // wide group: four lanes per output (rows part, part + 4, ...),
+                        // reduced over the four, from the staged tile
                         double ar = 0.0, ai = 0.0;
-                        if (lane < 8 && jxs[o8 + lane] != (1 << 28)) {
-                            const int node = o8 + lane;
+                        const int node = o8 + (lane >> 2), part = lane & 3;
+                        if (jxs[node] != (1 << 28)) {
                             const int jx0 = jxs[node], jy0 = jys[node];
-                            for (int i = 0; i < W; ++i) {
+                            for (int i = part; i < W; i += 4) {
                                 double rr = 0.0, ri = 0.0;
+#pragma unroll
                                 for (int j = 0; j < W; ++j) {
                                     const double2 gv = S[TT::at(jx0 + i, jy0 + j)];
                                     const double wyj = wys[node * W + j];
@@ -1405,9 +1408,13 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
                                 ai = fma(ri, wxs[node * W + i], ai);
                             }
                         }
-                        // lanes 0..7 hold outputs o8 + lane: hand them to the owners
-                        ar = __shfl_sync(0xffffffffu, ar, lane & 7);
-                        ai = __shfl_sync(0xffffffffu, ai, lane & 7);
+                        ar += __shfl_xor_sync(0xffffffffu, ar, 1);
+                        ai += __shfl_xor_sync(0xffffffffu, ai, 1);
+                        ar += __shfl_xor_sync(0xffffffffu, ar, 2);
+                        ai += __shfl_xor_sync(0xffffffffu, ai, 2);
+                        // lanes 4k hold output o8 + k: hand them to the owners
+                        ar = __shfl_sync(0xffffffffu, ar, (lane & 7) << 2);
+                        ai = __shfl_sync(0xffffffffu, ai, (lane & 7) << 2);
                         if ((lane >> 3) == grp) {
                             accr = ar;
                             acci = ai;

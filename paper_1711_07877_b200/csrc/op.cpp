@@ -204,8 +204,6 @@ struct sbd_op {
     // the host to know f is real (host buffers are scanned, device buffers
     // checked with one reduction + sync)
     bool hfft_ok = false;
-    DevBuf<double2> spec_v;        // conj spectrum at the mirror images (fwd_out order)
-    DevBuf<uint32_t> perm_v;       // fwd_in tag-0 output position -> mirror-image position
     DevBuf<int> imag_flag;
     StageTimer tm;
     std::mutex mu;
@@ -283,20 +281,18 @@ struct sbd_op {
             fwd_in->hrole = 0;
             return;
         }
+        // the spread reads the mirror images' values as conjugates of their
+        // partners (Plan::hv_src); check that the computed outputs of fwd_in are
+        // exactly the tag-0 points of fwd_out
         const uint64_t nx = d.n_xi(), n0 = n_half;
-        std::vector<uint32_t> ps(nx), of(n0), pv(n0);
+        std::vector<uint32_t> ps(nx);
         if (fwd_in->perm_s.n)
             ck(cudaMemcpyAsync(ps.data(), fwd_in->perm_s.p, nx * 4, cudaMemcpyDeviceToHost, stream), "perm");
         else
             for (uint64_t i = 0; i < nx; ++i) ps[i] = (uint32_t)i;
-        ck(cudaMemcpyAsync(of.data(), fwd_out->hv_of.p, n0 * 4, cudaMemcpyDeviceToHost, stream), "perm");
         ck(cudaStreamSynchronize(stream), "perm");
-        for (uint64_t v = 0; v < n0; ++v) {
+        for (uint64_t v = 0; v < n0; ++v)
             if (ps[v] >= n0) return;  // tag-0 outputs must map to tag-0 nodes
-            pv[v] = of[ps[v]];
-        }
-        perm_v.upload(pv.data(), n0, stream);
-        spec_v.alloc(n0);
         imag_flag.alloc(1);
         ck(cudaStreamSynchronize(stream), "hfft");
         hfft_ok = true;
@@ -488,8 +484,7 @@ struct sbd_op {
                 if (hfft_now) {
                     hin.hfft = hout.hfft = true;
                     hin.hcols = fwd_in->hcols;
-                    hin.out2 = hout.out2 = spec_v.p;
-                    hin.perm2 = perm_v.p;
+
                 }
             }
             // spectrum_b = NUFFT-(f) * w * pre_out, with f_sorted kept for the CSR pass
@@ -558,7 +553,7 @@ struct sbd_op {
         } else {
             h.n = ~0ull;
             h.two_re = true;
-            h.out2 = hfft_ok ? spec_v.p : nullptr;
+
         }
         return h;
     }
@@ -587,8 +582,6 @@ struct sbd_op {
         HermArgs h;
         if (shard_real) {
             h = shard_herm(false, st);
-            // the mirror images' values: conjugates of the reduced spectrum
-            if (hfft_ok) launch_conj_scatter(spec_in, n_half, fwd_out->hv_of.p, spec_v.p, st);
         }
         fwd_out->apply_pruned(spec_in, true, nullptr, q, nullptr, qs.p, work, st, &tm, "spread_xi",
                               "fft_out", "interp_tgt", 0, ~0ull, lo, hi, shard_real ? &h : nullptr);

@@ -329,6 +329,7 @@ bool Plan::enable_hfft(int role, cudaStream_t st) {
         ck(cudaStreamSynchronize(st), "mirror map");
         for (uint64_t i = 0; i < n0_pts; ++i) inv[hs[i]] = (uint32_t)i;
         hv_of.upload(inv.data(), n0_pts, st);
+        hv_src = std::move(src);
         // columns m2 in [clo, n2/2] of the Hermitian grid, as full-length columns
         hnm = n2 / 2 - clo + 1;
         hnby = std::min(tg.nby, (n2 / 2 + 1 - clo + kTileC - 1) / kTileC);
@@ -554,7 +555,9 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         so.cend = clo + hnm;
         so.nby_run = hnby;
         so.pos2 = hv_t.p;
-        so.b2 = herm->out2;
+        // the spread reads each mirror image's value as the conjugate of its
+        // partner's (only images near the m2 = n2/2 line are ever read)
+        so.src2 = hv_src.p;
         launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, hA.p, st, hv_bins.p, nullptr, &so);
         if (tm) tm->stop();
         if (tm) tm->start(tag_fft);

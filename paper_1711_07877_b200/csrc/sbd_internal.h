@@ -240,6 +240,7 @@ class Plan {
     int hnm = 0, hnby = 0, hb1 = 0, hB1 = 0, hcols = 0;
     DevBuf<double2> hv_t;             // role 2: mirrored tag-0 points, sorted by tile
     DevBuf<uint32_t> hv_bins, hv_of;  // their bins; tag-0 sorted position -> mirrored position
+    DevBuf<uint32_t> hv_src;          // mirrored position -> tag-0 sorted position
     DevBuf<double> hdx_band;          // role 2: deconvolution of the band rows
     bool enable_hfft(int role, cudaStream_t st);
 
@@ -312,6 +313,7 @@ struct SpreadOut {
     int nby_run = 0;
     const double2* pos2 = nullptr;
     const double2* b2 = nullptr;
+    const uint32_t* src2 = nullptr;  // mirror image -> tag-0 partner (b2 = conj(b[src2]))
 };
 
 // ---------------------------------------------------------------- kernels
