@@ -47,7 +47,7 @@ for i, e in enumerate(one):
     wr = e.get("dram__bytes_write.sum", 0)
     nm = e["name"].split("(")[0][:70]
     lines.append(f"| {i} | `{nm}` | {t * unit_scale:.1f} | {100 * t / total:.1f}% | {rd / 1e6:.1f} | {wr / 1e6:.1f} |")
-    if any(k in e["name"] for k in ("k_spread_mma", "k_interp", "k_spmv_vec")):
+    if any(k in e["name"] for k in ("k_spread_mma", "k_spread_cta", "k_interp", "k_spmv_vec")):
         try:
             traffic[next(stage_iter)] = rd + wr
         except StopIteration:
@@ -72,7 +72,7 @@ want = [("gpu__time_duration.sum", "duration (ms)"),
         ("launch__registers_per_thread", "regs/thread"),
         ("smsp__inst_executed.sum", "warp instr")]
 out = [f"# ncu --set full, hot kernels of one apply ({tag})", "",
-       "`ncu --set full --clock-control none --import-source on -k regex:\"k_interp|k_spread_mma|k_spmv_vec\"` "
+       "`ncu --set full --clock-control none -k regex:\"k_interp|k_spread_cta|k_spmv_vec\"` "
        "on `tools/prof_apply.py` (config 4), second apply.", "",
        "| kernel | " + " | ".join(w[1] for w in want) + " |", "|---" * (len(want) + 1) + "|"]
 for row in r[2:]:
