@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
 //    fragments, so the MMA loop is a list load, two fragment loads and the
 //    DMMAs -- no bounds checks (lists are padded to a multiple of 4 with an
 //    all-zero point).
-constexpr int kSCB = 48;   // points per staged batch (<= 64)
+constexpr int kSCB = 32;   // points per staged batch (<= 64; 32 keeps 7 CTAs per SM resident)
 constexpr int kSCQ = 256;  // candidate ring (>= kSCB - 1 + 128)
 constexpr int kSCS = 18;   // scan segments: 2 point sets x 3 x 3 bins
 
@@ -552,7 +552,7 @@ struct SCta {
 };
 
 template <int W, bool CPLX>
-__global__ void __launch_bounds__(128, 5) k_spread_cta(WindowPoly P, GridGeom g, TileGeom tg,
+__global__ void __launch_bounds__(128, 7) k_spread_cta(WindowPoly P, GridGeom g, TileGeom tg,
                                                      const uint32_t* __restrict__ bin_start,
                                                      const double2* __restrict__ bsorted,
                                                      const double2* __restrict__ pos,

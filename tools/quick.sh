@@ -6,5 +6,5 @@ if [ "$1" != "notest" ]; then
 fi
 for v in ${SPREADS:-c}; do
   SBD_SPREAD=$v timeout 400 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$v.log 2>&1; echo bench=$?
-  tail -1 gpurun_out/bench_$v.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', round(d['ms_per_step'],3), d['roofline']['stages_ms'])"
+  tail -1 gpurun_out/bench_$v.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['roofline']['stages_ms'])"
 done
