@@ -114,6 +114,32 @@ __global__ void k_tile_keys(const double2* __restrict__ pos, uint64_t n, double 
               (tag && tag[k] ? 0x80000000u : 0u);
 }
 
+// Region lists of the CTA spread (k_spread_cta<.., LIST>): each point emits
+// the 32 x 32 spread regions its stencil overlaps (at most 2 x 2 for W <= 32)
+// as (region, entry) pairs, region count for unused slots; a stable sort by
+// region then keeps the points of a region in sorted-point order.
+__global__ void k_region_pairs(const double2* __restrict__ pos, uint64_t n, double half, int w,
+                               TileGeom tg, int ncx, int ncy, uint32_t base, uint32_t tagbit,
+                               uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double2 p = pos[k];
+    const int rx = (int)ceil(p.x - half) - tg.rlo, ry = (int)ceil(p.y - half) - tg.clo;
+    const int x0 = rx >> 5, x1 = (rx + w - 1) >> 5, y0 = ry >> 5, y1 = (ry + w - 1) >> 5;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int cx = x0 + (q >> 1), cy = y0 + (q & 1);
+        const bool ok = cx <= x1 && cy <= y1 && cx >= 0 && cy >= 0 && cx < ncx && cy < ncy;
+        keys[4 * k + q] = ok ? (uint32_t)cx * (uint32_t)ncy + (uint32_t)cy : (uint32_t)ncx * (uint32_t)ncy;
+        vals[4 * k + q] = ((uint32_t)k + base) | tagbit;
+    }
+}
+
+__global__ void k_shift_keys(uint32_t* __restrict__ keys, uint64_t n) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i < n) keys[i] <<= 5;
+}
+
 // start[b] = first sorted position with key >= b, for b in [0, nbins]
 __global__ void k_bin_bounds(const uint32_t* __restrict__ key, uint64_t n, uint32_t nbins,
                              uint32_t* __restrict__ start, uint32_t base, uint32_t mask) {
@@ -551,7 +577,7 @@ struct SCta {
                                    (size_t)2 * kSCB * 4;
 };
 
-template <int W, bool CPLX>
+template <int W, bool CPLX, bool LIST>
 __global__ void __launch_bounds__(128, 7) k_spread_cta(WindowPoly P, GridGeom g, TileGeom tg,
                                                      const uint32_t* __restrict__ bin_start,
                                                      const double2* __restrict__ bsorted,
@@ -590,7 +616,7 @@ __global__ void __launch_bounds__(128, 7) k_spread_cta(WindowPoly P, GridGeom g,
         sB[i] = 0.0;
     }
     // scan segments: (set, bin) -> [first sorted position, size), prefix sums
-    if (warp == 0) {
+    if (!LIST && warp == 0) {
         uint32_t k0 = 0, sz = 0;
         const bool use2 = bin_start2 && !(herm && *herm);
         if (lane < kSCS) {
@@ -622,14 +648,13 @@ __global__ void __launch_bounds__(128, 7) k_spread_cta(WindowPoly P, GridGeom g,
     __syncthreads();
 
     uint32_t head = 0, tail = 0;  // ring positions (uniform across the CTA)
-    auto flush = [&](int n) {
+    // t, b2: position and coefficient of point (tid & 63) of the batch
+    auto flush = [&](int n, double2 t, double2 b2) {
         // 1. taps: thread -> (point, axis)
         {
             const int p = tid & 63;
             if (p < n) {
-                const double2 t = sQt[(head + p) & (kSCQ - 1)];
                 if (tid < 64) {
-                    const double2 b2 = sQb[(head + p) & (kSCQ - 1)];
                     const int ix0 = (int)ceil(t.x - g.half);
                     const int dx = ix0 - X0;  // in [1 - W, 32)
                     const int r0 = max(0, ((dx + 64) >> 3) - 8), r1 = min(3, ((dx + W - 1 + 64) >> 3) - 8);
@@ -697,58 +722,100 @@ __global__ void __launch_bounds__(128, 7) k_spread_cta(WindowPoly P, GridGeom g,
         __syncthreads();  // staged rows, starts and lists are rewritten next batch
     };
 
-    const uint32_t total = sPre[kSCS];
-    constexpr int kU = 2;  // candidate loads in flight per thread
-    int seg = 0;           // segment of the current sub-chunk's first candidate (uniform)
-    for (uint32_t s = 0; s < total; s += 128 * kU) {
-        double2 tt[kU], tb[kU];
-        uint32_t ent[kU];
+    if (LIST) {
+        // plan-time region lists (SpreadLists): the batches are the region's
+        // entries in order, positions and coefficients loaded one batch ahead
+        const uint32_t region = (uint32_t)cx * (uint32_t)so.lists.ncy + (uint32_t)cy;
+        const uint32_t s1 = so.lists.s1[region], e1 = so.lists.s1[region + 1];
+        uint32_t s2 = 0, e2 = 0;
+        if (so.lists.s2 && !(herm && *herm)) {
+            s2 = so.lists.s2[region];
+            e2 = so.lists.s2[region + 1];
+        }
+        const uint32_t n1 = e1 - s1, nall = n1 + (e2 - s2);
+        const int p = tid & 63;
+        // two-stage prefetch: list entries two batches ahead, positions and
+        // coefficients one batch ahead
+        auto entry = [&](uint32_t q0) -> uint32_t {
+            const uint32_t q = q0 + p;
+            if (p >= kSCB || q >= nall) return 0xffffffffu;
+            return q < n1 ? so.lists.e1[s1 + q] : so.lists.e2[s2 + (q - n1)];
+        };
+        auto fetch = [&](uint32_t e, double2& t, double2& b2) {
+            if (e != 0xffffffffu) {
+                const uint32_t k = e & 0x7fffffffu;
+                t = (e >> 31) ? so.pos2[k] : pos[k];
+                if (tid < 64) b2 = (e >> 31) ? mirror_coef(so, bsorted, k) : bsorted[k];
+            }
+        };
+        double2 tn = make_double2(0.0, 0.0), bn = tn;
+        uint32_t en = entry(kSCB);
+        fetch(entry(0), tn, bn);
+        for (uint32_t q0 = 0; q0 < nall; q0 += kSCB) {
+            const double2 t = tn, b2 = bn;
+            fetch(en, tn, bn);
+            en = entry(q0 + 2 * kSCB);
+            flush((int)min((uint32_t)kSCB, nall - q0), t, b2);
+        }
+    } else {
+        const uint32_t total = sPre[kSCS];
+        constexpr int kU = 2;  // candidate loads in flight per thread
+        int seg = 0;           // segment of the current sub-chunk's first candidate (uniform)
+        for (uint32_t s = 0; s < total; s += 128 * kU) {
+            double2 tt[kU], tb[kU];
+            uint32_t ent[kU];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const uint32_t i = s + u * 128 + tid;
-            ent[u] = 0xffffffffu;
-            tt[u] = make_double2(-1e30, -1e30);
-            while (seg < kSCS - 1 && s + u * 128 >= sPre[seg + 1]) ++seg;
-            if (i < total) {
-                int sg = seg;
-                while (i >= sPre[sg + 1]) ++sg;
-                const uint32_t e0 = sSeg[sg];
-                const uint32_t k = (e0 & 0x7fffffffu) + (i - sPre[sg]);
-                tt[u] = (e0 >> 31) ? so.pos2[k] : pos[k];
-                tb[u] = (e0 >> 31) ? mirror_coef(so, bsorted, k) : bsorted[k];
-                ent[u] = k | (e0 & 0x80000000u);
+            for (int u = 0; u < kU; ++u) {
+                const uint32_t i = s + u * 128 + tid;
+                ent[u] = 0xffffffffu;
+                tt[u] = make_double2(-1e30, -1e30);
+                while (seg < kSCS - 1 && s + u * 128 >= sPre[seg + 1]) ++seg;
+                if (i < total) {
+                    int sg = seg;
+                    while (i >= sPre[sg + 1]) ++sg;
+                    const uint32_t e0 = sSeg[sg];
+                    const uint32_t k = (e0 & 0x7fffffffu) + (i - sPre[sg]);
+                    tt[u] = (e0 >> 31) ? so.pos2[k] : pos[k];
+                    tb[u] = (e0 >> 31) ? mirror_coef(so, bsorted, k) : bsorted[k];
+                    ent[u] = k | (e0 & 0x80000000u);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                if (s + u * 128 >= total) break;  // uniform
+                const int ix0 = (int)ceil(tt[u].x - g.half), iy0 = (int)ceil(tt[u].y - g.half);
+                const bool take = ent[u] != 0xffffffffu && ix0 < X0 + 32 && ix0 + W > X0 && iy0 < Y0 + 32 &&
+                                  iy0 + W > Y0;
+                const unsigned m = __ballot_sync(0xffffffffu, take);
+                if (lane == 0) sCnt[warp] = __popc(m);
+                __syncthreads();
+                int off = 0, tot = 0;
+#pragma unroll
+                for (int w2 = 0; w2 < 4; ++w2) {
+                    const int c = sCnt[w2];
+                    off += w2 < warp ? c : 0;
+                    tot += c;
+                }
+                if (take) {
+                    const uint32_t slot = (tail + off + __popc(m & lt)) & (kSCQ - 1);
+                    sQt[slot] = tt[u];
+                    sQb[slot] = tb[u];
+                }
+                tail += tot;
+                __syncthreads();
+                while (tail - head >= (uint32_t)kSCB) {
+                    const int p = tid & 63;
+                    flush(kSCB, sQt[(head + p) & (kSCQ - 1)], sQb[(head + p) & (kSCQ - 1)]);
+                    head += kSCB;
+                }
             }
         }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            if (s + u * 128 >= total) break;  // uniform
-            const int ix0 = (int)ceil(tt[u].x - g.half), iy0 = (int)ceil(tt[u].y - g.half);
-            const bool take = ent[u] != 0xffffffffu && ix0 < X0 + 32 && ix0 + W > X0 && iy0 < Y0 + 32 &&
-                              iy0 + W > Y0;
-            const unsigned m = __ballot_sync(0xffffffffu, take);
-            if (lane == 0) sCnt[warp] = __popc(m);
-            __syncthreads();
-            int off = 0, tot = 0;
-#pragma unroll
-            for (int w2 = 0; w2 < 4; ++w2) {
-                const int c = sCnt[w2];
-                off += w2 < warp ? c : 0;
-                tot += c;
-            }
-            if (take) {
-                const uint32_t slot = (tail + off + __popc(m & lt)) & (kSCQ - 1);
-                sQt[slot] = tt[u];
-                sQb[slot] = tb[u];
-            }
-            tail += tot;
-            __syncthreads();
-            while (tail - head >= (uint32_t)kSCB) {
-                flush(kSCB);
-                head += kSCB;
-            }
+        if (tail != head) {
+            const int p = tid & 63;
+            flush((int)(tail - head), sQt[(head + p) & (kSCQ - 1)], sQb[(head + p) & (kSCQ - 1)]);
         }
     }
-    if (tail != head) flush((int)(tail - head));
+
 
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -1750,7 +1817,7 @@ struct SpreadTilesRun {
     static size_t smem() { return (size_t)4 * 32 * W * 24 + 4 * 128 * sizeof(uint32_t) + 4 * 256 * sizeof(uint32_t); }
     static void run(const WindowPoly& P, GridGeom g, TileGeom tg, const uint32_t* bs,
                     const double2* b, const double2* pos, double2* grid, cudaStream_t st,
-                    const uint32_t* bs2, const int* herm, const SpreadOut* out) {
+                    const uint32_t* bs2, const int* herm, const SpreadOut* out, const SpreadLists* lists) {
         static bool attr = false;
         if (!attr) {
             ck(cudaFuncSetAttribute(k_spread_tiles<W, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1766,14 +1833,22 @@ struct SpreadTilesRun {
         if (use_mma < 0) {
             const char* e = getenv("SBD_SPREAD");
             use_mma = !(e && e[0] == 's');
-            use_cta = !(e && (e[0] == 's' || e[0] == 'w'));
+            // default: CTA spread over the plan's region lists; 'c': CTA spread
+            // scanning the bins; 'w': per-warp DMMA spread; 's': scalar
+            use_cta = (e && (e[0] == 's' || e[0] == 'w')) ? 0 : (e && e[0] == 'c') ? 2 : 1;
             ck(cudaFuncSetAttribute(k_spread_mma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem()),
                "smem attr");
-            ck(cudaFuncSetAttribute(k_spread_cta<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            ck(cudaFuncSetAttribute(k_spread_cta<W, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)SCta<W>::smem),
                "smem attr");
-            ck(cudaFuncSetAttribute(k_spread_cta<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            ck(cudaFuncSetAttribute(k_spread_cta<W, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)SCta<W>::smem),
+               "smem attr");
+            ck(cudaFuncSetAttribute(k_spread_cta<W, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)SCta<W>::smem),
+               "smem attr");
+            ck(cudaFuncSetAttribute(k_spread_cta<W, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)SCta<W>::smem),
                "smem attr");
         }
@@ -1790,12 +1865,17 @@ struct SpreadTilesRun {
             so.nby_run = tg.nby;
         }
         if (out && !(use_mma && tg.tr == 16)) throw Error(3, "spread output modes need the DMMA spread");
+        if (lists) so.lists = *lists;
         if (use_cta && tg.tr == 16) {
             const int nblk = ((tg.nbx + 1) / 2) * ((so.nby_run + 1) / 2);
-            if (so.mode == 0 || so.mode == 2)
-                k_spread_cta<W, true><<<nblk, 128, SCta<W>::smem, st>>>(P, g, tg, bs, b, pos, grid, bs2, herm, so);
-            else
-                k_spread_cta<W, false><<<nblk, 128, SCta<W>::smem, st>>>(P, g, tg, bs, b, pos, grid, bs2, herm, so);
+            const bool cplx = so.mode == 0 || so.mode == 2, list = so.lists.s1 && use_cta == 1;
+#define SBD_SPREAD_CTA(C, LI) \
+    k_spread_cta<W, C, LI><<<nblk, 128, SCta<W>::smem, st>>>(P, g, tg, bs, b, pos, grid, bs2, herm, so)
+            if (cplx && list) SBD_SPREAD_CTA(true, true);
+            else if (cplx) SBD_SPREAD_CTA(true, false);
+            else if (list) SBD_SPREAD_CTA(false, true);
+            else SBD_SPREAD_CTA(false, false);
+#undef SBD_SPREAD_CTA
         } else if (use_mma && tg.tr == 16)
             k_spread_mma<W><<<(tg.nbx * so.nby_run + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid, bs2,
                                                                                herm, so);
@@ -1912,6 +1992,33 @@ void launch_tile_keys(const double2* pos, uint64_t n, double half, TileGeom tg, 
     ck(cudaGetLastError(), "k_tile_keys");
 }
 
+void build_region_lists(const double2* pos, uint64_t n, int w, TileGeom tg, uint32_t base, uint32_t tagbit,
+                        DevBuf<uint32_t>& start, DevBuf<uint32_t>& ent, cudaStream_t st) {
+    const int ncx = (tg.nbx + 1) / 2, ncy = (tg.nby + 1) / 2;
+    const uint32_t nreg = (uint32_t)ncx * (uint32_t)ncy;
+    start.alloc((uint64_t)nreg + 1);
+    if (!n) {
+        ck(cudaMemsetAsync(start.p, 0, ((uint64_t)nreg + 1) * 4, st), "region lists");
+        ent.alloc(1);
+        return;
+    }
+    DevBuf<uint32_t> keys(4 * n), vals(4 * n);
+    k_region_pairs<<<blocks(n, 256), 256, 0, st>>>(pos, n, 0.5 * w, w, tg, ncx, ncy, base, tagbit, keys.p,
+                                                   vals.p);
+    count_launch();
+    ck(cudaGetLastError(), "k_region_pairs");
+    sort_by_key(keys.p, vals.p, 4 * n, st);
+    // k_bin_bounds reads key >> 5; the unused slots (key nreg) sort last
+    k_shift_keys<<<blocks(4 * n, 256), 256, 0, st>>>(keys.p, 4 * n);
+    launch_bin_bounds(keys.p, 4 * n, nreg, start.p, st);
+    uint32_t used = 0;
+    ck(cudaMemcpyAsync(&used, start.p + nreg, 4, cudaMemcpyDeviceToHost, st), "region lists");
+    ck(cudaStreamSynchronize(st), "region lists");
+    ent.alloc(std::max<uint32_t>(used, 1));
+    ck(cudaMemcpyAsync(ent.p, vals.p, (size_t)used * 4, cudaMemcpyDeviceToDevice, st), "region lists");
+    ck(cudaStreamSynchronize(st), "region lists");
+}
+
 void launch_bin_bounds(const uint32_t* sorted_keys, uint64_t n, uint32_t nbins, uint32_t* start,
                        cudaStream_t st, uint32_t base, uint32_t mask) {
     k_bin_bounds<<<blocks(n + 1, 256), 256, 0, st>>>(sorted_keys, n, nbins, start, base, mask);
@@ -1922,9 +2029,9 @@ void launch_bin_bounds(const uint32_t* sorted_keys, uint64_t n, uint32_t nbins, 
 void launch_spread_tiles(int w, const WindowPoly& win, GridGeom g, TileGeom tg,
                          const uint32_t* bin_start, const double2* b, const double2* pos,
                          double2* grid, cudaStream_t st, const uint32_t* bin_start2,
-                         const int* herm, const SpreadOut* out) {
+                         const int* herm, const SpreadOut* out, const SpreadLists* lists) {
     if (tg.nbx * tg.nby == 0) return;
-    dispatch_w<SpreadTilesRun>(w, win, g, tg, bin_start, b, pos, grid, st, bin_start2, herm, out);
+    dispatch_w<SpreadTilesRun>(w, win, g, tg, bin_start, b, pos, grid, st, bin_start2, herm, out, lists);
     count_launch();
     ck(cudaGetLastError(), "k_spread_tiles");
 }

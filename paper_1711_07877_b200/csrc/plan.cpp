@@ -190,6 +190,12 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
             } else {
                 launch_bin_bounds(keys.p, n, nbins, bin_start.p, st);
             }
+            if (tg.tr == 16) {
+                const uint64_t n0 = tagged_pts ? n0_pts : n;
+                build_region_lists(pos.p, n0, w, tg, 0u, 0u, rl1_s, rl1_e, st);
+                // tag-1 points: entries index the same arrays (from n0)
+                if (tagged_pts) build_region_lists(pos.p + n0, n - n0, w, tg, (uint32_t)n0, 0u, rl2_s, rl2_e, st);
+            }
         } else {
             // 32 x 32 blocks of the Z order (k_interp_tile)
             out_shift = oshift;
@@ -330,6 +336,7 @@ bool Plan::enable_hfft(int role, cudaStream_t st) {
         for (uint64_t i = 0; i < n0_pts; ++i) inv[hs[i]] = (uint32_t)i;
         hv_of.upload(inv.data(), n0_pts, st);
         hv_src = std::move(src);
+        if (rl1_s.n) build_region_lists(hv_t.p, n0_pts, w, tg, 0u, 0x80000000u, rlh_s, rlh_e, st);
         // columns m2 in [clo, n2/2] of the Hermitian grid, as full-length columns
         hnm = n2 / 2 - clo + 1;
         hnby = std::min(tg.nby, (n2 / 2 + 1 - clo + kTileC - 1) / kTileC);
@@ -521,6 +528,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         so.rend = rhi;
         so.cend = chi;
         so.nby_run = tg.nby;
+        so.lists = lists(false);
         launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, nullptr, st, bs2, hflag, &so);
         if (tm) tm->stop();
         if (tm) tm->start(tag_fft);
@@ -558,6 +566,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         // the spread reads each mirror image's value as the conjugate of its
         // partner's (only images near the m2 = n2/2 line are ever read)
         so.src2 = hv_src.p;
+        so.lists = lists(true);
         launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, hA.p, st, hv_bins.p, nullptr, &so);
         if (tm) tm->stop();
         if (tm) tm->start(tag_fft);
@@ -584,7 +593,10 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
     }
     if (dft) {
         // compact support grid -> rows pass -> band-columns pass -> transposed band
-        launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, wk.grid.p, st, bs2, hflag);
+        {
+            const SpreadLists sl = lists(false);
+            launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, wk.grid.p, st, bs2, hflag, nullptr, &sl);
+        }
         if (tm) tm->stop();
         if (tm) tm->start(tag_fft);
         launch_pruned_dft(pass1, wk.grid.p, wk.T1.p, tw1.p, st);
@@ -608,7 +620,8 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         zero_rect_minus(wk.grid.p, n2, wk.gr0, wk.gr1, wk.gc0, wk.gc1, rlo, rhi, clo, chi, st);
     else if (wk.g_pitch)  // written by a plan of another grid size: clear all of it
         zero_rect_minus(wk.grid.p, wk.g_pitch, wk.gr0, wk.gr1, wk.gc0, wk.gc1, 0, 0, 0, 0, st);
-    launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, wk.grid.p, st, bs2, hflag);
+    const SpreadLists sl = lists(false);
+    launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, wk.grid.p, st, bs2, hflag, nullptr, &sl);
     wk.gr0 = rlo;
     wk.gr1 = rhi;
     wk.gc0 = clo;

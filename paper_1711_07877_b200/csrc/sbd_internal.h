@@ -168,6 +168,15 @@ struct PrunedPass {
 // ("s": gather in apply, spread in apply_transpose) are stored in a sorted
 // order chosen for locality; perm_* map sorted position -> caller index (empty
 // when the caller's order is kept).
+// Plan-time region lists of the CTA spread: for each 32 x 32 region (row-major,
+// ncy regions per row) the entries (point index | 0x80000000 for the second
+// point arrays) of the points whose stencil overlaps it; list 2 is skipped
+// while the device half-split flag is set.
+struct SpreadLists {
+    const uint32_t *s1 = nullptr, *e1 = nullptr, *s2 = nullptr, *e2 = nullptr;
+    int ncy = 0;
+};
+
 struct HermArgs;
 
 class Plan {
@@ -241,6 +250,18 @@ class Plan {
     DevBuf<double2> hv_t;             // role 2: mirrored tag-0 points, sorted by tile
     DevBuf<uint32_t> hv_bins, hv_of;  // their bins; tag-0 sorted position -> mirrored position
     DevBuf<uint32_t> hv_src;          // mirrored position -> tag-0 sorted position
+    // region lists of the CTA spread: set 1 (tag-0 or all points), set 2
+    // (tag-1 points), mirror images (role 2)
+    DevBuf<uint32_t> rl1_s, rl1_e, rl2_s, rl2_e, rlh_s, rlh_e;
+    SpreadLists lists(bool mirror) const {
+        SpreadLists l;
+        l.s1 = rl1_s.p;
+        l.e1 = rl1_e.p;
+        l.s2 = mirror ? rlh_s.p : rl2_s.p;
+        l.e2 = mirror ? rlh_e.p : rl2_e.p;
+        l.ncy = (tg.nby + 1) / 2;
+        return l;
+    }
     DevBuf<double> hdx_band;          // role 2: deconvolution of the band rows
     bool enable_hfft(int role, cudaStream_t st);
 
@@ -314,6 +335,7 @@ struct SpreadOut {
     const double2* pos2 = nullptr;
     const double2* b2 = nullptr;
     const uint32_t* src2 = nullptr;  // mirror image -> tag-0 partner (b2 = conj(b[src2]))
+    SpreadLists lists;
 };
 
 // ---------------------------------------------------------------- kernels
@@ -347,7 +369,11 @@ void launch_bin_bounds(const uint32_t* sorted_keys, uint64_t n, uint32_t nbins, 
 void launch_spread_tiles(int w, const WindowPoly& win, GridGeom g, TileGeom tg,
                          const uint32_t* bin_start, const double2* b, const double2* pos,
                          double2* grid, cudaStream_t st, const uint32_t* bin_start2 = nullptr,
-                         const int* herm = nullptr, const SpreadOut* out = nullptr);
+                         const int* herm = nullptr, const SpreadOut* out = nullptr,
+                         const SpreadLists* lists = nullptr);
+// SpreadLists of n points (tile-geometry grid coordinates), entries (base + k) | tagbit
+void build_region_lists(const double2* pos, uint64_t n, int w, TileGeom tg, uint32_t base, uint32_t tagbit,
+                        DevBuf<uint32_t>& start, DevBuf<uint32_t>& ent, cudaStream_t st);
 // Tt[c * n1 + r] = T[(r - rin0) * n2 + m(c)] for r in [r0, r1), c < B,
 // m(c) = c (c <= b) else n2 - B + c
 void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int B, double2* Tt,

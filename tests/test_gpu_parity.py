@@ -6,6 +6,8 @@ inputs and parameters to relative l2 <= 1e-9; the direct O(N^2) sum to
 Checkers: golden fixtures from the unmodified reference (tests/golden/), the
 compiled reference (oracle/_ref, when present) and the C restatement.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -384,3 +386,42 @@ def test_hermitian_fft_mode_device_and_host_agree(ops, name, monkeypatch):
     monkeypatch.delenv("SBD_NO_HFFT")
     qp = plain.apply(f)
     assert rel_l2(q.real, qp.real) <= 1e-13 and rel_l2(q, qp) <= 1e-13
+
+
+_SPREAD_SCRIPT = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_1711_07877_b200 as sbd
+from tests.conftest import golden
+out = []
+for name in {names!r}:
+    path, g = golden(name)
+    op = sbd.CompressedOperator.load(path)
+    f = np.random.default_rng(5).standard_normal(len(g["f"])) + 0j
+    out += [op.apply(g["f"]), op.apply(f)]
+np.save({dst!r}, np.concatenate(out))
+"""
+
+
+@pytest.mark.gpu
+def test_spread_variants_agree(tmp_path):
+    # The spread kernel is chosen once per process (SBD_SPREAD): the default
+    # CTA spread over plan-time region lists, the CTA spread scanning bins
+    # ('c') and the per-warp DMMA spread ('w') must agree on the complex path
+    # (Helmholtz), the real-input Hermitian pipelines and two-cloud plans.
+    import subprocess
+    import sys
+    from tests.conftest import ROOT
+    names = ["lap_star_n1500", "helm_disk_n800", "lap_two_clouds"]
+    res = {}
+    for v in ["", "c", "w"]:
+        dst = str(tmp_path / f"q_{v or 'default'}.npy")
+        env = dict(os.environ)
+        env.pop("SBD_SPREAD", None)
+        if v:
+            env["SBD_SPREAD"] = v
+        subprocess.run([sys.executable, "-c", _SPREAD_SCRIPT.format(root=ROOT, names=names, dst=dst)],
+                       check=True, env=env, cwd=ROOT)
+        res[v] = np.load(dst)
+    for v in ["c", "w"]:
+        assert rel_l2(res[v], res[""]) <= 1e-13, v
