@@ -548,6 +548,32 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
     }
 }
 
+// Window taps i in [I0, I1) of the pairs (i, W-1-i), plus the middle tap when
+// MID (odd W): a slice of kb_taps_each, for splitting one point over threads.
+template <int W, int I0, int I1, bool MID, typename F>
+__device__ __forceinline__ void kb_taps_slice(double u, const WindowPoly& P, F&& f) {
+    const double v = 2.0 * u - 1.0;
+    const double v2 = v * v;
+#pragma unroll
+    for (int i = I0; i < I1; ++i) {
+        double e = P.e[i][kHorner - 1], o = P.o[i][kHorner - 1];
+#pragma unroll
+        for (int h = kHorner - 2; h >= 0; --h) {
+            e = fma(e, v2, P.e[i][h]);
+            o = fma(o, v2, P.o[i][h]);
+        }
+        f(i, fma(v, o, e));
+        f(W - 1 - i, fma(-v, o, e));
+    }
+    if (MID && (W & 1)) {
+        constexpr int m = W / 2;
+        double e = P.e[m][kHorner - 1];
+#pragma unroll
+        for (int h = kHorner - 2; h >= 0; --h) e = fma(e, v2, P.e[m][h]);
+        f(m, e);
+    }
+}
+
 // CTA-cooperative DMMA spread (default). One CTA owns a 32 x 32 cell region:
 // four 16 x 16 warp tiles with the accumulators of k_spread_mma in registers.
 // Against the per-warp kernel it
@@ -563,7 +589,7 @@ __global__ void __launch_bounds__(128, 4) k_spread_mma(WindowPoly P, GridGeom g,
 //    fragments, so the MMA loop is a list load, two fragment loads and the
 //    DMMAs -- no bounds checks (lists are padded to a multiple of 4 with an
 //    all-zero point).
-constexpr int kSCB = 32;   // points per staged batch (<= 64; 32 keeps 7 CTAs per SM resident)
+constexpr int kSCB = 32;   // points per staged batch (one per lane; keeps 7 CTAs per SM resident)
 constexpr int kSCQ = 256;  // candidate ring (>= kSCB - 1 + 128)
 constexpr int kSCS = 18;   // scan segments: 2 point sets x 3 x 3 bins
 
@@ -650,27 +676,37 @@ __global__ void __launch_bounds__(128, 7) k_spread_cta(WindowPoly P, GridGeom g,
     uint32_t head = 0, tail = 0;  // ring positions (uniform across the CTA)
     // t, b2: position and coefficient of point (tid & 63) of the batch
     auto flush = [&](int n, double2 t, double2 b2) {
-        // 1. taps: thread -> (point, axis)
+        // 1. taps: warp -> (axis, half of the tap pairs), lane -> point
         {
-            const int p = tid & 63;
+            const int p = lane;
+            constexpr int H = (W / 2 + 1) / 2;  // pairs [0, H) | [H, W/2) + middle
             if (p < n) {
-                if (tid < 64) {
+                if (warp < 2) {
                     const int ix0 = (int)ceil(t.x - g.half);
-                    const int dx = ix0 - X0;  // in [1 - W, 32)
-                    const int r0 = max(0, ((dx + 64) >> 3) - 8), r1 = min(3, ((dx + W - 1 + 64) >> 3) - 8);
-                    sDX[p] = ((p * L - dx + 7) << 4) | (((2 << r1) - 1) & ~((1 << r0) - 1));
-                    double wt[W];
-                    kb_taps<W>((ix0 - t.x) + g.half, P, wt);
+                    const double u = (ix0 - t.x) + g.half;
                     double2* a = sA + p * L + 7;
-#pragma unroll
-                    for (int i = 0; i < W; ++i) a[i] = make_double2(b2.x * wt[i], b2.y * wt[i]);
+                    auto put = [&](int i, double v) { a[i] = make_double2(b2.x * v, b2.y * v); };
+                    if (warp == 0) {
+                        const int dx = ix0 - X0;  // in [1 - W, 32)
+                        const int r0 = max(0, ((dx + 64) >> 3) - 8), r1 = min(3, ((dx + W - 1 + 64) >> 3) - 8);
+                        sDX[p] = ((p * L - dx + 7) << 4) | (((2 << r1) - 1) & ~((1 << r0) - 1));
+                        kb_taps_slice<W, 0, H, false>(u, P, put);
+                    } else {
+                        kb_taps_slice<W, H, W / 2, true>(u, P, put);
+                    }
                 } else {
                     const int iy0 = (int)ceil(t.y - g.half);
-                    const int dy = iy0 - Y0;
-                    const int c0 = max(0, ((dy + 64) >> 3) - 8), c1 = min(3, ((dy + W - 1 + 64) >> 3) - 8);
-                    sDY[p] = ((p * L - dy + 7) << 4) | (((2 << c1) - 1) & ~((1 << c0) - 1));
+                    const double u = (iy0 - t.y) + g.half;
                     double* bb = sB + p * L + 7;
-                    kb_taps_each<W>((iy0 - t.y) + g.half, P, [&](int i, double v) { bb[i] = v; });
+                    auto put = [&](int i, double v) { bb[i] = v; };
+                    if (warp == 2) {
+                        const int dy = iy0 - Y0;
+                        const int c0 = max(0, ((dy + 64) >> 3) - 8), c1 = min(3, ((dy + W - 1 + 64) >> 3) - 8);
+                        sDY[p] = ((p * L - dy + 7) << 4) | (((2 << c1) - 1) & ~((1 << c0) - 1));
+                        kb_taps_slice<W, 0, H, false>(u, P, put);
+                    } else {
+                        kb_taps_slice<W, H, W / 2, true>(u, P, put);
+                    }
                 }
             }
         }
@@ -733,19 +769,19 @@ __global__ void __launch_bounds__(128, 7) k_spread_cta(WindowPoly P, GridGeom g,
             e2 = so.lists.s2[region + 1];
         }
         const uint32_t n1 = e1 - s1, nall = n1 + (e2 - s2);
-        const int p = tid & 63;
+        const int p = lane;
         // two-stage prefetch: list entries two batches ahead, positions and
         // coefficients one batch ahead
         auto entry = [&](uint32_t q0) -> uint32_t {
             const uint32_t q = q0 + p;
-            if (p >= kSCB || q >= nall) return 0xffffffffu;
+            if (q >= nall) return 0xffffffffu;
             return q < n1 ? so.lists.e1[s1 + q] : so.lists.e2[s2 + (q - n1)];
         };
         auto fetch = [&](uint32_t e, double2& t, double2& b2) {
             if (e != 0xffffffffu) {
                 const uint32_t k = e & 0x7fffffffu;
                 t = (e >> 31) ? so.pos2[k] : pos[k];
-                if (tid < 64) b2 = (e >> 31) ? mirror_coef(so, bsorted, k) : bsorted[k];
+                if (warp < 2) b2 = (e >> 31) ? mirror_coef(so, bsorted, k) : bsorted[k];
             }
         };
         double2 tn = make_double2(0.0, 0.0), bn = tn;
@@ -804,15 +840,13 @@ __global__ void __launch_bounds__(128, 7) k_spread_cta(WindowPoly P, GridGeom g,
                 tail += tot;
                 __syncthreads();
                 while (tail - head >= (uint32_t)kSCB) {
-                    const int p = tid & 63;
-                    flush(kSCB, sQt[(head + p) & (kSCQ - 1)], sQb[(head + p) & (kSCQ - 1)]);
+                    flush(kSCB, sQt[(head + lane) & (kSCQ - 1)], sQb[(head + lane) & (kSCQ - 1)]);
                     head += kSCB;
                 }
             }
         }
         if (tail != head) {
-            const int p = tid & 63;
-            flush((int)(tail - head), sQt[(head + p) & (kSCQ - 1)], sQb[(head + p) & (kSCQ - 1)]);
+            flush((int)(tail - head), sQt[(head + lane) & (kSCQ - 1)], sQb[(head + lane) & (kSCQ - 1)]);
         }
     }
 
