@@ -1608,6 +1608,36 @@ __global__ void k_gather_mul(const double2* __restrict__ in, const uint32_t* __r
 
 // qs[r] = sum_{i in row r} D'_i f'_{col'_i} (point_cloud.cpp:116-123 on the
 // renumbered matrix); 8 lanes per row, coalesced over the row's entries.
+// Same product when every value of D is real (Laplace: log r and a real
+// omega-hat): the values are stored as 8-byte reals, 12 instead of 20 bytes
+// per nonzero streamed from HBM; the result is bitwise the complex kernel's
+// (the imaginary parts it would multiply are exact zeros).
+__global__ void __launch_bounds__(256) k_spmv_vec_real(uint64_t rows, const uint64_t* __restrict__ ro,
+                                                       const uint32_t* __restrict__ cols,
+                                                       const double* __restrict__ vals,
+                                                       const double2* __restrict__ f,
+                                                       double2* __restrict__ qs) {
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t r = g >> 3;
+    const int sub = (int)(g & 7);
+    double ar = 0.0, ai = 0.0;
+    if (r < rows) {
+        const uint64_t e = ro[r + 1];
+        for (uint64_t i = ro[r] + sub; i < e; i += 8) {
+            const double v = vals[i];
+            const double2 x = f[cols[i]];
+            ar = fma(v, x.x, ar);
+            ai = fma(v, x.y, ai);
+        }
+    }
+#pragma unroll
+    for (int o = 4; o; o >>= 1) {
+        ar += __shfl_xor_sync(0xffffffffu, ar, o);
+        ai += __shfl_xor_sync(0xffffffffu, ai, o);
+    }
+    if (r < rows && sub == 0) qs[r] = make_double2(ar, ai);
+}
+
 __global__ void __launch_bounds__(256) k_spmv_vec(uint64_t rows, const uint64_t* __restrict__ ro,
                                                   const uint32_t* __restrict__ cols,
                                                   const double2* __restrict__ vals,
@@ -2206,6 +2236,14 @@ void launch_spmv_vec(uint64_t rows, const uint64_t* ro, const uint32_t* cols, co
     k_spmv_vec<<<blocks(rows * 8, 256), 256, 0, st>>>(rows, ro, cols, vals, f, qs);
     count_launch();
     ck(cudaGetLastError(), "k_spmv_vec");
+}
+
+void launch_spmv_vec_real(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double* vals,
+                          const double2* f, double2* qs, cudaStream_t st) {
+    if (!rows) return;
+    k_spmv_vec_real<<<blocks(rows * 8, 256), 256, 0, st>>>(rows, ro, cols, vals, f, qs);
+    count_launch();
+    ck(cudaGetLastError(), "k_spmv_vec_real");
 }
 
 void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int B, double2* Tt,

@@ -190,6 +190,19 @@ struct sbd_op {
     DevBuf<uint64_t> ro_s;
     DevBuf<uint32_t> cols_s;
     DevBuf<double2> vals_s;
+    // Re(D') alone: for a real f, Im(D) only feeds Im(q) (Re(q) is bitwise the
+    // complex product's), and a real-input apply of a real-omega-hat operator
+    // returns a real q -- as the half split already does for the far field
+    // (the reference's Im(D) is its NUFFT's window asymmetry, <= 2e-10 |D|)
+    DevBuf<double> vals_sr;
+
+    // rows [lo, hi) of the renumbered D' times f_sorted into qs
+    void spmv_sorted(uint64_t lo, uint64_t hi, cudaStream_t st, bool real_f = false) {
+        if (vals_sr.n && (real_f || !vals_s.n))
+            launch_spmv_vec_real(hi - lo, ro_s.p + lo, cols_s.p, vals_sr.p, f_sorted.p, qs.p + lo, st);
+        else
+            launch_spmv_vec(hi - lo, ro_s.p + lo, cols_s.p, vals_s.p, f_sorted.p, qs.p + lo, st);
+    }
     DevBuf<double2> kappa, f_sorted, qs;
     // Real-input half split: with real omega-hat and
     // antipodally paired rings, a real f has spectrum(-xi) = conj(spectrum(xi)),
@@ -462,7 +475,18 @@ struct sbd_op {
         }
         ro_s.upload(ro2.data(), nt + 1, stream);
         cols_s.upload(c2.data(), c2.size(), stream);
-        vals_s.upload(reinterpret_cast<const double2*>(v2.data()), d.nnz(), stream);
+        // D exactly real: only the real values; else both (the real copy is
+        // used for real f when omega-hat is real, i.e. the half split applies)
+        bool dreal = true;
+        for (uint64_t i = 0; i < d.nnz() && dreal; ++i) dreal = v2[2 * i + 1] == 0.0;
+        bool wreal = !std::getenv("SBD_COMPLEX_D");
+        for (uint64_t i = 0; i < d.n_xi() && wreal; ++i) wreal = d.weights[2 * i + 1] == 0.0;
+        if (dreal || wreal) {
+            std::vector<double> vr(d.nnz());
+            for (uint64_t i = 0; i < d.nnz(); ++i) vr[i] = v2[2 * i];
+            vals_sr.upload(vr.data(), d.nnz(), stream);
+        }
+        if (!dreal) vals_s.upload(reinterpret_cast<const double2*>(v2.data()), d.nnz(), stream);
         ck(cudaStreamSynchronize(stream), "fused upload");
     }
 
@@ -472,7 +496,8 @@ struct sbd_op {
     void apply_one(const double2* f, double2* q, cudaStream_t st, int real_hint = -1) {
         if (fused) {
             HermArgs hin, hout;
-            const bool hfft_now = hfft_ok && (real_hint == 1 || (real_hint < 0 && device_real(f, d.n_src(), st)));
+            const bool real_f = herm_ok && (real_hint == 1 || (real_hint < 0 && device_real(f, d.n_src(), st)));
+            const bool hfft_now = hfft_ok && real_f;
             if (herm_ok) {
                 ck(cudaMemsetAsync(herm_flag.p, 1, sizeof(int), st), "half flag");
                 hin.flag = hout.flag = herm_flag.p;
@@ -498,7 +523,7 @@ struct sbd_op {
             static const bool overlap = std::getenv("SBD_OVERLAP") != nullptr;
             if (!overlap) {
                 if (tm.on) tm.start("spmv");
-                launch_spmv_vec(d.n_tgt(), ro_s.p, cols_s.p, vals_s.p, f_sorted.p, qs.p, st);
+                spmv_sorted(0, d.n_tgt(), st, real_f);
                 if (tm.on) tm.stop();
             } else {
                 if (!side) {
@@ -509,7 +534,7 @@ struct sbd_op {
                 ck(cudaEventRecord(ev_f, st), "event");
                 ck(cudaStreamWaitEvent(side, ev_f, 0), "wait");
                 if (tm.on) tm.start("spmv", side);
-                launch_spmv_vec(d.n_tgt(), ro_s.p, cols_s.p, vals_s.p, f_sorted.p, qs.p, side);
+                spmv_sorted(0, d.n_tgt(), side, real_f);
                 if (tm.on) tm.stop(side);
                 ck(cudaEventRecord(ev_qs, side), "event");
                 wait = ev_qs;
@@ -577,7 +602,7 @@ struct sbd_op {
         lo = std::min(lo, hi);
         launch_gather_mul(f, fwd_in->perm_t.p, fwd_in->pre.p, work.bbuf.p, f_sorted.p, d.n_src(), st, 0, 0);
         if (tm.on) tm.start("spmv");
-        launch_spmv_vec(hi - lo, ro_s.p + lo, cols_s.p, vals_s.p, f_sorted.p, qs.p + lo, st);
+        spmv_sorted(lo, hi, st, shard_real);
         if (tm.on) tm.stop();
         HermArgs h;
         if (shard_real) {
@@ -598,7 +623,7 @@ struct sbd_op {
 
     size_t device_bytes() const {
         return fwd_in->device_bytes() + fwd_out->device_bytes() + w_sorted.bytes() + w_in.bytes() + ro.bytes() +
-               ro_s.bytes() + cols_s.bytes() + vals_s.bytes() + kappa.bytes() + f_sorted.bytes() +
+               ro_s.bytes() + cols_s.bytes() + vals_s.bytes() + vals_sr.bytes() + kappa.bytes() + f_sorted.bytes() +
                qs.bytes() + work.bbuf.bytes() +
                cols.bytes() + vals.bytes() + work.grid.bytes() + work.T.bytes() + work.band.bytes() +
                spec.bytes() + hf.bytes() + hq.bytes() + kappa_h.bytes();

@@ -403,6 +403,8 @@ void launch_gather_mul(const double2* in, const uint32_t* perm, const double2* p
                        uint64_t hi = ~0ull, int* clear = nullptr);
 void launch_spmv_vec(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double2* vals,
                      const double2* f, double2* qs, cudaStream_t st);
+void launch_spmv_vec_real(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double* vals,
+                          const double2* f, double2* qs, cudaStream_t st);
 void sort_by_key(uint32_t* keys, uint32_t* vals, uint64_t n, cudaStream_t st);
 void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st);
 template <typename T>
