@@ -380,6 +380,14 @@ __device__ __forceinline__ double2 mirror_coef(const SpreadOut& so, const double
     return so.b2[k];
 }
 
+// storage position of mode j of a column transformed by a radix-r first pass
+// (k_untangle_dif): (j mod r) M + j / r, the quotient by multiply-high
+__device__ __forceinline__ int rad_pos(const GridGeom& g, int j) {
+    if (g.rad <= 1) return j;
+    const int q = (int)__umulhi((unsigned)j, g.rad_magic);
+    return (j - q * g.rad) * g.rad_m + q;
+}
+
 // fp64 tensor-core MMA: D(8x8) = A(8x4) B(4x8) + C (mma.sync m8n8k4 f64; SASS
 // DMMA.8x8x4). Fragments: a = A[lane/4][lane%4], b = B[lane%4][lane/4],
 // c = {C[lane/4][2(lane%4)], C[lane/4][2(lane%4)+1]}.
@@ -1412,10 +1420,11 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
                     const int gr = wrap_near(X0 + r, g.n1), gc = wrap_near(Y0 + c, g.n2);
                     if (TRANS && hcols && gc >= hcols) {
                         // negative column: conjugate of the mirrored stored cell
-                        const double2 m = __ldg(grid + (size_t)(g.n2 - gc) * g.n1 + (gr ? g.n1 - gr : 0));
+                        const double2 m =
+                            __ldg(grid + (size_t)(g.n2 - gc) * g.n1 + rad_pos(g, gr ? g.n1 - gr : 0));
                         v[u] = make_double2(m.x, -m.y);
                     } else {
-                        v[u] = __ldg(TRANS ? grid + (size_t)gc * g.n1 + gr : grid + (size_t)gr * g.n2 + gc);
+                        v[u] = __ldg(TRANS ? grid + (size_t)gc * g.n1 + rad_pos(g, gr) : grid + (size_t)gr * g.n2 + gc);
                     }
                     f[u] = (dxt ? __ldg(dxt + gr) : 1.0) * (dyt ? __ldg(dyt + gc) : 1.0);
                 }
@@ -1776,6 +1785,91 @@ __global__ void __launch_bounds__(256) k_untangle_transpose(const double2* __res
 // c (mode j1(c)) has half-spectrum X_c[m] = Y[(m - m0) * n1 + j1(c)] for m in
 // [m0, n2/2] (zero below m0); row k of Z (full length n2, m in [m0, n2 - m0])
 // = X_{2k}(m) + i X_{2k+1}(m) with X(m) = conj X(n2 - m) for m > n2/2.
+// ---- radix-r first pass of a length n = r M transform (FFTW_BACKWARD sign) --
+// Decimation in frequency: X[r j' + s] = DFT_M(y_s)[j'] with
+//   y_s[k] = w_n^{s k} sum_rho x[k + M rho] w_r^{s rho},  w_m = e^{+2 pi i/m},
+// so the producer of x writes y (position s M + k), one batched length-M
+// cuFFT pass follows, and mode j is read at position (j mod r) M + j / r.
+// tw[m] = w_n^m for m < n.
+template <int R>
+__device__ __forceinline__ void dft_small(const double2 (&x)[R], double2 (&y)[R], const double2* __restrict__ tw,
+                                          int M) {
+    if (R == 9) {
+        // 9 = 3 x 3: rho = 3 a + b, s = s1 + 3 s2
+        const double h = 0.8660254037844386467637231707529362;  // sqrt(3) / 2
+        double2 t[3][3];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+            const double2 p = x[b], q = x[3 + b], u = x[6 + b];
+            const double2 sum = make_double2(q.x + u.x, q.y + u.y), dif = make_double2(q.x - u.x, q.y - u.y);
+            const double2 m = make_double2(p.x - 0.5 * sum.x, p.y - 0.5 * sum.y);
+            t[b][0] = make_double2(p.x + sum.x, p.y + sum.y);
+            t[b][1] = make_double2(m.x - h * dif.y, m.y + h * dif.x);
+            t[b][2] = make_double2(m.x + h * dif.y, m.y - h * dif.x);
+            if (b) {
+                t[b][1] = cmul(t[b][1], __ldg(tw + b * M));      // w_9^{b s1}, s1 = 1
+                t[b][2] = cmul(t[b][2], __ldg(tw + 2 * b * M));  // s1 = 2
+            }
+        }
+#pragma unroll
+        for (int s1 = 0; s1 < 3; ++s1) {
+            const double2 p = t[0][s1], q = t[1][s1], u = t[2][s1];
+            const double2 sum = make_double2(q.x + u.x, q.y + u.y), dif = make_double2(q.x - u.x, q.y - u.y);
+            const double2 m = make_double2(p.x - 0.5 * sum.x, p.y - 0.5 * sum.y);
+            y[s1] = make_double2(p.x + sum.x, p.y + sum.y);
+            y[s1 + 3] = make_double2(m.x - h * dif.y, m.y + h * dif.x);
+            y[s1 + 6] = make_double2(m.x + h * dif.y, m.y - h * dif.x);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            double2 a = x[0];
+#pragma unroll
+            for (int rho = 1; rho < R; ++rho) {
+                const double2 w = __ldg(tw + ((k * rho) % R) * M);
+                a.x += x[rho].x * w.x - x[rho].y * w.y;
+                a.y += x[rho].x * w.y + x[rho].y * w.x;
+            }
+            y[k] = a;
+        }
+    }
+}
+
+// k_untangle_transpose with the radix-R first pass of the column transform
+// folded in: the band columns c < B of the untangled real rows x[m1] (rows
+// [r0, r0 + 2 nr), zero elsewhere) leave as y_s[k] (column c at c * n1 +
+// s M + k, n1 = R M) for a batched length-M column transform.
+template <int R>
+__global__ void __launch_bounds__(256) k_untangle_dif(const double2* __restrict__ T, int n2, int nr, int B,
+                                                      double2* __restrict__ Tt, int n1, int r0, int M,
+                                                      const double2* __restrict__ tw) {
+    __shared__ double2 so[R][8][33];
+    const int c0 = blockIdx.x * 32, k0 = blockIdx.y * 8;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int c = c0 + lane, k = k0 + w;
+    double2 x[R], y[R];
+#pragma unroll
+    for (int rho = 0; rho < R; ++rho) {
+        const int m1 = k + M * rho;
+        x[rho] = make_double2(0.0, 0.0);
+        if (c < B && m1 >= r0 && m1 < r0 + 2 * nr) {
+            const int kk = (m1 - r0) >> 1;
+            const double2 a = T[(size_t)kk * n2 + c], b = T[(size_t)kk * n2 + (c ? n2 - c : 0)];
+            x[rho] = ((m1 - r0) & 1) ? make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x))
+                                     : make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+        }
+    }
+    dft_small<R>(x, y, tw, M);
+#pragma unroll
+    for (int sI = 0; sI < R; ++sI) so[sI][w][lane] = sI ? cmul(y[sI], __ldg(tw + sI * k)) : y[sI];
+    __syncthreads();
+    const int kl = threadIdx.x & 7;
+    for (int p = threadIdx.x >> 3; p < 32 * R; p += 32) {
+        const int sI = p >> 5, cl = p & 31;
+        if (c0 + cl < B) Tt[(size_t)(c0 + cl) * n1 + (size_t)sI * M + k0 + kl] = so[sI][kl][cl];
+    }
+}
+
 __global__ void __launch_bounds__(256) k_pack_rows(const double2* __restrict__ Y, int n1, int m0,
                                                    int n2, int b1, int B1, double2* __restrict__ Z) {
     __shared__ double2 sy[32][33];  // [m][band row]
@@ -2253,6 +2347,23 @@ void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int 
     k_band_transpose<<<grid, 256, 0, st>>>(T, n2, r0, r1, b, B, Tt, n1, rin0, conj_out);
     count_launch();
     ck(cudaGetLastError(), "k_band_transpose");
+}
+
+void launch_untangle_dif(const double2* T, int n2, int nr, int B, double2* Tt, int n1, int r0, int R,
+                        const double2* tw, cudaStream_t st) {
+    if (nr <= 0 || B <= 0) return;
+    const int M = n1 / R;
+    dim3 grid((unsigned)((B + 31) / 32), (unsigned)(M / 8));
+    if (R == 9)
+        k_untangle_dif<9><<<grid, 256, 0, st>>>(T, n2, nr, B, Tt, n1, r0, M, tw);
+    else if (R == 5)
+        k_untangle_dif<5><<<grid, 256, 0, st>>>(T, n2, nr, B, Tt, n1, r0, M, tw);
+    else if (R == 3)
+        k_untangle_dif<3><<<grid, 256, 0, st>>>(T, n2, nr, B, Tt, n1, r0, M, tw);
+    else
+        throw Error(3, "untangle_dif: unsupported radix");
+    count_launch();
+    ck(cudaGetLastError(), "k_untangle_dif");
 }
 
 void launch_untangle_transpose(const double2* T, int n2, int nr, int B, double2* Tt, int n1, int r0,

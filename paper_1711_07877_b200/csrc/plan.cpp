@@ -285,6 +285,20 @@ Plan::~Plan() {
     if (hp2) cufftDestroy(hp2);
 }
 
+// Radix r of a first pass folded into the producer of a length-n transform
+// (n = r M, r in {3, 5, 9}, M <= 4096 a multiple of 8: cuFFT then runs one
+// length-M pass instead of two length-n passes). 1: none. Used for n > 4096;
+// SBD_RADIX=0 turns it off, SBD_RADIX=force uses it for any such n (tests).
+static int pick_radix(int n) {
+    const char* e = std::getenv("SBD_RADIX");
+    if (e && e[0] == '0') return 1;
+    const bool force = e && e[0] == 'f';
+    if (!force && n <= 4096) return 1;
+    for (int r : {3, 5, 9})
+        if (n % r == 0 && n / r <= 4096 && (n / r) % 8 == 0) return r;
+    return 1;
+}
+
 bool Plan::enable_hfft(int role, cudaStream_t st) {
     if (!fast || !pruned || dft) return false;
     const int n1 = ax.n, n2 = ay.n, R = rhi - rlo;
@@ -301,7 +315,21 @@ bool Plan::enable_hfft(int role, cudaStream_t st) {
         hC.alloc((size_t)hcols * n1);
         int nr[1] = {n2}, nc[1] = {n1};
         ckfft(cufftPlanMany(&hp1, 1, nr, nr, 1, n2, nr, 1, n2, CUFFT_Z2Z, R / 2), "hfft Z2Z rows");
-        ckfft(cufftPlanMany(&hp2, 1, nc, nc, 1, n1, nc, 1, n1, CUFFT_Z2Z, hcols), "hfft Z2Z cols");
+        hrad = pick_radix(n1);
+        if (hrad > 1) {
+            // the untangle does the radix-hrad first pass; cuFFT one length-M pass
+            const int M = n1 / hrad;
+            int nm[1] = {M};
+            ckfft(cufftPlanMany(&hp2, 1, nm, nm, 1, M, nm, 1, M, CUFFT_Z2Z, hcols * hrad), "hfft Z2Z cols (M)");
+            std::vector<double2> tw(n1);
+            for (int m = 0; m < n1; ++m) {
+                const long double a = 2.0L * 3.14159265358979323846264338327950288L * m / n1;
+                tw[m] = make_double2((double)cosl(a), (double)sinl(a));
+            }
+            htw.upload(tw.data(), n1, st);
+        } else {
+            ckfft(cufftPlanMany(&hp2, 1, nc, nc, 1, n1, nc, 1, n1, CUFFT_Z2Z, hcols), "hfft Z2Z cols");
+        }
     } else if (role == 2) {
         if (!tagged_pts || !n0_pts) return false;
         const GridGeom g{n1, n2, 0.5 * w};
@@ -536,7 +564,10 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         ckfft(cufftExecZ2Z(hp1, reinterpret_cast<cufftDoubleComplex*>(hA.p),
                            reinterpret_cast<cufftDoubleComplex*>(hD.p), CUFFT_INVERSE),
               "hfft Z2Z rows");
-        launch_untangle_transpose(hD.p, n2, (rhi - rlo) / 2, hcols, hB.p, ax.n, rlo, st);
+        if (hrad > 1)
+            launch_untangle_dif(hD.p, n2, (rhi - rlo) / 2, hcols, hB.p, ax.n, rlo, hrad, htw.p, st);
+        else
+            launch_untangle_transpose(hD.p, n2, (rhi - rlo) / 2, hcols, hB.p, ax.n, rlo, st);
         ckfft(cufftSetStream(hp2, st), "cufftSetStream");
         ckfft(cufftExecZ2Z(hp2, reinterpret_cast<cufftDoubleComplex*>(hB.p),
                            reinterpret_cast<cufftDoubleComplex*>(hC.p), CUFFT_INVERSE),
@@ -545,7 +576,12 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         if (tm) tm->stop();
         if (before_interp) ck(cudaStreamWaitEvent(st, before_interp, 0), "wait");
         if (tm) tm->start(tag_interp);
-        const GridGeom gt{ax.n, bc, 0.5 * w};
+        GridGeom gt{ax.n, bc, 0.5 * w};
+        if (hrad > 1) {
+            gt.rad = hrad;
+            gt.rad_m = ax.n / hrad;
+            gt.rad_magic = (unsigned)((0x100000000ull + hrad - 1) / hrad);
+        }
         launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx.p, dy_band.p, hC.p, perm_p, out_p, 0, 0, st,
                       add_p, /*transposed=*/true, &otiles, hp);
         if (tm) tm->stop();

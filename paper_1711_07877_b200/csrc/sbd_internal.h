@@ -245,6 +245,8 @@ class Plan {
     // Z2Z rows give the real band for the target interpolation.
     int hrole = 0;
     cufftHandle hp1 = 0, hp2 = 0;
+    int hrad = 1;                    // role 1: radix of the column transform's first pass (1: none)
+    DevBuf<double2> htw;             // its twiddles e^{+2 pi i m / n1}
     mutable DevBuf<double2> hA, hB, hC, hD;
     int hnm = 0, hnby = 0, hb1 = 0, hB1 = 0, hcols = 0;
     DevBuf<double2> hv_t;             // role 2: mirrored tag-0 points, sorted by tile
@@ -343,6 +345,10 @@ struct SpreadOut {
 struct GridGeom {
     int n1, n2;
     double half;
+    // rows stored in radix-r first-pass order (k_untangle_dif): mode j at
+    // (j mod rad) rad_m + j / rad; rad_magic = ceil(2^32 / rad)
+    int rad = 1, rad_m = 0;
+    unsigned rad_magic = 0;
 };
 
 void launch_plan_points(const double2* pts, uint64_t n, Axis ax, Axis ay, double beta,
@@ -387,6 +393,10 @@ void launch_any_imag(const double2* x, uint64_t n, int* flag, cudaStream_t st);
 // packed real rows -> untangled, transposed half band (see kernels.cu)
 void launch_untangle_transpose(const double2* T, int n2, int nr, int B, double2* Tt, int n1, int r0,
                                cudaStream_t st);
+// the same untangle with the radix-R (3, 5, 9) first pass of the length
+// n1 = R M column transform folded in; tw[m] = e^{+2 pi i m / n1}
+void launch_untangle_dif(const double2* T, int n2, int nr, int B, double2* Tt, int n1, int r0, int R,
+                         const double2* tw, cudaStream_t st);
 // Hermitian band rows from half-plane columns -> pairs packed into full rows
 void launch_pack_rows(const double2* Y, int n1, int m0, int n2, int b1, int B1, double2* Z, cudaStream_t st);
 // interpolation from a real band grid whose rows are packed in pairs (row r =

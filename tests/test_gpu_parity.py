@@ -424,3 +424,21 @@ def test_spread_variants_agree(tmp_path):
         res[v] = np.load(dst)
     for v in ["c", "w"]:
         assert rel_l2(res[v], res[""]) <= 1e-13, v
+
+
+@pytest.mark.parametrize("name", HALF_CASES)
+def test_radix_first_pass_agrees(ops, name, monkeypatch):
+    # Hermitian source side: the radix-r first pass of the column transform
+    # folded into the untangle (k_untangle_dif + length-M cuFFT, band read in
+    # (j mod r) M + j / r order) against the plain length-n1 transform.
+    # Used by default above n1 = 4096 (config 4: 18432 = 9 x 2048); forced here.
+    path, g = golden(name)
+    f = np.random.default_rng(41).standard_normal(len(g["f"])) + 0j
+    monkeypatch.setenv("SBD_RADIX", "force")
+    rad = sbd.CompressedOperator.load(path)
+    monkeypatch.setenv("SBD_RADIX", "0")
+    plain = sbd.CompressedOperator.load(path)
+    monkeypatch.delenv("SBD_RADIX")
+    q = rad.apply(f)
+    assert rel_l2(q, plain.apply(f)) <= 1e-13
+    assert rel_l2(q, ops[name].apply(f)) <= 1e-13
