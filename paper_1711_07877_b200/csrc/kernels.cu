@@ -1274,7 +1274,7 @@ __global__ void __launch_bounds__(128) k_interp_real_tile(
                     const int r = i / E, c = i - (i / E) * E;
                     const int gr = wrap_near(X0 + r, g.n1), gc = wrap_near(Y0 + c, g.n2);
                     // rows packed in pairs (component gr & 1 of complex row gr >> 1)
-                    v[u] = __ldg(grid + 2 * ((size_t)(gr >> 1) * g.n2 + gc) + (gr & 1));
+                    v[u] = __ldg(grid + 2 * ((size_t)(gr >> 1) * g.n2 + rad_pos(g, gc)) + (gr & 1));
                 }
             }
 #pragma unroll
@@ -1870,6 +1870,47 @@ __global__ void __launch_bounds__(256) k_untangle_dif(const double2* __restrict_
     }
 }
 
+// k_pack_rows with the radix-R first pass of the length n2 = R M row
+// transform folded in: packed row k (band rows 2k, 2k+1 as z = a + i b, the
+// columns above n2/2 their conjugate mirror) leaves as y_s[k1] at
+// k n2 + s M + k1 for a batched length-M row transform.
+template <int R>
+__global__ void __launch_bounds__(256) k_pack_dif(const double2* __restrict__ Y, int n1, int m0, int n2,
+                                                  int b1, int B1, double2* __restrict__ Z, int M,
+                                                  const double2* __restrict__ tw) {
+    __shared__ double2 so[R][8][33];  // [s][k1][packed row]
+    const int kb = blockIdx.x * 32, k10 = blockIdx.y * 8;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int k = kb + lane, k1 = k10 + w;
+    const int mhi = n2 / 2, K = (B1 + 1) / 2;
+    const int ra = 2 * k, rb = 2 * k + 1;
+    const int ia = ra <= b1 ? ra : n1 - B1 + ra, ib = rb <= b1 ? rb : n1 - B1 + rb;
+    double2 z[R], y[R];
+#pragma unroll
+    for (int rho = 0; rho < R; ++rho) {
+        const int m = k1 + M * rho;
+        z[rho] = make_double2(0.0, 0.0);
+        if (k < K) {
+            const bool dir = m >= m0 && m <= mhi;
+            const int mm = dir ? m : n2 - m;  // mirrored source column
+            if (dir || (m > mhi && mm >= m0)) {
+                const double2 a = Y[(size_t)(mm - m0) * n1 + ia];
+                const double2 b = rb < B1 ? Y[(size_t)(mm - m0) * n1 + ib] : make_double2(0.0, 0.0);
+                z[rho] = dir ? make_double2(a.x - b.y, a.y + b.x) : make_double2(a.x + b.y, -a.y + b.x);
+            }
+        }
+    }
+    dft_small<R>(z, y, tw, M);
+#pragma unroll
+    for (int sI = 0; sI < R; ++sI) so[sI][w][lane] = sI ? cmul(y[sI], __ldg(tw + sI * k1)) : y[sI];
+    __syncthreads();
+    const int kl = threadIdx.x & 7;
+    for (int p = threadIdx.x >> 3; p < 32 * R; p += 32) {
+        const int sI = p >> 5, rl = p & 31;
+        if (kb + rl < K) Z[(size_t)(kb + rl) * n2 + (size_t)sI * M + k10 + kl] = so[sI][kl][rl];
+    }
+}
+
 __global__ void __launch_bounds__(256) k_pack_rows(const double2* __restrict__ Y, int n1, int m0,
                                                    int n2, int b1, int B1, double2* __restrict__ Z) {
     __shared__ double2 sy[32][33];  // [m][band row]
@@ -2364,6 +2405,23 @@ void launch_untangle_dif(const double2* T, int n2, int nr, int B, double2* Tt, i
         throw Error(3, "untangle_dif: unsupported radix");
     count_launch();
     ck(cudaGetLastError(), "k_untangle_dif");
+}
+
+void launch_pack_dif(const double2* Y, int n1, int m0, int n2, int b1, int B1, double2* Z, int R,
+                     const double2* tw, cudaStream_t st) {
+    const int K = (B1 + 1) / 2, M = n2 / R;
+    if (K <= 0) return;
+    dim3 grid((unsigned)((K + 31) / 32), (unsigned)(M / 8));
+    if (R == 9)
+        k_pack_dif<9><<<grid, 256, 0, st>>>(Y, n1, m0, n2, b1, B1, Z, M, tw);
+    else if (R == 5)
+        k_pack_dif<5><<<grid, 256, 0, st>>>(Y, n1, m0, n2, b1, B1, Z, M, tw);
+    else if (R == 3)
+        k_pack_dif<3><<<grid, 256, 0, st>>>(Y, n1, m0, n2, b1, B1, Z, M, tw);
+    else
+        throw Error(3, "pack_dif: unsupported radix");
+    count_launch();
+    ck(cudaGetLastError(), "k_pack_dif");
 }
 
 void launch_untangle_transpose(const double2* T, int n2, int nr, int B, double2* Tt, int n1, int r0,

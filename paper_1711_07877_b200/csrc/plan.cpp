@@ -289,6 +289,17 @@ Plan::~Plan() {
 // (n = r M, r in {3, 5, 9}, M <= 4096 a multiple of 8: cuFFT then runs one
 // length-M pass instead of two length-n passes). 1: none. Used for n > 4096;
 // SBD_RADIX=0 turns it off, SBD_RADIX=force uses it for any such n (tests).
+// tw[m] = e^{+2 pi i m / n}, m < n (long double arguments)
+static void upload_twiddles(DevBuf<double2>& tw, int n, cudaStream_t st) {
+    std::vector<double2> h(n);
+    for (int m = 0; m < n; ++m) {
+        const long double a = 2.0L * 3.14159265358979323846264338327950288L * m / n;
+        h[m] = make_double2((double)cosl(a), (double)sinl(a));
+    }
+    tw.upload(h.data(), n, st);
+    ck(cudaStreamSynchronize(st), "twiddles");
+}
+
 static int pick_radix(int n) {
     const char* e = std::getenv("SBD_RADIX");
     if (e && e[0] == '0') return 1;
@@ -321,12 +332,7 @@ bool Plan::enable_hfft(int role, cudaStream_t st) {
             const int M = n1 / hrad;
             int nm[1] = {M};
             ckfft(cufftPlanMany(&hp2, 1, nm, nm, 1, M, nm, 1, M, CUFFT_Z2Z, hcols * hrad), "hfft Z2Z cols (M)");
-            std::vector<double2> tw(n1);
-            for (int m = 0; m < n1; ++m) {
-                const long double a = 2.0L * 3.14159265358979323846264338327950288L * m / n1;
-                tw[m] = make_double2((double)cosl(a), (double)sinl(a));
-            }
-            htw.upload(tw.data(), n1, st);
+            upload_twiddles(htw, n1, st);
         } else {
             ckfft(cufftPlanMany(&hp2, 1, nc, nc, 1, n1, nc, 1, n1, CUFFT_Z2Z, hcols), "hfft Z2Z cols");
         }
@@ -384,7 +390,16 @@ bool Plan::enable_hfft(int role, cudaStream_t st) {
         hdx_band.upload(hb.data(), hB1, st);
         int nc[1] = {n1}, nr[1] = {n2};
         ckfft(cufftPlanMany(&hp1, 1, nc, nc, 1, n1, nc, 1, n1, CUFFT_Z2Z, hnm), "hfft Z2Z cols");
-        ckfft(cufftPlanMany(&hp2, 1, nr, nr, 1, n2, nr, 1, n2, CUFFT_Z2Z, K), "hfft Z2Z rows");
+        hrad = pick_radix(n2);
+        if (hrad > 1) {
+            // the packing does the radix-hrad first pass; cuFFT one length-M pass
+            const int M = n2 / hrad;
+            int nm[1] = {M};
+            ckfft(cufftPlanMany(&hp2, 1, nm, nm, 1, M, nm, 1, M, CUFFT_Z2Z, K * hrad), "hfft Z2Z rows (M)");
+            upload_twiddles(htw, n2, st);
+        } else {
+            ckfft(cufftPlanMany(&hp2, 1, nr, nr, 1, n2, nr, 1, n2, CUFFT_Z2Z, K), "hfft Z2Z rows");
+        }
     } else {
         return false;
     }
@@ -612,7 +627,10 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
               "hfft Z2Z cols");
         // two Hermitian band rows per complex row: their transforms are the
         // real and imaginary parts of one e^{+} transform
-        launch_pack_rows(hB.p, ax.n, clo, n2, hb1, hB1, hC.p, st);
+        if (hrad > 1)
+            launch_pack_dif(hB.p, ax.n, clo, n2, hb1, hB1, hC.p, hrad, htw.p, st);
+        else
+            launch_pack_rows(hB.p, ax.n, clo, n2, hb1, hB1, hC.p, st);
         ckfft(cufftSetStream(hp2, st), "cufftSetStream");
         ckfft(cufftExecZ2Z(hp2, reinterpret_cast<cufftDoubleComplex*>(hC.p),
                            reinterpret_cast<cufftDoubleComplex*>(hD.p), CUFFT_INVERSE),
@@ -621,7 +639,12 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         if (tm) tm->stop();
         if (before_interp) ck(cudaStreamWaitEvent(st, before_interp, 0), "wait");
         if (tm) tm->start(tag_interp);
-        const GridGeom gr{hB1, n2, 0.5 * w};
+        GridGeom gr{hB1, n2, 0.5 * w};
+        if (hrad > 1) {
+            gr.rad = hrad;
+            gr.rad_m = n2 / hrad;
+            gr.rad_magic = (unsigned)((0x100000000ull + hrad - 1) / hrad);
+        }
         launch_interp_real(w, win, gr, nout, s_p, post_p, hdx_band.p, dy.p,
                            reinterpret_cast<const double*>(hD.p), perm_p, add_p, out_p, st, &otiles);
         if (tm) tm->stop();

@@ -245,8 +245,9 @@ class Plan {
     // Z2Z rows give the real band for the target interpolation.
     int hrole = 0;
     cufftHandle hp1 = 0, hp2 = 0;
-    int hrad = 1;                    // role 1: radix of the column transform's first pass (1: none)
-    DevBuf<double2> htw;             // its twiddles e^{+2 pi i m / n1}
+    int hrad = 1;                    // radix of the first pass folded into untangle (role 1, columns)
+                                     // or pack (role 2, rows); 1: none
+    DevBuf<double2> htw;             // its twiddles e^{+2 pi i m / n}
     mutable DevBuf<double2> hA, hB, hC, hD;
     int hnm = 0, hnby = 0, hb1 = 0, hB1 = 0, hcols = 0;
     DevBuf<double2> hv_t;             // role 2: mirrored tag-0 points, sorted by tile
@@ -399,6 +400,10 @@ void launch_untangle_dif(const double2* T, int n2, int nr, int B, double2* Tt, i
                          const double2* tw, cudaStream_t st);
 // Hermitian band rows from half-plane columns -> pairs packed into full rows
 void launch_pack_rows(const double2* Y, int n1, int m0, int n2, int b1, int B1, double2* Z, cudaStream_t st);
+// the same packing with the radix-R first pass of the length n2 = R M row
+// transform folded in (rows in (j mod R) M + j / R order); tw[m] = e^{+2 pi i m / n2}
+void launch_pack_dif(const double2* Y, int n1, int m0, int n2, int b1, int B1, double2* Z, int R,
+                     const double2* tw, cudaStream_t st);
 // interpolation from a real band grid whose rows are packed in pairs (row r =
 // component r & 1 of complex row r >> 1, complex pitch g.n2):
 // out[perm?perm[k]:k] = Re(sum taps * dx dy * grid * phase[k]) + addend[k]
