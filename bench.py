@@ -344,6 +344,35 @@ def run_b200(args, w):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
+    # batched right-hand sides (GMRES-style blocks, BASELINE config 5's "batch of
+    # 8"): one apply of nrhs columns, D read once for all of them (k_spmm)
+    batched = None
+    if world == 1 and args.nrhs > 1:
+        fb = np.stack([rhs(w, n, np.random.default_rng(SEED + 10 + r)) for r in range(args.nrhs)])
+        fb_dev = torch.from_numpy(fb.view(np.float64).reshape(-1).copy()).cuda()
+        qb_dev = torch.empty(2 * n * args.nrhs, dtype=torch.float64, device="cuda")
+
+        def bstep():
+            op.apply_device(fb_dev.data_ptr(), qb_dev.data_ptr(), args.nrhs, sh)
+        bstep()
+        torch.cuda.synchronize()
+        op.set_profiling(True)
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        b0.record(stream)
+        for _ in range(reps):
+            bstep()
+        b1.record(stream)
+        torch.cuda.synchronize()
+        bst = op.stage_times()
+        op.set_profiling(False)
+        bms = b0.elapsed_time(b1) / reps
+        spmv_ms = sum(ms for nm, ms in bst if nm == "spmv") / reps
+        batched = {"nrhs": args.nrhs, "value": n * args.nrhs / (bms / 1e3), "unit": "points/s",
+                   "ms_per_apply": round(bms, 3), "spmv_ms_per_apply": round(spmv_ms, 3),
+                   "note": "one apply of nrhs right-hand sides; D' streamed once for up to 8 columns"}
+        del fb_dev, qb_dev
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         kind, apply, fs, path = reference_sample(w, args.sample_n)
@@ -373,6 +402,7 @@ def run_b200(args, w):
                     "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n},
             "gpu_launches": launches,
             "clocks": clk,
+            "batched_rhs": batched,
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -391,6 +421,7 @@ def main():
     ap.add_argument("--sample-n", type=int, default=50000, help="reference CPU sample size")
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nrhs", type=int, default=8, help="also time one batched apply of this many RHS (1: off)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     w = workload(args.config, args.scale)

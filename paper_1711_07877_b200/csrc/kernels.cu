@@ -2373,6 +2373,87 @@ void launch_spmv_vec(uint64_t rows, const uint64_t* ro, const uint32_t* cols, co
     ck(cudaGetLastError(), "k_spmv_vec");
 }
 
+// k_spmv_vec / k_spmv_vec_real for NR right-hand sides at once: each
+// nonzero's value and column are loaded once; per column the summation
+// order is the single-RHS kernels' (bitwise equal results).
+template <int NR, bool RD>
+__global__ void __launch_bounds__(256) k_spmm(uint64_t rows, const uint64_t* __restrict__ ro,
+                                              const uint32_t* __restrict__ cols,
+                                              const double2* __restrict__ vals,
+                                              const double* __restrict__ vals_r,
+                                              const double2* __restrict__ f, uint64_t ldf,
+                                              double2* __restrict__ qs, uint64_t ldq, SpmmCols cs) {
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t r = g >> 3;
+    const int sub = (int)(g & 7);
+    double ar[NR], ai[NR];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) ar[j] = ai[j] = 0.0;
+    if (r < rows) {
+        const uint64_t e = ro[r + 1];
+        for (uint64_t i = ro[r] + sub; i < e; i += 8) {
+            const uint32_t c = cols[i];
+            if (RD) {
+                const double v = vals_r[i];
+#pragma unroll
+                for (int j = 0; j < NR; ++j) {
+                    const double2 x = f[(size_t)cs.idx[j] * ldf + c];
+                    ar[j] = fma(v, x.x, ar[j]);
+                    ai[j] = fma(v, x.y, ai[j]);
+                }
+            } else {
+                const double2 v = vals[i];
+#pragma unroll
+                for (int j = 0; j < NR; ++j) {
+                    const double2 x = f[(size_t)cs.idx[j] * ldf + c];
+                    ar[j] = fma(v.x, x.x, ar[j]);
+                    ar[j] = fma(-v.y, x.y, ar[j]);
+                    ai[j] = fma(v.x, x.y, ai[j]);
+                    ai[j] = fma(v.y, x.x, ai[j]);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NR; ++j)
+#pragma unroll
+        for (int o = 4; o; o >>= 1) {
+            ar[j] += __shfl_xor_sync(0xffffffffu, ar[j], o);
+            ai[j] += __shfl_xor_sync(0xffffffffu, ai[j], o);
+        }
+    if (r < rows && sub == 0)
+#pragma unroll
+        for (int j = 0; j < NR; ++j) qs[(size_t)cs.idx[j] * ldq + r] = make_double2(ar[j], ai[j]);
+}
+
+template <int NR>
+static void spmm_nr(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double2* vals,
+                    const double* vals_r, const double2* f, uint64_t ldf, double2* qs, uint64_t ldq,
+                    const SpmmCols& cs, cudaStream_t st) {
+    if (vals_r)
+        k_spmm<NR, true><<<blocks(rows * 8, 256), 256, 0, st>>>(rows, ro, cols, vals, vals_r, f, ldf, qs, ldq, cs);
+    else
+        k_spmm<NR, false><<<blocks(rows * 8, 256), 256, 0, st>>>(rows, ro, cols, vals, vals_r, f, ldf, qs, ldq, cs);
+}
+
+void launch_spmm(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double2* vals,
+                 const double* vals_r, const double2* f, uint64_t ldf, double2* qs, uint64_t ldq,
+                 const SpmmCols& cs, cudaStream_t st) {
+    if (!rows || !cs.n) return;
+    switch (cs.n) {
+        case 1: spmm_nr<1>(rows, ro, cols, vals, vals_r, f, ldf, qs, ldq, cs, st); break;
+        case 2: spmm_nr<2>(rows, ro, cols, vals, vals_r, f, ldf, qs, ldq, cs, st); break;
+        case 3: spmm_nr<3>(rows, ro, cols, vals, vals_r, f, ldf, qs, ldq, cs, st); break;
+        case 4: spmm_nr<4>(rows, ro, cols, vals, vals_r, f, ldf, qs, ldq, cs, st); break;
+        case 5: spmm_nr<5>(rows, ro, cols, vals, vals_r, f, ldf, qs, ldq, cs, st); break;
+        case 6: spmm_nr<6>(rows, ro, cols, vals, vals_r, f, ldf, qs, ldq, cs, st); break;
+        case 7: spmm_nr<7>(rows, ro, cols, vals, vals_r, f, ldf, qs, ldq, cs, st); break;
+        default: spmm_nr<8>(rows, ro, cols, vals, vals_r, f, ldf, qs, ldq, cs, st); break;
+    }
+    count_launch();
+    ck(cudaGetLastError(), "k_spmm");
+}
+
 void launch_spmv_vec_real(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double* vals,
                           const double2* f, double2* qs, cudaStream_t st) {
     if (!rows) return;

@@ -493,10 +493,52 @@ struct sbd_op {
     // conv_operator.cpp:301-309 on device buffers, one right-hand side.
     // real_hint: 1 = f is real, 0 = complex, -1 = unknown (checked on the
     // device when the Hermitian-FFT mode could use it)
-    void apply_one(const double2* f, double2* q, cudaStream_t st, int real_hint = -1) {
+    // real f for the half split / Re(D): 1, 0, or -1 (decide on the device)
+    bool decide_real(const double2* f, int real_hint, cudaStream_t st) {
+        return herm_ok && (real_hint == 1 || (real_hint < 0 && device_real(f, d.n_src(), st)));
+    }
+
+    // Batched right-hand sides: D f for all columns in one
+    // pass over D (k_spmm: the values and columns are read once for up to 8
+    // right-hand sides), then the far field per column with qs_pre as addend.
+    DevBuf<double2> fs_all, qs_all;
+    void apply_batch(const double2* f, double2* q, int nrhs, cudaStream_t st, const int* real_hint) {
+        const uint64_t ns = d.n_src(), nt = d.n_tgt();
+        std::vector<int> real(nrhs);
+        for (int r = 0; r < nrhs; ++r)
+            real[r] = decide_real(f + (size_t)r * ns, real_hint ? real_hint[r] : -1, st) ? 1 : 0;
+        if (fs_all.n < ns * nrhs) fs_all.alloc(ns * nrhs);
+        if (qs_all.n < nt * nrhs) qs_all.alloc(nt * nrhs);
+        for (int r = 0; r < nrhs; ++r)
+            launch_gather(f + (size_t)r * ns, fwd_in->perm_t.p, fs_all.p + (size_t)r * ns, ns, st);
+        if (tm.on) tm.start("spmv");
+        for (int pass = 0; pass < 2; ++pass) {  // real columns (Re(D) when kept), then the others
+            const bool rd = pass == 0 && vals_sr.n;
+            SpmmCols cs;
+            auto flush = [&]() {
+                if (!cs.n) return;
+                launch_spmm(nt, ro_s.p, cols_s.p, vals_s.p, rd || !vals_s.n ? vals_sr.p : nullptr, fs_all.p, ns,
+                            qs_all.p, nt, cs, st);
+                cs.n = 0;
+            };
+            for (int r = 0; r < nrhs; ++r) {
+                const bool mine = pass == 0 ? (real[r] && vals_sr.n) : !(real[r] && vals_sr.n);
+                if (!mine) continue;
+                cs.idx[cs.n++] = r;
+                if (cs.n == kSpmmMax) flush();
+            }
+            flush();
+        }
+        if (tm.on) tm.stop();
+        for (int r = 0; r < nrhs; ++r)
+            apply_one(f + (size_t)r * ns, q + (size_t)r * nt, st, real[r], qs_all.p + (size_t)r * nt);
+    }
+
+    void apply_one(const double2* f, double2* q, cudaStream_t st, int real_hint = -1,
+                   const double2* qs_pre = nullptr) {
         if (fused) {
             HermArgs hin, hout;
-            const bool real_f = herm_ok && (real_hint == 1 || (real_hint < 0 && device_real(f, d.n_src(), st)));
+            const bool real_f = decide_real(f, real_hint, st);
             const bool hfft_now = hfft_ok && real_f;
             if (herm_ok) {
                 ck(cudaMemsetAsync(herm_flag.p, 1, sizeof(int), st), "half flag");
@@ -521,7 +563,9 @@ struct sbd_op {
             // spread and the second FFT (measured: no gain on config 4 -- the
             // overlapped kernels slow down by the CSR pass's time)
             static const bool overlap = std::getenv("SBD_OVERLAP") != nullptr;
-            if (!overlap) {
+            if (qs_pre) {
+                // D f already formed by the batched pass
+            } else if (!overlap) {
                 if (tm.on) tm.start("spmv");
                 spmv_sorted(0, d.n_tgt(), st, real_f);
                 if (tm.on) tm.stop();
@@ -540,8 +584,9 @@ struct sbd_op {
                 wait = ev_qs;
             }
             // q = NUFFT+(spectrum) + D f, scattered to the caller's target order
-            fwd_out->apply_pruned(spec.p, true, nullptr, q, nullptr, qs.p, work, st, &tm, "spread_xi",
-                                  "fft_out", "interp_tgt", 0, ~0ull, 0, ~0ull, herm_ok ? &hout : nullptr, wait);
+            fwd_out->apply_pruned(spec.p, true, nullptr, q, nullptr, qs_pre ? qs_pre : qs.p, work, st, &tm,
+                                  "spread_xi", "fft_out", "interp_tgt", 0, ~0ull, 0, ~0ull,
+                                  herm_ok ? &hout : nullptr, wait);
             return;
         }
         fwd_in->apply(f, spec.p, work, st, &tm, w_in.p, "spread_src", "fft_in", "interp_xi");
@@ -623,7 +668,7 @@ struct sbd_op {
 
     size_t device_bytes() const {
         return fwd_in->device_bytes() + fwd_out->device_bytes() + w_sorted.bytes() + w_in.bytes() + ro.bytes() +
-               ro_s.bytes() + cols_s.bytes() + vals_s.bytes() + vals_sr.bytes() + kappa.bytes() + f_sorted.bytes() +
+               ro_s.bytes() + cols_s.bytes() + vals_s.bytes() + vals_sr.bytes() + fs_all.bytes() + qs_all.bytes() + kappa.bytes() + f_sorted.bytes() +
                qs.bytes() + work.bbuf.bytes() +
                cols.bytes() + vals.bytes() + work.grid.bytes() + work.T.bytes() + work.band.bytes() +
                spec.bytes() + hf.bytes() + hq.bytes() + kappa_h.bytes();
@@ -822,9 +867,14 @@ static void apply_device_rhs(sbd_op* op, const double* d_f, double* d_q, int nrh
     op->tm.stream = st;
     const auto* f = reinterpret_cast<const double2*>(d_f);
     auto* q = reinterpret_cast<double2*>(d_q);
-    for (int r = 0; r < nrhs; ++r)
-        op->apply_one(f + (size_t)r * op->d.n_src(), q + (size_t)r * op->d.n_tgt(), st,
-                      real_hint ? real_hint[r] : -1);
+    static const bool no_spmm = std::getenv("SBD_NO_SPMM") != nullptr;
+    if (op->fused && nrhs > 1 && !no_spmm) {
+        op->apply_batch(f, q, nrhs, st, real_hint);
+    } else {
+        for (int r = 0; r < nrhs; ++r)
+            op->apply_one(f + (size_t)r * op->d.n_src(), q + (size_t)r * op->d.n_tgt(), st,
+                          real_hint ? real_hint[r] : -1);
+    }
     ck(cudaGetLastError(), "apply");
 }
 

@@ -420,6 +420,17 @@ void launch_spmv_vec(uint64_t rows, const uint64_t* ro, const uint32_t* cols, co
                      const double2* f, double2* qs, cudaStream_t st);
 void launch_spmv_vec_real(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double* vals,
                           const double2* f, double2* qs, cudaStream_t st);
+// D' times up to kSpmmMax right-hand sides in one pass over D': column j of
+// the set is f + idx[j] * ldf -> qs + idx[j] * ldq. vals_r (Re(D')) replaces
+// vals when given.
+constexpr int kSpmmMax = 8;
+struct SpmmCols {
+    int n = 0;
+    int idx[kSpmmMax] = {};
+};
+void launch_spmm(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double2* vals,
+                 const double* vals_r, const double2* f, uint64_t ldf, double2* qs, uint64_t ldq,
+                 const SpmmCols& cs, cudaStream_t st);
 void sort_by_key(uint32_t* keys, uint32_t* vals, uint64_t n, cudaStream_t st);
 void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st);
 template <typename T>
