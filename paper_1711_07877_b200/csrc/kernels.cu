@@ -1325,49 +1325,52 @@ constexpr int kITW = 6;  // warps per CTA sharing one staged block
 template <int W, bool TRANS>
 struct ITile {
     static constexpr int E = kIT + W - 1;  // footprint edge
-    static constexpr int RE = E + 7;       // rows incl. the zero rows an 8-row MMA slice may touch
-    static constexpr int CE = E + 3;       // cols incl. the zero cols a 4-col MMA slice may touch
-    // [col][row] (TRANS) or [row][col] layout, pitch chosen so the 8 x 4 cell
-    // reads of one quarter-warp hit distinct 16-byte bank groups
+    static constexpr int RE = E + 3;       // rows incl. the zero rows a 4-row MMA slice may touch
+    static constexpr int CE = E + 7;       // cols incl. the zero cols an 8-col MMA slice may touch
+    // [col][row] (TRANS) or [row][col] layout, pitch chosen so the 4-row x
+    // 8-col B-fragment reads of one quarter-warp hit distinct 16-byte bank groups
     static constexpr int ext = TRANS ? RE : CE;
-    static constexpr int mod = TRANS ? 2 : 4;
+    static constexpr int mod = TRANS ? 4 : 2;
     static constexpr int P = ext + ((mod - ext % 8) + 8) % 8;
     static constexpr int cells = (TRANS ? CE : RE) * P;
     static constexpr size_t smem = (size_t)cells * sizeof(double2) + 2 * kITW * 32 * W * sizeof(double);
     __device__ static int at(int r, int c) { return TRANS ? c * P + r : r * P + c; }
 };
 
-template <int W, bool TRANS, int NRT, int NCT>
-__device__ __forceinline__ void mma_group_s(const double2* __restrict__ S, int rl, int cl, int gid,
-                                            int kq, const double* wys, int nb, int jyl,
-                                            const double* wxs, int na, int jxl0, int jxl1,
-                                            double& p0r, double& p0i, double& p1r, double& p1i) {
+// One 8-output group on the tensor cores, rows contracted first:
+//   C[node][col] = sum_row Wx[node][row] S[row][col]  (m8n8k4: m = node,
+//   k = 4 rows, n = 8 cols; NRC row chunks x NC8 column tiles), then each lane
+//   weights its two columns by Wy and the four lanes of a node reduce.
+// Lane (gid, kq) ends with a partial of output `node` = o8 + gid.
+template <int W, bool TRANS, int NRC, int NC8>
+__device__ __forceinline__ void mma_group_t(const double2* __restrict__ S, int rl, int cl, int gid, int kq,
+                                            const double* wxs, const double* wys, int node, int jx0, int jy0,
+                                            double& pr, double& pi) {
     using TT = ITile<W, TRANS>;
-    double hr[NRT][2], hi[NRT][2];
+    double hr[NC8][2], hi[NC8][2];
 #pragma unroll
-    for (int t = 0; t < NRT; ++t) hr[t][0] = hr[t][1] = hi[t][0] = hi[t][1] = 0.0;
+    for (int t = 0; t < NC8; ++t) hr[t][0] = hr[t][1] = hi[t][0] = hi[t][1] = 0.0;
 #pragma unroll
-    for (int c = 0; c < NCT; ++c) {
-        const int cc = cl + 4 * c + kq;
-        const int jb = cc - jyl;
-        const double b = (unsigned)jb < (unsigned)W ? wys[nb * W + jb] : 0.0;
+    for (int c = 0; c < NRC; ++c) {
+        const int row = rl + 4 * c + kq;
+        const int ix = row - jx0;
+        const double a = (unsigned)ix < (unsigned)W ? wxs[node * W + ix] : 0.0;
 #pragma unroll
-        for (int t = 0; t < NRT; ++t) {
-            const double2 a = S[TT::at(rl + 8 * t + gid, cc)];
-            dmma(hr[t][0], hr[t][1], a.x, b);
-            dmma(hi[t][0], hi[t][1], a.y, b);
+        for (int t = 0; t < NC8; ++t) {
+            const double2 b = S[TT::at(row, cl + 8 * t + gid)];
+            dmma(hr[t][0], hr[t][1], a, b.x);
+            dmma(hi[t][0], hi[t][1], a, b.y);
         }
     }
 #pragma unroll
-    for (int t = 0; t < NRT; ++t) {
-        const int row = rl + 8 * t + gid;
-        const int i0 = row - jxl0, i1 = row - jxl1;
-        const double w0 = (unsigned)i0 < (unsigned)W ? wxs[na * W + i0] : 0.0;
-        const double w1 = (unsigned)i1 < (unsigned)W ? wxs[(na + 1) * W + i1] : 0.0;
-        p0r = fma(hr[t][0], w0, p0r);
-        p0i = fma(hi[t][0], w0, p0i);
-        p1r = fma(hr[t][1], w1, p1r);
-        p1i = fma(hi[t][1], w1, p1i);
+    for (int t = 0; t < NC8; ++t) {
+        const int j0 = cl + 8 * t + 2 * kq - jy0;
+        const double w0 = (unsigned)j0 < (unsigned)W ? wys[node * W + j0] : 0.0;
+        const double w1 = (unsigned)(j0 + 1) < (unsigned)W ? wys[node * W + j0 + 1] : 0.0;
+        pr = fma(hr[t][0], w0, pr);
+        pr = fma(hr[t][1], w1, pr);
+        pi = fma(hi[t][0], w0, pi);
+        pi = fma(hi[t][1], w1, pi);
     }
 }
 
@@ -1482,22 +1485,18 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
                     cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
                 }
                 if (rmax < rmin) break;
-                const int nb = o8 + gid;
-                const int jyl = jys[nb];
-                const int na = o8 + 2 * kq;
-                const int jxl0 = jxs[na], jxl1 = jxs[na + 1];
-                double p0r = 0.0, p0i = 0.0, p1r = 0.0, p1i = 0.0;
-                const int nrt = (rmax - rmin + 7) >> 3, nct = (cmax - cmin + 3) >> 2;
-                const int shape = (nrt <= 3 && nct <= 6 && nct >= 3) ? (nrt - 1) * 4 + (nct - 3) : -1;
-#define SBD_MMA_CASE(R, C)                                                                         \
-    case (R - 1) * 4 + (C - 3):                                                                    \
-        mma_group_s<W, TRANS, R, C>(S, rmin, cmin, gid, kq, wys, nb, jyl, wxs, na, jxl0, jxl1, p0r, \
-                                    p0i, p1r, p1i);                                                \
+                const int node = o8 + gid;
+                const int jxn = jxs[node], jyn = jys[node];
+                double pr = 0.0, pi = 0.0;
+                const int nrc = (rmax - rmin + 3) >> 2, nc8 = (cmax - cmin + 7) >> 3;
+                const int shape = (nrc >= 3 && nrc <= 6 && nc8 >= 2 && nc8 <= 3) ? (nrc - 3) * 2 + (nc8 - 2) : -1;
+#define SBD_MMA_CASE(R, C)                                                                              \
+    case (R - 3) * 2 + (C - 2):                                                                         \
+        mma_group_t<W, TRANS, R, C>(S, rmin, cmin, gid, kq, wxs, wys, node, jxn, jyn, pr, pi);          \
         break;
                 switch (shape) {
-                    SBD_MMA_CASE(1, 3) SBD_MMA_CASE(1, 4) SBD_MMA_CASE(1, 5) SBD_MMA_CASE(1, 6)
-                    SBD_MMA_CASE(2, 3) SBD_MMA_CASE(2, 4) SBD_MMA_CASE(2, 5) SBD_MMA_CASE(2, 6)
-                    SBD_MMA_CASE(3, 3) SBD_MMA_CASE(3, 4) SBD_MMA_CASE(3, 5) SBD_MMA_CASE(3, 6)
+                    SBD_MMA_CASE(3, 2) SBD_MMA_CASE(3, 3) SBD_MMA_CASE(4, 2) SBD_MMA_CASE(4, 3)
+                    SBD_MMA_CASE(5, 2) SBD_MMA_CASE(5, 3) SBD_MMA_CASE(6, 2) SBD_MMA_CASE(6, 3)
                     default: {
                         // wide group: four lanes per output (rows part, part + 4, ...),
                         // reduced over the four, from the staged tile
@@ -1534,20 +1533,16 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
                 }
 #undef SBD_MMA_CASE
                 if (shape >= 0) {
-#pragma unroll
-                    for (int o = 4; o <= 16; o <<= 1) {
-                        p0r += __shfl_xor_sync(0xffffffffu, p0r, o);
-                        p0i += __shfl_xor_sync(0xffffffffu, p0i, o);
-                        p1r += __shfl_xor_sync(0xffffffffu, p1r, o);
-                        p1i += __shfl_xor_sync(0xffffffffu, p1i, o);
-                    }
-                    // lanes kq = 0..3 now hold outputs o8 + 2 kq (+1): hand them to the owners
-                    const int src = (lane & 7) >> 1;
-                    const double r0 = __shfl_sync(0xffffffffu, p0r, src), i0 = __shfl_sync(0xffffffffu, p0i, src);
-                    const double r1 = __shfl_sync(0xffffffffu, p1r, src), i1 = __shfl_sync(0xffffffffu, p1i, src);
+                    // the four lanes of each node, then lanes 4k hold output o8 + k
+                    pr += __shfl_xor_sync(0xffffffffu, pr, 1);
+                    pi += __shfl_xor_sync(0xffffffffu, pi, 1);
+                    pr += __shfl_xor_sync(0xffffffffu, pr, 2);
+                    pi += __shfl_xor_sync(0xffffffffu, pi, 2);
+                    pr = __shfl_sync(0xffffffffu, pr, (lane & 7) << 2);
+                    pi = __shfl_sync(0xffffffffu, pi, (lane & 7) << 2);
                     if ((lane >> 3) == grp) {
-                        accr = (lane & 1) ? r1 : r0;
-                        acci = (lane & 1) ? i1 : i0;
+                        accr = pr;
+                        acci = pi;
                     }
                 }
             }
