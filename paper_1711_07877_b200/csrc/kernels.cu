@@ -1475,16 +1475,18 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
                 const int e = lane & 7;
                 const int jxe = jxs[o8 + e], jye = jys[o8 + e];
                 const bool real = jxe != (1 << 28);
-                int rmin = real ? jxe : 1 << 29, rmax = real ? jxe + W : -(1 << 29);
-                int cmin = real ? jye : 1 << 29, cmax = real ? jye + W : -(1 << 29);
+                // group bounding box: (row, col) starts packed in 16-bit halves
+                // (tile-local, < 2^15), min/max by SIMD-in-word over 8 lanes
+                unsigned lo = real ? ((unsigned)jxe << 16) | (unsigned)jye : 0xffffffffu;
+                unsigned hi = real ? ((unsigned)(jxe + W) << 16) | (unsigned)(jye + W) : 0u;
 #pragma unroll
                 for (int o = 1; o <= 4; o <<= 1) {
-                    rmin = min(rmin, __shfl_xor_sync(0xffffffffu, rmin, o));
-                    rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
-                    cmin = min(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
-                    cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+                    lo = __vminu2(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+                    hi = __vmaxu2(hi, __shfl_xor_sync(0xffffffffu, hi, o));
                 }
-                if (rmax < rmin) break;
+                if (hi == 0u) break;
+                const int rmin = (int)(lo >> 16), cmin = (int)(lo & 0xffffu);
+                const int rmax = (int)(hi >> 16), cmax = (int)(hi & 0xffffu);
                 const int node = o8 + gid;
                 const int jxn = jxs[node], jyn = jys[node];
                 double pr = 0.0, pi = 0.0;
