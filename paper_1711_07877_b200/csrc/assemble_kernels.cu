@@ -13,6 +13,8 @@
 // which is what makes its offline stage take hours at N = 1e7): the omega-hat
 // spectrum is spread once onto a small grid, transformed once, and each pair's
 // difference is formed on the fly and interpolated (k_close_values).
+#include <cstdlib>
+#include <cstdio>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -302,7 +304,8 @@ void build_close_matrix_gpu(const CloseMatrixInput& in, CloseMatrixOutput& out) 
     count_launch();
     exclusive_scan(counts.p, ro.p, nt + 1, st);
     uint64_t nnz = 0;
-    ck(cudaMemcpy(&nnz, ro.p + nt, 8, cudaMemcpyDeviceToHost), "nnz");
+    ck(cudaMemcpyAsync(&nnz, ro.p + nt, 8, cudaMemcpyDeviceToHost, st), "nnz");
+    ck(cudaStreamSynchronize(st), "nnz sync");
     DevBuf<uint32_t> cols(std::max<uint64_t>(nnz, 1)), row(std::max<uint64_t>(nnz, 1));
     if (nnz) {
         k_pairs<true><<<nblk(nt, 128), 128, 0, st>>>(tgt.p, nt, src_sorted.p, idx.p, cstart.p, g, r2,
@@ -325,12 +328,15 @@ void build_close_matrix_gpu(const CloseMatrixInput& in, CloseMatrixOutput& out) 
     // ---- far field at every pair difference (conv_operator.cpp:186-206)
     DevBuf<unsigned long long> ext(4);
     const unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
-    ck(cudaMemcpy(ext.p, init, sizeof(init), cudaMemcpyHostToDevice), "ext init");
+    // st is non-blocking: every host transfer goes through st (a legacy-stream
+    // cudaMemcpy would not wait for the kernels queued on st)
+    ck(cudaMemcpyAsync(ext.p, init, sizeof(init), cudaMemcpyHostToDevice, st), "ext init");
     k_diff_extrema<<<std::min<uint64_t>(nblk(nnz, 256), 148 * 8), 256, 0, st>>>(tgt.p, src.p, row.p, cols.p,
                                                                              nnz, in.single, ext.p);
     count_launch();
     unsigned long long he[4];
-    ck(cudaMemcpy(he, ext.p, sizeof(he), cudaMemcpyDeviceToHost), "ext D2H");
+    ck(cudaMemcpyAsync(he, ext.p, sizeof(he), cudaMemcpyDeviceToHost, st), "ext D2H");
+    ck(cudaStreamSynchronize(st), "ext sync");
     auto unord = [](unsigned long long u) {
         const unsigned long long b = (u >> 63) ? (u & 0x7fffffffffffffffull) : ~u;
         double d;
@@ -344,7 +350,7 @@ void build_close_matrix_gpu(const CloseMatrixInput& in, CloseMatrixOutput& out) 
     }
     DevBuf<double2> vals(nnz);
     DevBuf<int> bad(1);
-    ck(cudaMemset(bad.p, 0, 4), "memset");
+    ck(cudaMemsetAsync(bad.p, 0, 4, st), "memset");
     const double2 diag = make_double2(-in.wsum_re, -in.wsum_im);
     NufftOpts o;
     o.tol = in.nufft_tol;
@@ -353,6 +359,15 @@ void build_close_matrix_gpu(const CloseMatrixInput& in, CloseMatrixOutput& out) 
     o.max_grid_bytes = in.max_grid_bytes;
     // Plan(xi, {box corners}, +): same geometry as a plan over all differences.
     Plan far(in.xi_xy, in.n_xi, corners, 2, +1, o, in.device, true, false, st);
+    if (!(std::isfinite(corners[0]) && std::isfinite(corners[1]) && std::isfinite(corners[2]) &&
+          std::isfinite(corners[3])))
+        throw Error(3, "assemble: pair-difference extent is not finite");
+    if (std::getenv("SBD_VERBOSE"))
+        std::fprintf(stderr, "[sbd] far plan: fast %d n %d x %d w %d gamma %.6g %.6g center %.6g %.6g fcenter %.6g %.6g "
+                             "corners %.6g %.6g %.6g %.6g nnz %llu n_xi %llu\n",
+                     (int)far.fast, far.ax.n, far.ay.n, far.w, far.ax.gamma, far.ay.gamma, far.ax.center, far.ay.center,
+                     far.ax.fcenter, far.ay.fcenter, corners[0], corners[1], corners[2], corners[3],
+                     (unsigned long long)nnz, (unsigned long long)in.n_xi);
     if (far.fast) {
         DevBuf<double2> grid(far.cells());
         DevBuf<double2> w;

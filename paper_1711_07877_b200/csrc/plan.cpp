@@ -127,7 +127,7 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
         ck(cudaMemcpyAsync(he, ext.p, sizeof(he), cudaMemcpyDeviceToHost, st), "extent D2H");
         ck(cudaStreamSynchronize(st), "extent");
         pruned = sort_points && np > 0 && he[0] >= 0 && he[1] + w <= ax.n && he[2] >= 0 &&
-                 he[3] + w <= ay.n;
+                 he[3] + w <= ay.n && !std::getenv("SBD_NO_PRUNE");
         if (pruned) {
             const char* env = std::getenv("SBD_TILE_ROWS");
             tg.tr = (env && std::atoi(env) == 8) ? 8 : 16;
@@ -798,6 +798,7 @@ std::vector<uint32_t> Plan::adopt_point_order(cudaStream_t st) {
     if (!fast) {
         // direct path keeps raw points; reorder them to match
         std::vector<double2> raw(np), sorted(np);
+        ck(cudaStreamSynchronize(st), "pts sync");  // st is non-blocking
         ck(cudaMemcpy(raw.data(), pts.p, np * 16, cudaMemcpyDeviceToHost), "pts D2H");
         for (uint64_t i = 0; i < np; ++i) sorted[i] = raw[h[i]];
         pts.upload(sorted.data(), np, st);
