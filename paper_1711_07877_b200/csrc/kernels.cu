@@ -609,10 +609,11 @@ struct SCta {
     static constexpr size_t smem = (size_t)NP * L * (sizeof(double2) + sizeof(double)) +
                                    (size_t)kSCQ * 2 * sizeof(double2) + (size_t)16 * LS * 4 +
                                    (size_t)2 * kSCB * 4;
+    static constexpr size_t smem_list = smem - (size_t)kSCQ * 2 * sizeof(double2);  // LIST: no ring
 };
 
 template <int W, bool CPLX, bool LIST>
-__global__ void __launch_bounds__(128, 7) k_spread_cta(WindowPoly P, GridGeom g, TileGeom tg,
+__global__ void __launch_bounds__(128, LIST ? 8 : 7) k_spread_cta(WindowPoly P, GridGeom g, TileGeom tg,
                                                      const uint32_t* __restrict__ bin_start,
                                                      const double2* __restrict__ bsorted,
                                                      const double2* __restrict__ pos,
@@ -624,8 +625,8 @@ __global__ void __launch_bounds__(128, 7) k_spread_cta(WindowPoly P, GridGeom g,
     extern __shared__ __align__(16) double smem_sc[];
     double2* sA = reinterpret_cast<double2*>(smem_sc);  // [NP][L]: b * x taps
     double2* sQt = sA + S::NP * L;                       // queued positions (16-byte aligned)
-    double2* sQb = sQt + kSCQ;                           // queued coefficients
-    double* sB = reinterpret_cast<double*>(sQb + kSCQ);  // [NP][L]: y taps
+    double2* sQb = sQt + (LIST ? 0 : kSCQ);              // queued coefficients (scan mode only)
+    double* sB = reinterpret_cast<double*>(sQb + (LIST ? 0 : kSCQ));  // [NP][L]: y taps
     uint32_t* sL = reinterpret_cast<uint32_t*>(sB + S::NP * L);  // [4 warps][4 sub-tiles][LS]
     // per staged point: fragment row base << 4 | mask of the region's 4
     // sub-tile rows (x) / columns (y) its stencil covers
@@ -2039,13 +2040,13 @@ struct SpreadTilesRun {
                                     (int)SCta<W>::smem),
                "smem attr");
             ck(cudaFuncSetAttribute(k_spread_cta<W, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)SCta<W>::smem),
+                                    (int)SCta<W>::smem_list),
                "smem attr");
             ck(cudaFuncSetAttribute(k_spread_cta<W, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)SCta<W>::smem),
                "smem attr");
             ck(cudaFuncSetAttribute(k_spread_cta<W, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)SCta<W>::smem),
+                                    (int)SCta<W>::smem_list),
                "smem attr");
         }
         SpreadOut so;
@@ -2066,7 +2067,8 @@ struct SpreadTilesRun {
             const int nblk = ((tg.nbx + 1) / 2) * ((so.nby_run + 1) / 2);
             const bool cplx = so.mode == 0 || so.mode == 2, list = so.lists.s1 && use_cta == 1;
 #define SBD_SPREAD_CTA(C, LI) \
-    k_spread_cta<W, C, LI><<<nblk, 128, SCta<W>::smem, st>>>(P, g, tg, bs, b, pos, grid, bs2, herm, so)
+    k_spread_cta<W, C, LI><<<nblk, 128, LI ? SCta<W>::smem_list : SCta<W>::smem, st>>>(P, g, tg, bs, b, pos, \
+                                                                                       grid, bs2, herm, so)
             if (cplx && list) SBD_SPREAD_CTA(true, true);
             else if (cplx) SBD_SPREAD_CTA(true, false);
             else if (list) SBD_SPREAD_CTA(false, true);
