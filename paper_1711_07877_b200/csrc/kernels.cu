@@ -1240,7 +1240,7 @@ __global__ void __launch_bounds__(256) k_interp_real(WindowPoly P, GridGeom g, u
 // interpolates one output of the block from shared memory. The band is read
 // from L2 once per block instead of W^2 times per output.
 template <int W>
-__global__ void __launch_bounds__(128) k_interp_real_tile(
+__global__ void __launch_bounds__(128, 8) k_interp_real_tile(
     WindowPoly P, GridGeom g, const uint32_t* __restrict__ tstart, uint32_t ntiles, int shift,
     uint64_t out_lo, uint64_t n, const double2* __restrict__ pos, const double2* __restrict__ phase,
     const double* __restrict__ dxt, const double* __restrict__ dyt, const double* __restrict__ grid,
