@@ -1838,7 +1838,7 @@ __device__ __forceinline__ void dft_small(const double2 (&x)[R], double2 (&y)[R]
 // [r0, r0 + 2 nr), zero elsewhere) leave as y_s[k] (column c at c * n1 +
 // s M + k, n1 = R M) for a batched length-M column transform.
 template <int R>
-__global__ void __launch_bounds__(256) k_untangle_dif(const double2* __restrict__ T, int n2, int nr, int B,
+__global__ void __launch_bounds__(256, 5) k_untangle_dif(const double2* __restrict__ T, int n2, int nr, int B,
                                                       double2* __restrict__ Tt, int n1, int r0, int M,
                                                       const double2* __restrict__ tw) {
     __shared__ double2 so[R][8][33];
@@ -1873,7 +1873,7 @@ __global__ void __launch_bounds__(256) k_untangle_dif(const double2* __restrict_
 // columns above n2/2 their conjugate mirror) leaves as y_s[k1] at
 // k n2 + s M + k1 for a batched length-M row transform.
 template <int R>
-__global__ void __launch_bounds__(256) k_pack_dif(const double2* __restrict__ Y, int n1, int m0, int n2,
+__global__ void __launch_bounds__(256, 5) k_pack_dif(const double2* __restrict__ Y, int n1, int m0, int n2,
                                                   int b1, int B1, double2* __restrict__ Z, int M,
                                                   const double2* __restrict__ tw) {
     __shared__ double2 so[R][8][33];  // [s][k1][packed row]
