@@ -613,7 +613,7 @@ struct SCta {
 };
 
 template <int W, bool CPLX, bool LIST>
-__global__ void __launch_bounds__(128, LIST ? 8 : 7) k_spread_cta(WindowPoly P, GridGeom g, TileGeom tg,
+__global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(WindowPoly P, GridGeom g, TileGeom tg,
                                                      const uint32_t* __restrict__ bin_start,
                                                      const double2* __restrict__ bsorted,
                                                      const double2* __restrict__ pos,
