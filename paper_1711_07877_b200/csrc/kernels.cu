@@ -1840,7 +1840,8 @@ __device__ __forceinline__ void dft_small(const double2 (&x)[R], double2 (&y)[R]
 template <int R>
 __global__ void __launch_bounds__(256, 5) k_untangle_dif(const double2* __restrict__ T, int n2, int nr, int B,
                                                       double2* __restrict__ Tt, int n1, int r0, int M,
-                                                      const double2* __restrict__ tw) {
+                                                      const double2* __restrict__ tw,
+                                                      const double* __restrict__ colf) {
     __shared__ double2 so[R][8][33];
     const int c0 = blockIdx.x * 32, k0 = blockIdx.y * 8;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1858,8 +1859,15 @@ __global__ void __launch_bounds__(256, 5) k_untangle_dif(const double2* __restri
         }
     }
     dft_small<R>(x, y, tw, M);
+    // the column's deconvolution factor (exact here: the column transform does
+    // not mix columns, and the factor is even in the mode, so the mirrored
+    // negative columns the interpolation reads carry theirs too)
+    const double fc = (colf && c < B) ? __ldg(colf + c) : 1.0;
 #pragma unroll
-    for (int sI = 0; sI < R; ++sI) so[sI][w][lane] = sI ? cmul(y[sI], __ldg(tw + sI * k)) : y[sI];
+    for (int sI = 0; sI < R; ++sI) {
+        const double2 v = sI ? cmul(y[sI], __ldg(tw + sI * k)) : y[sI];
+        so[sI][w][lane] = make_double2(v.x * fc, v.y * fc);
+    }
     __syncthreads();
     const int kl = threadIdx.x & 7;
     for (int p = threadIdx.x >> 3; p < 32 * R; p += 32) {
@@ -2471,16 +2479,16 @@ void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int 
 }
 
 void launch_untangle_dif(const double2* T, int n2, int nr, int B, double2* Tt, int n1, int r0, int R,
-                        const double2* tw, cudaStream_t st) {
+                        const double2* tw, cudaStream_t st, const double* colf) {
     if (nr <= 0 || B <= 0) return;
     const int M = n1 / R;
     dim3 grid((unsigned)((B + 31) / 32), (unsigned)(M / 8));
     if (R == 9)
-        k_untangle_dif<9><<<grid, 256, 0, st>>>(T, n2, nr, B, Tt, n1, r0, M, tw);
+        k_untangle_dif<9><<<grid, 256, 0, st>>>(T, n2, nr, B, Tt, n1, r0, M, tw, colf);
     else if (R == 5)
-        k_untangle_dif<5><<<grid, 256, 0, st>>>(T, n2, nr, B, Tt, n1, r0, M, tw);
+        k_untangle_dif<5><<<grid, 256, 0, st>>>(T, n2, nr, B, Tt, n1, r0, M, tw, colf);
     else if (R == 3)
-        k_untangle_dif<3><<<grid, 256, 0, st>>>(T, n2, nr, B, Tt, n1, r0, M, tw);
+        k_untangle_dif<3><<<grid, 256, 0, st>>>(T, n2, nr, B, Tt, n1, r0, M, tw, colf);
     else
         throw Error(3, "untangle_dif: unsupported radix");
     count_launch();

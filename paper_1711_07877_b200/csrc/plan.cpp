@@ -580,7 +580,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
                            reinterpret_cast<cufftDoubleComplex*>(hD.p), CUFFT_INVERSE),
               "hfft Z2Z rows");
         if (hrad > 1)
-            launch_untangle_dif(hD.p, n2, (rhi - rlo) / 2, hcols, hB.p, ax.n, rlo, hrad, htw.p, st);
+            launch_untangle_dif(hD.p, n2, (rhi - rlo) / 2, hcols, hB.p, ax.n, rlo, hrad, htw.p, st, dy_band.p);
         else
             launch_untangle_transpose(hD.p, n2, (rhi - rlo) / 2, hcols, hB.p, ax.n, rlo, st);
         ckfft(cufftSetStream(hp2, st), "cufftSetStream");
@@ -597,8 +597,9 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
             gt.rad_m = ax.n / hrad;
             gt.rad_magic = (unsigned)((0x100000000ull + hrad - 1) / hrad);
         }
-        launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx.p, dy_band.p, hC.p, perm_p, out_p, 0, 0, st,
-                      add_p, /*transposed=*/true, &otiles, hp);
+        // with the radix pass the column factors are already in the band
+        launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx.p, hrad > 1 ? nullptr : dy_band.p, hC.p, perm_p,
+                      out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles, hp);
         if (tm) tm->stop();
         return;
     }

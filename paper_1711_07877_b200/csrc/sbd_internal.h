@@ -397,7 +397,7 @@ void launch_untangle_transpose(const double2* T, int n2, int nr, int B, double2*
 // the same untangle with the radix-R (3, 5, 9) first pass of the length
 // n1 = R M column transform folded in; tw[m] = e^{+2 pi i m / n1}
 void launch_untangle_dif(const double2* T, int n2, int nr, int B, double2* Tt, int n1, int r0, int R,
-                         const double2* tw, cudaStream_t st);
+                         const double2* tw, cudaStream_t st, const double* colf = nullptr);
 // Hermitian band rows from half-plane columns -> pairs packed into full rows
 void launch_pack_rows(const double2* Y, int n1, int m0, int n2, int b1, int B1, double2* Z, cudaStream_t st);
 // the same packing with the radix-R first pass of the length n2 = R M row
