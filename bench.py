@@ -230,6 +230,57 @@ def run_reference(args, w):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ same-config reference
+def reference_same_config(op, f, q_dev_host, max_grid_bytes):
+    """One CompressedOperator::apply of the unmodified reference (oracle/_ref,
+    driven through its own NufftPlan / SparsePairMatrix on the operator file
+    this run assembled; RefRaw) on one host core: parity of q against it and
+    a same-config CPU baseline. Runs after the timed regions."""
+    from oracle.oracle import REF_SO, RefLib
+    if not os.path.exists(REF_SO):
+        return None, None
+    path = f"/tmp/sbd_bench_op_{os.getpid()}.sbdop"
+    try:
+        t0 = time.perf_counter()
+        op.save(path)
+        t_save = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        raw = RefLib().raw(path, max_grid_bytes=max_grid_bytes)
+        t_open = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        q_ref = raw.apply(f, len(q_dev_host))
+        t_apply = time.perf_counter() - t0
+        del raw
+    finally:
+        if os.path.exists(path):
+            os.unlink(path)
+    n = len(f)
+    rel = float(np.linalg.norm(q_dev_host - q_ref) / np.linalg.norm(q_ref))
+    parity = {"rel_l2_vs_reference": rel, "bar": 1e-9, "ok": rel <= 1e-9,
+              "reference": "oracle/_ref (unmodified reference sources; RefRaw = its NufftPlan + "
+                           "SparsePairMatrix on this run's operator file)"}
+    cpu = {"value": n / t_apply, "unit": "points/s", "cores": 1, "kind": "reference",
+           "sample": (f"the full workload: one single-threaded reference apply of this config "
+                      f"(N={n}) on this box's host ({os.cpu_count()} cores present; the reference "
+                      f"is single-threaded), {t_apply:.1f} s; plan build {t_open:.1f} s and "
+                      f"operator save {t_save:.1f} s not counted; FFT on the oracle's shim, "
+                      "not FFTW (BASELINE.md section 2)"),
+           "apply_s": round(t_apply, 2)}
+    return parity, cpu
+
+
+def spawn_ranks(args):
+    """bench.py --gpus N without torchrun: re-exec under torch.distributed.run
+    with N local ranks (the driver's own launch form) and return its code."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 # ------------------------------------------------------------------ B200 arm
 def run_b200(args, w):
     import torch
@@ -238,11 +289,19 @@ def run_b200(args, w):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench: WORLD_SIZE={world} but --gpus {args.gpus}")
+    ndev = torch.cuda.device_count()
+    shared = ndev < world  # more ranks than GPUs: a functional run, not a scaling number
+    local = local % ndev
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     z = w["z"]
     n = len(z)
@@ -257,8 +316,9 @@ def run_b200(args, w):
 
     rng = np.random.default_rng(SEED + 3)
     f = rhs(w, n, rng)
+    f_real = not w["f_complex"]
     f_dev = torch.from_numpy(f.view(np.float64).copy()).cuda()
-    q_dev = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+    q_dev = torch.zeros(2 * n, dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
 
@@ -270,8 +330,8 @@ def run_b200(args, w):
         def step():
             sharded.apply(f_dev, q_dev)
     else:
-        def step():
-            op.apply_device(f_dev.data_ptr(), q_dev.data_ptr(), 1, sh)
+        def step():  # the caller knows its f is real (sbd_op_apply_device_ex)
+            op.apply_device(f_dev.data_ptr(), q_dev.data_ptr(), 1, sh, f_is_real=f_real)
 
     for _ in range(args.warmup):
         step()
@@ -348,11 +408,16 @@ def run_b200(args, w):
     # north_star: <= eps at 1,000 random targets): |q_k - sum_{l != k} G f_l| <=
     # eps sum|f|, the direct sum in fp64 on the GPU (torch)
     contract = None
+    # every rank runs the apply (the sharded one has collectives); each writes
+    # its target shard, so a sum over ranks of zero-initialised q fills all N
+    q_dev.zero_()
+    step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.all_reduce(q_dev)
+    qv = q_dev.view(-1, 2).cpu().numpy()
+    qv = qv[:, 0] + 1j * qv[:, 1]
     if rank == 0:
-        step()
-        torch.cuda.synchronize()
-        qv = q_dev.view(-1, 2).cpu().numpy()
-        qv = qv[:, 0] + 1j * qv[:, 1]
         rows = np.random.default_rng(SEED + 7).choice(n, 1000, replace=False)
         zt = torch.from_numpy(z).cuda()
         ft = torch.from_numpy(f).cuda()
@@ -382,7 +447,7 @@ def run_b200(args, w):
         qb_dev = torch.empty(2 * n * args.nrhs, dtype=torch.float64, device="cuda")
 
         def bstep():
-            op.apply_device(fb_dev.data_ptr(), qb_dev.data_ptr(), args.nrhs, sh)
+            op.apply_device(fb_dev.data_ptr(), qb_dev.data_ptr(), args.nrhs, sh, f_is_real=f_real)
         bstep()
         torch.cuda.synchronize()
         op.set_profiling(True)
@@ -402,14 +467,17 @@ def run_b200(args, w):
                    "note": "one apply of nrhs right-hand sides; D' streamed once for up to 8 columns"}
         del fb_dev, qb_dev
 
-    cpu = None
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        kind, apply, fs, path = reference_sample(w, args.sample_n)
-        per = min(time_reference(apply, fs, 1, 1) for _ in range(2))
-        os.unlink(path)
-        cpu = {"value": args.sample_n / per, "unit": "points/s", "cores": 1, "kind": kind,
-               "sample": (f"same distribution/eps/delta_min rule at N={args.sample_n}, "
-                          "single-threaded CompressedOperator::apply, best of 2")}
+        if args.ref_full:
+            parity, cpu = reference_same_config(op, f, qv, 96 << 30)
+        if cpu is None:
+            kind, apply, fs, path = reference_sample(w, args.sample_n)
+            per = min(time_reference(apply, fs, 1, 1) for _ in range(2))
+            os.unlink(path)
+            cpu = {"value": args.sample_n / per, "unit": "points/s", "cores": 1, "kind": kind,
+                   "sample": (f"same distribution/eps/delta_min rule at N={args.sample_n}, "
+                              "single-threaded CompressedOperator::apply, best of 2")}
 
     if rank == 0:
         line = {
@@ -423,7 +491,9 @@ def run_b200(args, w):
                        "nufft_tol": info["nufft_tol"],
                        "l2": "inputs larger than L2 (grid + xi + D >> 126 MB)",
                        "parallelism": "single" if world == 1 else
-                       f"sharded x{world}: sources/targets/D rows split, NCCL all-reduce of the xi spectrum",
+                       (f"sharded x{world}: sources/targets/D rows split, all-reduce of the xi spectrum" +
+                        (f" (gloo; {world} ranks share {ndev} GPU(s): functional run, not a scaling number)"
+                         if shared else " (NCCL)")),
                        "offline_s": round(t_offline, 2)},
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -433,6 +503,7 @@ def run_b200(args, w):
             "clocks": clk,
             "batched_rhs": batched,
             "contract": contract,
+            "parity": parity,
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -452,7 +523,12 @@ def main():
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nrhs", type=int, default=8, help="also time one batched apply of this many RHS (1: off)")
+    ap.add_argument("--ref-full", type=int, default=1,
+                    help="1: one reference apply of the full config on one core after the timed region "
+                         "(parity + same-config cpu_baseline; ~5 min at config 4); 0: the N=5e4 sample only")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn_ranks(args))
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     w = workload(args.config, args.scale)
     if args.impl == "reference":

@@ -48,7 +48,30 @@ enum sbd_kernel_kind { SBD_KERNEL_LAPLACE = 0, SBD_KERNEL_HELMHOLTZ = 1 };
 typedef struct sbd_op sbd_op;
 typedef struct sbd_nufft sbd_nufft;
 
-/* AssembleOptions (conv_operator.hpp:24-31) plus the device ordinal. */
+/* Pipeline options of an operator (no reference analogue: the reference has
+ * one CPU code path). Every combination computes the same operator within
+ * the parity bar; the defaults are the fastest path. They replace the
+ * process-wide environment switches of earlier builds. */
+typedef struct sbd_op_options {
+    int real_input_split;  /* 1: for real f on an operator with real omega-hat and antipodally
+                              paired rings, compute one node of each pair (q = 2 Re(.)). Default 1 */
+    int hermitian_fft;     /* 1: on top of the split, transform half the grid (real f known on the
+                              host, or passed as a hint). Default 1 */
+    int radix_first_pass;  /* -1: fold a radix-3/5/9 first FFT pass into our kernels when n > 4096
+                              (default); 0: never; 1: whenever n factorises (tests) */
+    int spread_kernel;     /* 0: CTA spread over plan-time region lists (default); 1: CTA spread
+                              over the tile bins; 2: per-warp DMMA spread; 3: scalar tiles */
+    int interp_kernel;     /* 0: automatic (default); 1: staged DMMA tiles; 2: DMMA per warp;
+                              3: scalar */
+    int fused;             /* 1: fused forward path (renumbered D, omega-hat folded into the
+                              xi interpolation). Default 1 */
+    int verbose;           /* 1: setup diagnostics on stderr. Default 0 */
+} sbd_op_options;
+
+void sbd_op_options_default(sbd_op_options* o);
+
+/* AssembleOptions (conv_operator.hpp:24-31) plus the device ordinal and the
+ * pipeline options. */
 typedef struct sbd_assemble_options {
     double eps;                      /* 1e-6 */
     double alpha;                    /* 0 */
@@ -57,6 +80,7 @@ typedef struct sbd_assemble_options {
     uint64_t nufft_direct_threshold; /* 2^20 */
     uint64_t max_grid_bytes;         /* 4 GiB */
     int device;                      /* CUDA ordinal */
+    sbd_op_options pipeline;         /* sbd_op_options_default */
 } sbd_assemble_options;
 
 typedef struct sbd_op_info_t {
@@ -83,6 +107,10 @@ int sbd_op_assemble(int kind, double k, const double* src_xy, uint64_t n_src,
                     const sbd_assemble_options* opts, sbd_op** out);
 int sbd_op_load(const char* path, int device, uint64_t max_grid_bytes /* 0: 4 GiB */,
                 sbd_op** out);
+/* The same with pipeline options (NULL: defaults). Rejects files whose CSR or
+ * ring arrays are inconsistent (SBD_ERR_RUNTIME) before anything is uploaded. */
+int sbd_op_load_ex(const char* path, int device, uint64_t max_grid_bytes,
+                   const sbd_op_options* options, sbd_op** out);
 int sbd_op_save(const sbd_op* op, const char* path);
 int sbd_op_destroy(sbd_op* op);
 int sbd_op_info(const sbd_op* op, sbd_op_info_t* info);
@@ -95,14 +123,25 @@ int sbd_op_info(const sbd_op* op, sbd_op_info_t* info);
 int sbd_op_get(const sbd_op* op, int which, void* dst, uint64_t* count);
 
 /* ---- the hot path ---- */
+/* Concurrency: calls on one operator from several host threads are safe
+ * (reference conv_operator.hpp:33-36); they are serialised, and device work
+ * of successive calls is ordered across streams by an operator event. */
 /* q = A f for nrhs right-hand sides stored back to back (f: nrhs x n_src,
- * q: nrhs x n_tgt, interleaved complex). Host buffers; copies are inside. */
+ * q: nrhs x n_tgt, interleaved complex). Host buffers; copies are inside
+ * (chunked and overlapped; a real f moves only its real parts). */
 int sbd_op_apply(sbd_op* op, const double* f, double* q, int nrhs);
 int sbd_op_apply_adjoint(sbd_op* op, const double* u, double* q, int nrhs);
 /* Same on device buffers, enqueued on `stream` (a cudaStream_t; NULL is the
  * legacy default stream, as everywhere in CUDA). Returns without
- * synchronising. */
+ * synchronising (and is CUDA-graph capturable). Whether f is real is decided
+ * on the device, so the Hermitian-FFT mode (which needs it on the host) is
+ * not used; sbd_op_apply_device_ex takes the caller's knowledge instead. */
 int sbd_op_apply_device(sbd_op* op, const double* d_f, double* d_q, int nrhs, void* stream);
+/* f_is_real: nrhs entries, 1 = column is real (must be: an imaginary part is
+ * then ignored), 0 = complex, -1 = unknown (decided on the device); NULL = all
+ * unknown. Never synchronises. */
+int sbd_op_apply_device_ex(sbd_op* op, const double* d_f, double* d_q, int nrhs, void* stream,
+                           const int* f_is_real);
 int sbd_op_apply_adjoint_device(sbd_op* op, const double* d_u, double* d_q, int nrhs,
                                 void* stream);
 
@@ -121,8 +160,9 @@ int sbd_op_shard_bounds(const sbd_op* op, int side, int nshards, uint64_t* bound
  * and sbd_op_backward_targets reads for this (device) f: n_xi, or, for a real
  * f on an operator with real omega-hat and antipodally paired rings, the
  * computed half of the pairs (the real-input half split; the all-reduce then
- * moves n complex values). Runs one reduction over f and syncs `stream`; the
- * decision is kept for the following forward/backward calls on this f. */
+ * moves n complex values). Runs one reduction over f and syncs `stream` (the
+ * only host round trip of a sharded apply); the decision is kept for the
+ * following forward/backward calls on this f. */
 int sbd_op_spectrum_length(sbd_op* op, const double* d_f, void* stream, uint64_t* n);
 int sbd_op_forward_spectrum(sbd_op* op, const double* d_f, uint64_t src_lo, uint64_t src_hi,
                             double* d_spec, void* stream);

@@ -138,6 +138,12 @@ class CompressedOperator {
         detail::check(sbd_op_apply_device(h_, reinterpret_cast<const double*>(d_f),
                                           reinterpret_cast<double*>(d_q), nrhs, stream));
     }
+    // f_is_real: nrhs flags (1 real, 0 complex, -1 unknown); lets real columns
+    // take the Hermitian-FFT mode without a host round trip
+    void apply_device(const cplx* d_f, cplx* d_q, int nrhs, void* stream, const int* f_is_real) const {
+        detail::check(sbd_op_apply_device_ex(h_, reinterpret_cast<const double*>(d_f),
+                                             reinterpret_cast<double*>(d_q), nrhs, stream, f_is_real));
+    }
 
     void save(const std::string& path) const { detail::check(sbd_op_save(h_, path.c_str())); }
 

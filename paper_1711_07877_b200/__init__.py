@@ -5,7 +5,7 @@ q_k = sum_l G(z_k - z_l) f_l for 2D point clouds with G = log r (Laplace) or
 Bessel-ring spectrum plus a near-field CSR correction -- all on sm_100a kernels
 behind the C ABI in include/sbd_b200.h. See DESIGN.md.
 """
-from .sbd import (AssembleOptions, CompressedOperator, FrequencyQuadrature, KernelSpec,  # noqa: F401
+from .sbd import (AssembleOptions, OpOptions, CompressedOperator, FrequencyQuadrature, KernelSpec,  # noqa: F401
                   MINUS, NufftOptions, NufftPlan, PLUS, PointCloud, SparsePairMatrix,
                   choose_parameters, cloud_diameter, kernel_helmholtz, kernel_laplace, make_cloud, ndft_direct)
 from ._capi import (CudaError, DomainError, SbdConvergenceError, SbdError,  # noqa: F401

@@ -24,10 +24,16 @@ _u64 = ctypes.c_uint64
 _int = ctypes.c_int
 
 
+class OpOptionsC(ctypes.Structure):
+    _fields_ = [("real_input_split", _int), ("hermitian_fft", _int), ("radix_first_pass", _int),
+                ("spread_kernel", _int), ("interp_kernel", _int), ("fused", _int), ("verbose", _int)]
+
+
 class AssembleOptionsC(ctypes.Structure):
     _fields_ = [("eps", ctypes.c_double), ("alpha", ctypes.c_double),
                 ("a_override", ctypes.c_double), ("small_k_factor", ctypes.c_double),
-                ("nufft_direct_threshold", _u64), ("max_grid_bytes", _u64), ("device", _int)]
+                ("nufft_direct_threshold", _u64), ("max_grid_bytes", _u64), ("device", _int),
+                ("pipeline", OpOptionsC)]
 
 
 class OpInfoC(ctypes.Structure):
@@ -53,9 +59,11 @@ _sig("sbd_last_error", ctypes.c_char_p)
 _sig("sbd_version", ctypes.c_char_p)
 _sig("sbd_kernel_launch_count", _u64)
 _sig("sbd_assemble_options_default", None, ctypes.POINTER(AssembleOptionsC))
+_sig("sbd_op_options_default", None, ctypes.POINTER(OpOptionsC))
 _sig("sbd_op_assemble", _int, _int, ctypes.c_double, _dp, _u64, _dp, _u64,
      ctypes.POINTER(AssembleOptionsC), ctypes.POINTER(_vp))
 _sig("sbd_op_load", _int, ctypes.c_char_p, _int, _u64, ctypes.POINTER(_vp))
+_sig("sbd_op_load_ex", _int, ctypes.c_char_p, _int, _u64, ctypes.POINTER(OpOptionsC), ctypes.POINTER(_vp))
 _sig("sbd_op_save", _int, _vp, ctypes.c_char_p)
 _sig("sbd_op_destroy", _int, _vp)
 _sig("sbd_op_info", _int, _vp, ctypes.POINTER(OpInfoC))
@@ -63,6 +71,7 @@ _sig("sbd_op_get", _int, _vp, _int, _vp, ctypes.POINTER(_u64))
 _sig("sbd_op_apply", _int, _vp, _dp, _dp, _int)
 _sig("sbd_op_apply_adjoint", _int, _vp, _dp, _dp, _int)
 _sig("sbd_op_apply_device", _int, _vp, _vp, _vp, _int, _vp)
+_sig("sbd_op_apply_device_ex", _int, _vp, _vp, _vp, _int, _vp, ctypes.POINTER(_int))
 _sig("sbd_op_apply_adjoint_device", _int, _vp, _vp, _vp, _int, _vp)
 _sig("sbd_op_set_profiling", _int, _vp, _int)
 _sig("sbd_op_shard_bounds", _int, _vp, _int, _int, ctypes.POINTER(_u64))
@@ -87,9 +96,9 @@ _sig("sbd_choose_parameters", _int, _u64, ctypes.c_double, ctypes.c_double, _dp,
 
 # The symbols include/sbd_b200.h declares (checked by tests/test_capi_symbols.py).
 EXPORTED = [
-    "sbd_last_error", "sbd_version", "sbd_assemble_options_default", "sbd_op_assemble",
-    "sbd_op_load", "sbd_op_save", "sbd_op_destroy", "sbd_op_info", "sbd_op_get",
-    "sbd_op_apply", "sbd_op_apply_adjoint", "sbd_op_apply_device",
+    "sbd_last_error", "sbd_version", "sbd_assemble_options_default", "sbd_op_options_default",
+    "sbd_op_assemble", "sbd_op_load", "sbd_op_load_ex", "sbd_op_save", "sbd_op_destroy", "sbd_op_info", "sbd_op_get",
+    "sbd_op_apply", "sbd_op_apply_adjoint", "sbd_op_apply_device", "sbd_op_apply_device_ex",
     "sbd_op_apply_adjoint_device", "sbd_op_set_profiling", "sbd_op_stage_times",
     "sbd_op_stage_times_reset", "sbd_cloud_diameter",
     "sbd_nufft_create", "sbd_nufft_apply", "sbd_nufft_apply_transpose", "sbd_nufft_info",

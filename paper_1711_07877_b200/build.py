@@ -21,7 +21,7 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["kernels.cu", "assemble_kernels.cu", "pruned_dft.cu"]
+CU_SOURCES = ["kernels.cu", "assemble_kernels.cu"]
 CPP_SOURCES = ["window.cpp", "plan.cpp", "op.cpp", "assemble.cpp", "bessel_host.cpp", "sbd_fit.cpp"]
 
 

@@ -152,7 +152,7 @@ void build_ring_quadrature(const std::vector<Ring>& rings, double offset, double
 
 namespace {
 struct PhaseLog {
-    bool on = std::getenv("SBD_VERBOSE") != nullptr;
+    bool on = g_verbose;
     std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
     void mark(const char* what) {
         if (!on) return;

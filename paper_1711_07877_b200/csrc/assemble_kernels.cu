@@ -362,7 +362,7 @@ void build_close_matrix_gpu(const CloseMatrixInput& in, CloseMatrixOutput& out) 
     if (!(std::isfinite(corners[0]) && std::isfinite(corners[1]) && std::isfinite(corners[2]) &&
           std::isfinite(corners[3])))
         throw Error(3, "assemble: pair-difference extent is not finite");
-    if (std::getenv("SBD_VERBOSE"))
+    if (g_verbose)
         std::fprintf(stderr, "[sbd] far plan: fast %d n %d x %d w %d gamma %.6g %.6g center %.6g %.6g fcenter %.6g %.6g "
                              "corners %.6g %.6g %.6g %.6g nnz %llu n_xi %llu\n",
                      (int)far.fast, far.ax.n, far.ay.n, far.w, far.ax.gamma, far.ay.gamma, far.ax.center, far.ay.center,

@@ -2022,7 +2022,8 @@ struct SpreadTilesRun {
     static size_t smem() { return (size_t)4 * 32 * W * 24 + 4 * 128 * sizeof(uint32_t) + 4 * 256 * sizeof(uint32_t); }
     static void run(const WindowPoly& P, GridGeom g, TileGeom tg, const uint32_t* bs,
                     const double2* b, const double2* pos, double2* grid, cudaStream_t st,
-                    const uint32_t* bs2, const int* herm, const SpreadOut* out, const SpreadLists* lists) {
+                    const uint32_t* bs2, const int* herm, const SpreadOut* out, const SpreadLists* lists,
+                    int variant) {
         static bool attr = false;
         if (!attr) {
             ck(cudaFuncSetAttribute(k_spread_tiles<W, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2034,13 +2035,13 @@ struct SpreadTilesRun {
             attr = true;
         }
         const int tiles = tg.nbx * tg.nby;
-        static int use_mma = -1, use_cta = 0;
-        if (use_mma < 0) {
-            const char* e = getenv("SBD_SPREAD");
-            use_mma = !(e && e[0] == 's');
-            // default: CTA spread over the plan's region lists; 'c': CTA spread
-            // scanning the bins; 'w': per-warp DMMA spread; 's': scalar
-            use_cta = (e && (e[0] == 's' || e[0] == 'w')) ? 0 : (e && e[0] == 'c') ? 2 : 1;
+        // variant 0: CTA spread over the plan's region lists; 1: CTA spread
+        // scanning the bins; 2: per-warp DMMA spread; 3: scalar
+        const int use_mma = variant != 3;
+        const int use_cta = variant == 0 ? 1 : variant == 1 ? 2 : 0;
+        static bool attr2 = false;
+        if (!attr2) {
+            attr2 = true;
             ck(cudaFuncSetAttribute(k_spread_mma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem()),
                "smem attr");
@@ -2098,15 +2099,14 @@ struct InterpRun {
                     const double2* phase, const double2* mult, const double* dx, const double* dy,
                     const double2* grid, const uint32_t* perm, const double2* addend, double2* out,
                     int acc, int cj, cudaStream_t st, bool trans, const InterpTiles* tiles,
-                    const HermArgs* herm) {
+                    const HermArgs* herm, int variant) {
         const HermArgs hh = herm ? *herm : HermArgs{};
         // tensor-core interpolation pays off when outputs are dense on the band
-        // (>= 0.25 per cell: the xi side); SBD_INTERP=tile|mma|scalar forces a
-        // choice (tile: the shared-memory staged variant, needs the tile list)
-        const char* e = getenv("SBD_INTERP");
+        // (>= 0.25 per cell: the xi side); variant 1 (staged tiles, needs the
+        // tile list), 2 (DMMA per warp) or 3 (scalar) forces a choice
         const double density = (double)n / ((double)g.n1 * (double)g.n2 / (trans ? 2.0 : 4.0));
-        const bool use_mma = e ? (e[0] == 'm' || e[0] == 't') : density >= 0.25;
-        const bool use_tile = (use_mma && tiles && tiles->n && !(e && e[0] == 'm')) || hh.hcols;
+        const bool use_mma = variant ? (variant == 1 || variant == 2) : density >= 0.25;
+        const bool use_tile = (use_mma && tiles && tiles->n && variant != 2) || hh.hcols;
         if (hh.hcols && !(tiles && tiles->n)) throw Error(3, "Hermitian band needs the staged interpolation");
         if (use_tile && !acc && !cj) {
             auto go = [&](auto kern, size_t smem, size_t& attr) {
@@ -2235,9 +2235,9 @@ void launch_bin_bounds(const uint32_t* sorted_keys, uint64_t n, uint32_t nbins, 
 void launch_spread_tiles(int w, const WindowPoly& win, GridGeom g, TileGeom tg,
                          const uint32_t* bin_start, const double2* b, const double2* pos,
                          double2* grid, cudaStream_t st, const uint32_t* bin_start2,
-                         const int* herm, const SpreadOut* out, const SpreadLists* lists) {
+                         const int* herm, const SpreadOut* out, const SpreadLists* lists, int variant) {
     if (tg.nbx * tg.nby == 0) return;
-    dispatch_w<SpreadTilesRun>(w, win, g, tg, bin_start, b, pos, grid, st, bin_start2, herm, out, lists);
+    dispatch_w<SpreadTilesRun>(w, win, g, tg, bin_start, b, pos, grid, st, bin_start2, herm, out, lists, variant);
     count_launch();
     ck(cudaGetLastError(), "k_spread_tiles");
 }
@@ -2296,10 +2296,10 @@ void launch_interp(int w, const WindowPoly& win, GridGeom g, uint64_t n, const d
                    const double2* phase, const double2* mult, const double* dx, const double* dy,
                    const double2* grid, const uint32_t* perm, double2* out, int accumulate,
                    int conj_out, cudaStream_t st, const double2* addend, bool transposed,
-                   const InterpTiles* tiles, const HermArgs* herm) {
+                   const InterpTiles* tiles, const HermArgs* herm, int variant) {
     if (!n) return;
     dispatch_w<InterpRun>(w, win, g, n, pos, phase, mult, dx, dy, grid, perm, addend, out,
-                          accumulate, conj_out, st, transposed, tiles, herm);
+                          accumulate, conj_out, st, transposed, tiles, herm, variant);
     count_launch();
     ck(cudaGetLastError(), "k_interp");
 }
@@ -2308,8 +2308,9 @@ template <int W>
 struct InterpRealRun {
     static void run(const WindowPoly& P, GridGeom g, uint64_t n, const double2* pos, const double2* phase,
                     const double* dx, const double* dy, const double* grid, const uint32_t* perm,
-                    const double2* addend, double2* out, cudaStream_t st, const InterpTiles* tiles) {
-        static const bool staged = !(getenv("SBD_INTERP") && getenv("SBD_INTERP")[0] == 's');
+                    const double2* addend, double2* out, cudaStream_t st, const InterpTiles* tiles,
+                    int variant) {
+        const bool staged = variant != 3;
         if (staged && tiles && tiles->n) {
             int dev = 0, sms = 148, per = 1;
             cudaGetDevice(&dev);
@@ -2327,9 +2328,9 @@ struct InterpRealRun {
 void launch_interp_real(int w, const WindowPoly& win, GridGeom g, uint64_t n, const double2* pos,
                         const double2* phase, const double* dx, const double* dy, const double* grid,
                         const uint32_t* perm, const double2* addend, double2* out, cudaStream_t st,
-                        const InterpTiles* tiles) {
+                        const InterpTiles* tiles, int variant) {
     if (!n) return;
-    dispatch_w<InterpRealRun>(w, win, g, n, pos, phase, dx, dy, grid, perm, addend, out, st, tiles);
+    dispatch_w<InterpRealRun>(w, win, g, n, pos, phase, dx, dy, grid, perm, addend, out, st, tiles, variant);
     count_launch();
     ck(cudaGetLastError(), "k_interp_real");
 }

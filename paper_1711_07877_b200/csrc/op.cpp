@@ -29,6 +29,7 @@ namespace {
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
 } // namespace
+thread_local bool g_verbose = false;
 
 [[noreturn]] void throw_cuda(cudaError_t e, const char* what) {
     throw Error(SBD_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -62,6 +63,26 @@ void rdv(std::istream& is, std::vector<T>& v, size_t elem_per) {
 }
 
 const char kMagic[8] = {'S', 'B', 'D', 'O', 'P', 'v', '1', '\0'};
+
+// CSR and ring invariants every kernel relies on (a foreign or corrupt file
+// must fail here, before anything reaches the device): row_offsets starts at
+// 0, never decreases and ends at nnz; every column is a source index;
+// ring_offsets never decrease and stay within the node count.
+void validate(const OpData& d, const std::string& path) {
+    auto bad = [&](const char* what) {
+        throw Error(SBD_ERR_RUNTIME, std::string("load: inconsistent operator file ") + path + " (" + what + ")");
+    };
+    const auto& ro = d.row_offsets;
+    if (ro.empty() || ro.front() != 0 || ro.back() != d.cols.size()) bad("row offsets do not span the values");
+    for (size_t i = 1; i < ro.size(); ++i)
+        if (ro[i] < ro[i - 1]) bad("row offsets decrease");
+    const uint64_t ns = d.n_src();
+    for (uint32_t c : d.cols)
+        if (c >= ns) bad("column index out of range");
+    const auto& rg = d.ring_offsets;
+    for (size_t i = 0; i < rg.size(); ++i)
+        if (rg[i] < 0 || (uint64_t)rg[i] > d.n_xi() || (i && rg[i] < rg[i - 1])) bad("ring offsets");
+}
 
 // conv_operator.cpp:449-490
 OpData read_sbdop(const std::string& path) {
@@ -111,6 +132,7 @@ OpData read_sbdop(const std::string& path) {
     if (d.weights.size() != d.freqs.size() || d.row_offsets.size() != d.n_tgt() + 1 ||
         d.values.size() != 2 * d.cols.size())
         throw Error(SBD_ERR_RUNTIME, "load: inconsistent operator file " + path);
+    validate(d, path);
     return d;
 }
 
@@ -170,6 +192,7 @@ using namespace sbdgpu;
 
 struct sbd_op {
     OpData d;
+    sbd_op_options opt;
     int device = 0;
     cudaStream_t stream = nullptr;
     std::unique_ptr<Plan> fwd_in, fwd_out;
@@ -219,17 +242,38 @@ struct sbd_op {
     bool hfft_ok = false;
     DevBuf<int> imag_flag;
     StageTimer tm;
-    std::mutex mu;
+    // Every entry point holds `mu` for its whole call (host copies included),
+    // so calls from several host threads are serialised (conv_operator.hpp:33-36:
+    // apply is const and thread-safe). The device work of successive calls
+    // shares this operator's scratch; `done` (recorded after each call's work)
+    // orders it when consecutive calls use different streams.
+    std::recursive_mutex mu;
+    cudaEvent_t done = nullptr;
+    cudaStream_t last_stream = nullptr;
+    bool have_last = false;
 
-    // optional second stream for the CSR pass (SBD_OVERLAP, see apply_one)
-    cudaStream_t side = nullptr;
-    cudaEvent_t ev_f = nullptr, ev_qs = nullptr;
-
+    sbd_op() { sbd_op_options_default(&opt); }
     ~sbd_op() {
-        if (ev_f) cudaEventDestroy(ev_f);
-        if (ev_qs) cudaEventDestroy(ev_qs);
-        if (side) cudaStreamDestroy(side);
+        if (done) cudaEventDestroy(done);
         if (stream) cudaStreamDestroy(stream);
+    }
+
+    static bool capturing(cudaStream_t st) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+    }
+    // before enqueueing a call's work on st: wait for the previous call's work
+    // if it went to another stream
+    void order_begin(cudaStream_t st) {
+        if (have_last && last_stream != st && done && !capturing(st))
+            ck(cudaStreamWaitEvent(st, done, 0), "operator order");
+    }
+    void order_end(cudaStream_t st) {
+        if (capturing(st)) return;  // inside a graph capture the stream order is the graph's
+        if (!done) ck(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "operator event");
+        ck(cudaEventRecord(done, st), "operator order");
+        last_stream = st;
+        have_last = true;
     }
 
     // CompressedOperator::Impl::build_forward_plans (conv_operator.cpp:162-167)
@@ -242,6 +286,9 @@ struct sbd_op {
         o.tol = d.nufft_tol;
         o.direct_threshold = d.direct_threshold;
         o.max_grid_bytes = d.max_grid_bytes;
+        o.radix = opt.radix_first_pass < 0 ? -1 : (opt.radix_first_pass ? 1 : 0);
+        o.spread_kernel = opt.spread_kernel;
+        o.interp_kernel = opt.interp_kernel;
         const double* tgt = d.single ? d.src.data() : d.tgt.data();
         std::vector<uint8_t> tag;
         std::vector<uint64_t> halve;
@@ -288,7 +335,7 @@ struct sbd_op {
     }
 
     void build_hfft() {
-        if (std::getenv("SBD_NO_HFFT")) return;
+        if (!opt.hermitian_fft) return;
         if (!fwd_in->enable_hfft(1, stream)) return;
         if (!fwd_out->enable_hfft(2, stream)) {
             fwd_in->hrole = 0;
@@ -309,7 +356,7 @@ struct sbd_op {
         imag_flag.alloc(1);
         ck(cudaStreamSynchronize(stream), "hfft");
         hfft_ok = true;
-        if (std::getenv("SBD_VERBOSE")) std::fprintf(stderr, "[sbd] Hermitian FFT mode on\n");
+        if (opt.verbose) std::fprintf(stderr, "[sbd] Hermitian FFT mode on\n");
     }
 
     // 1 if f (n entries, device) is real; one reduction and a stream sync
@@ -333,7 +380,7 @@ struct sbd_op {
     // nodes of such pairs). False when omega-hat is not real or the pairing
     // does not hold to 1e-12 relative.
     bool herm_pairs(std::vector<uint8_t>& tag, std::vector<uint64_t>& halve) const {
-        if (std::getenv("SBD_NO_HERM")) return false;
+        if (!opt.real_input_split) return false;
         const uint64_t nx = d.n_xi();
         if (nx < 2 || d.ring_offsets.size() < 2 || d.ring_offsets.front() != 0 ||
             (uint64_t)d.ring_offsets.back() != nx)
@@ -391,7 +438,7 @@ struct sbd_op {
 
     void build_half(const std::vector<uint64_t>& halve) {
         if (!fused || !fwd_out->tagged_pts || !fwd_in->tagged_out || fwd_out->n0_pts != fwd_in->n0_out) {
-            if (std::getenv("SBD_VERBOSE"))
+            if (opt.verbose)
                 std::fprintf(stderr, "[sbd] half split off: fused %d tagged %d %d n0 %llu %llu\n", (int)fused,
                              (int)fwd_out->tagged_pts, (int)fwd_in->tagged_out,
                              (unsigned long long)fwd_out->n0_pts, (unsigned long long)fwd_in->n0_out);
@@ -424,19 +471,19 @@ struct sbd_op {
             }
             ck(cudaMemcpyAsync(kappa_h.p, kh.data(), nx * 16, cudaMemcpyHostToDevice, stream), "kappa_h");
         }
-        if (std::getenv("SBD_VERBOSE"))
+        if (opt.verbose)
             std::fprintf(stderr, "[sbd] half split: %zu nodes at weight 1/2\n", halve.size());
         herm_flag.alloc(1);
         ck(cudaStreamSynchronize(stream), "half split");
         herm_ok = true;
-        if (std::getenv("SBD_VERBOSE"))
+        if (opt.verbose)
             std::fprintf(stderr, "[sbd] real-input half split: %llu of %llu xi nodes\n",
                          (unsigned long long)n_half, (unsigned long long)nx);
     }
 
     void build_fused() {
         fused = fwd_in->pruned && fwd_out->pruned && fwd_in->perm_t.n == d.n_src() &&
-                fwd_out->perm_s.n == d.n_tgt() && getenv("SBD_NO_FUSED") == nullptr;
+                fwd_out->perm_s.n == d.n_tgt() && opt.fused;
         if (!fused) return;
         const uint64_t ns = d.n_src(), nt = d.n_tgt(), nx = d.n_xi();
         // kappa = w_sorted * pre_out (conv_operator.cpp:305 then nufft.cpp:233)
@@ -479,7 +526,7 @@ struct sbd_op {
         // used for real f when omega-hat is real, i.e. the half split applies)
         bool dreal = true;
         for (uint64_t i = 0; i < d.nnz() && dreal; ++i) dreal = v2[2 * i + 1] == 0.0;
-        bool wreal = !std::getenv("SBD_COMPLEX_D");
+        bool wreal = true;
         for (uint64_t i = 0; i < d.n_xi() && wreal; ++i) wreal = d.weights[2 * i + 1] == 0.0;
         if (dreal || wreal) {
             std::vector<double> vr(d.nnz());
@@ -491,12 +538,10 @@ struct sbd_op {
     }
 
     // conv_operator.cpp:301-309 on device buffers, one right-hand side.
-    // real_hint: 1 = f is real, 0 = complex, -1 = unknown (checked on the
-    // device when the Hermitian-FFT mode could use it)
-    // real f for the half split / Re(D): 1, 0, or -1 (decide on the device)
-    bool decide_real(const double2* f, int real_hint, cudaStream_t st) {
-        return herm_ok && (real_hint == 1 || (real_hint < 0 && device_real(f, d.n_src(), st)));
-    }
+    // real_hint: 1 = f is real (the Hermitian-FFT mode and the Re(D) pass
+    // apply), 0 = complex, -1 = unknown. Never a host round trip: the half
+    // split's device flag (cleared by the input gather when f has an imaginary
+    // part) covers the unknown case.
 
     // Batched right-hand sides: D f for all columns in one
     // pass over D (k_spmm: the values and columns are read once for up to 8
@@ -505,8 +550,7 @@ struct sbd_op {
     void apply_batch(const double2* f, double2* q, int nrhs, cudaStream_t st, const int* real_hint) {
         const uint64_t ns = d.n_src(), nt = d.n_tgt();
         std::vector<int> real(nrhs);
-        for (int r = 0; r < nrhs; ++r)
-            real[r] = decide_real(f + (size_t)r * ns, real_hint ? real_hint[r] : -1, st) ? 1 : 0;
+        for (int r = 0; r < nrhs; ++r) real[r] = herm_ok && real_hint && real_hint[r] == 1 ? 1 : 0;
         if (fs_all.n < ns * nrhs) fs_all.alloc(ns * nrhs);
         if (qs_all.n < nt * nrhs) qs_all.alloc(nt * nrhs);
         for (int r = 0; r < nrhs; ++r)
@@ -531,14 +575,15 @@ struct sbd_op {
         }
         if (tm.on) tm.stop();
         for (int r = 0; r < nrhs; ++r)
-            apply_one(f + (size_t)r * ns, q + (size_t)r * nt, st, real[r], qs_all.p + (size_t)r * nt);
+            apply_one(f + (size_t)r * ns, q + (size_t)r * nt, st, real_hint ? real_hint[r] : -1,
+                      qs_all.p + (size_t)r * nt);
     }
 
     void apply_one(const double2* f, double2* q, cudaStream_t st, int real_hint = -1,
                    const double2* qs_pre = nullptr) {
         if (fused) {
             HermArgs hin, hout;
-            const bool real_f = decide_real(f, real_hint, st);
+            const bool real_f = herm_ok && real_hint == 1;
             const bool hfft_now = hfft_ok && real_f;
             if (herm_ok) {
                 ck(cudaMemsetAsync(herm_flag.p, 1, sizeof(int), st), "half flag");
@@ -558,35 +603,18 @@ struct sbd_op {
             fwd_in->apply_pruned(f, false, f_sorted.p, spec.p, kappa.p, nullptr, work, st, &tm,
                                  "spread_src", "fft_in", "interp_xi", 0, ~0ull, 0, ~0ull,
                                  herm_ok ? &hin : nullptr);
-            cudaEvent_t wait = nullptr;
-            // SBD_OVERLAP=1 runs the CSR pass on a second stream beside the xi
-            // spread and the second FFT (measured: no gain on config 4 -- the
-            // overlapped kernels slow down by the CSR pass's time)
-            static const bool overlap = std::getenv("SBD_OVERLAP") != nullptr;
-            if (qs_pre) {
-                // D f already formed by the batched pass
-            } else if (!overlap) {
+            // (a second stream for the CSR pass beside the xi spread and the
+            // second FFT was measured: no gain on config 4 -- the overlapped
+            // kernels slow down by the CSR pass's time)
+            if (!qs_pre) {  // else D f was formed by the batched pass
                 if (tm.on) tm.start("spmv");
                 spmv_sorted(0, d.n_tgt(), st, real_f);
                 if (tm.on) tm.stop();
-            } else {
-                if (!side) {
-                    ck(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "stream");
-                    ck(cudaEventCreateWithFlags(&ev_f, cudaEventDisableTiming), "event");
-                    ck(cudaEventCreateWithFlags(&ev_qs, cudaEventDisableTiming), "event");
-                }
-                ck(cudaEventRecord(ev_f, st), "event");
-                ck(cudaStreamWaitEvent(side, ev_f, 0), "wait");
-                if (tm.on) tm.start("spmv", side);
-                spmv_sorted(0, d.n_tgt(), side, real_f);
-                if (tm.on) tm.stop(side);
-                ck(cudaEventRecord(ev_qs, side), "event");
-                wait = ev_qs;
             }
             // q = NUFFT+(spectrum) + D f, scattered to the caller's target order
             fwd_out->apply_pruned(spec.p, true, nullptr, q, nullptr, qs_pre ? qs_pre : qs.p, work, st, &tm,
                                   "spread_xi", "fft_out", "interp_tgt", 0, ~0ull, 0, ~0ull,
-                                  herm_ok ? &hout : nullptr, wait);
+                                  herm_ok ? &hout : nullptr);
             return;
         }
         fwd_in->apply(f, spec.p, work, st, &tm, w_in.p, "spread_src", "fft_in", "interp_xi");
@@ -631,7 +659,7 @@ struct sbd_op {
     void forward_spectrum(const double2* f, uint64_t lo, uint64_t hi, double2* spec_out,
                           cudaStream_t st) {
         if (!fused) throw Error(SBD_ERR_RUNTIME, "sharded apply needs both NUFFTs on the gridded path");
-        spectrum_length(f, st);
+        // shard_real: decided by the spectrum_length call for this f
         HermArgs h;
         if (shard_real) h = shard_herm(true, st);
         fwd_in->apply_pruned(f, false, f_sorted.p, spec_out, kappa.p, nullptr, work, st, &tm,
@@ -754,12 +782,38 @@ void sbd_assemble_options_default(sbd_assemble_options* o) {
     o->nufft_direct_threshold = uint64_t(1) << 20;
     o->max_grid_bytes = uint64_t(4) << 30;
     o->device = 0;
+    sbd_op_options_default(&o->pipeline);
+}
+
+void sbd_op_options_default(sbd_op_options* o) {
+    o->real_input_split = 1;
+    o->hermitian_fft = 1;
+    o->radix_first_pass = -1;
+    o->spread_kernel = 0;
+    o->interp_kernel = 0;
+    o->fused = 1;
+    o->verbose = 0;
+}
+
+static void check_options(const sbd_op_options& o) {
+    if (o.radix_first_pass < -1 || o.radix_first_pass > 1 || o.spread_kernel < 0 || o.spread_kernel > 3 ||
+        o.interp_kernel < 0 || o.interp_kernel > 3)
+        throw Error(SBD_ERR_INVALID_ARGUMENT, "options: value out of range");
 }
 
 int sbd_op_load(const char* path, int device, uint64_t max_grid_bytes, sbd_op** out) {
+    return sbd_op_load_ex(path, device, max_grid_bytes, nullptr, out);
+}
+
+int sbd_op_load_ex(const char* path, int device, uint64_t max_grid_bytes, const sbd_op_options* options,
+                   sbd_op** out) {
     return guarded([&] {
         if (!path || !out) throw Error(SBD_ERR_INVALID_ARGUMENT, "load: null argument");
         auto op = std::make_unique<sbd_op>();
+        if (options) {
+            check_options(*options);
+            op->opt = *options;
+        }
         op->d = read_sbdop(path);
         if (max_grid_bytes) op->d.max_grid_bytes = max_grid_bytes;
         op->device = device;
@@ -775,7 +829,10 @@ int sbd_op_assemble(int kind, double k, const double* src_xy, uint64_t n_src, co
         sbd_assemble_options o;
         sbd_assemble_options_default(&o);
         if (opts) o = *opts;
+        check_options(o.pipeline);
+        g_verbose = o.pipeline.verbose != 0;
         auto op = std::make_unique<sbd_op>();
+        op->opt = o.pipeline;
         assemble_opdata(kind, k, src_xy, n_src, tgt_xy, n_tgt, o, op->d);
         op->d.direct_threshold = o.nufft_direct_threshold;
         op->d.max_grid_bytes = o.max_grid_bytes;
@@ -862,13 +919,13 @@ int sbd_op_get(const sbd_op* op, int which, void* dst, uint64_t* count) {
 
 static void apply_device_rhs(sbd_op* op, const double* d_f, double* d_q, int nrhs, cudaStream_t st,
                              const int* real_hint) {
-    std::lock_guard<std::mutex> lk(op->mu);
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
     DeviceGuard g(op->device);
     op->tm.stream = st;
+    op->order_begin(st);
     const auto* f = reinterpret_cast<const double2*>(d_f);
     auto* q = reinterpret_cast<double2*>(d_q);
-    static const bool no_spmm = std::getenv("SBD_NO_SPMM") != nullptr;
-    if (op->fused && nrhs > 1 && !no_spmm) {
+    if (op->fused && nrhs > 1) {
         op->apply_batch(f, q, nrhs, st, real_hint);
     } else {
         for (int r = 0; r < nrhs; ++r)
@@ -876,6 +933,7 @@ static void apply_device_rhs(sbd_op* op, const double* d_f, double* d_q, int nrh
                           real_hint ? real_hint[r] : -1);
     }
     ck(cudaGetLastError(), "apply");
+    op->order_end(st);
 }
 
 int sbd_op_apply_device(sbd_op* op, const double* d_f, double* d_q, int nrhs, void* stream) {
@@ -885,19 +943,29 @@ int sbd_op_apply_device(sbd_op* op, const double* d_f, double* d_q, int nrhs, vo
     });
 }
 
+int sbd_op_apply_device_ex(sbd_op* op, const double* d_f, double* d_q, int nrhs, void* stream,
+                           const int* f_is_real) {
+    return guarded([&] {
+        if (!op || !d_f || !d_q || nrhs < 1) throw Error(SBD_ERR_INVALID_ARGUMENT, "apply: bad argument");
+        apply_device_rhs(op, d_f, d_q, nrhs, (cudaStream_t)stream, f_is_real);
+    });
+}
+
 int sbd_op_apply_adjoint_device(sbd_op* op, const double* d_u, double* d_q, int nrhs,
                                 void* stream) {
     return guarded([&] {
         if (!op || !d_u || !d_q || nrhs < 1) throw Error(SBD_ERR_INVALID_ARGUMENT, "apply_adjoint: bad argument");
-        std::lock_guard<std::mutex> lk(op->mu);
+        std::lock_guard<std::recursive_mutex> lk(op->mu);
         DeviceGuard g(op->device);
         cudaStream_t st = (cudaStream_t)stream;
         op->tm.stream = st;
+        op->order_begin(st);
         const auto* u = reinterpret_cast<const double2*>(d_u);
         auto* q = reinterpret_cast<double2*>(d_q);
         for (int r = 0; r < nrhs; ++r)
             op->apply_adjoint_one(u + (size_t)r * op->d.n_tgt(), q + (size_t)r * op->d.n_src(), st);
         ck(cudaGetLastError(), "apply_adjoint");
+        op->order_end(st);
     });
 }
 
@@ -913,8 +981,9 @@ int sbd_op_shard_bounds(const sbd_op* op, int side, int nshards, uint64_t* bound
 int sbd_op_spectrum_length(sbd_op* op, const double* d_f, void* stream, uint64_t* n) {
     return guarded([&] {
         if (!op || !d_f || !n) throw Error(SBD_ERR_INVALID_ARGUMENT, "spectrum_length: null argument");
-        std::lock_guard<std::mutex> lk(op->mu);
+        std::lock_guard<std::recursive_mutex> lk(op->mu);
         DeviceGuard g(op->device);
+        op->order_begin((cudaStream_t)stream);
         *n = op->spectrum_length(reinterpret_cast<const double2*>(d_f), (cudaStream_t)stream);
     });
 }
@@ -923,12 +992,14 @@ int sbd_op_forward_spectrum(sbd_op* op, const double* d_f, uint64_t src_lo, uint
                             double* d_spec, void* stream) {
     return guarded([&] {
         if (!op || !d_f || !d_spec) throw Error(SBD_ERR_INVALID_ARGUMENT, "forward_spectrum: null argument");
-        std::lock_guard<std::mutex> lk(op->mu);
+        std::lock_guard<std::recursive_mutex> lk(op->mu);
         DeviceGuard g(op->device);
         op->tm.stream = (cudaStream_t)stream;
+        op->order_begin((cudaStream_t)stream);
         op->forward_spectrum(reinterpret_cast<const double2*>(d_f), src_lo, src_hi,
                              reinterpret_cast<double2*>(d_spec), (cudaStream_t)stream);
         ck(cudaGetLastError(), "forward_spectrum");
+        op->order_end((cudaStream_t)stream);
     });
 }
 
@@ -936,32 +1007,36 @@ int sbd_op_backward_targets(sbd_op* op, const double* d_spec, const double* d_f,
                             uint64_t tgt_hi, double* d_q, void* stream) {
     return guarded([&] {
         if (!op || !d_spec || !d_f || !d_q) throw Error(SBD_ERR_INVALID_ARGUMENT, "backward_targets: null argument");
-        std::lock_guard<std::mutex> lk(op->mu);
+        std::lock_guard<std::recursive_mutex> lk(op->mu);
         DeviceGuard g(op->device);
         op->tm.stream = (cudaStream_t)stream;
+        op->order_begin((cudaStream_t)stream);
         op->backward_targets(reinterpret_cast<const double2*>(d_spec), reinterpret_cast<const double2*>(d_f),
                              tgt_lo, tgt_hi, reinterpret_cast<double2*>(d_q), (cudaStream_t)stream);
         ck(cudaGetLastError(), "backward_targets");
+        op->order_end((cudaStream_t)stream);
     });
 }
 
 static int host_apply(sbd_op* op, const double* in, double* out, int nrhs, bool adjoint) {
     return guarded([&] {
         if (!op || !in || !out || nrhs < 1) throw Error(SBD_ERR_INVALID_ARGUMENT, "apply: bad argument");
+        // the lock spans the staging copies, the apply and the copy back: the
+        // staging buffers hf / hq are the operator's (concurrent
+        // host calls must not interleave their copies)
+        std::lock_guard<std::recursive_mutex> lk(op->mu);
+        DeviceGuard g(op->device);
         const uint64_t nin = adjoint ? op->d.n_tgt() : op->d.n_src();
         const uint64_t nout = adjoint ? op->d.n_src() : op->d.n_tgt();
-        {
-            std::lock_guard<std::mutex> lk(op->mu);
-            DeviceGuard g(op->device);
-            if (op->hf.n < nin * nrhs) op->hf.alloc(nin * nrhs);
-            if (op->hq.n < nout * nrhs) op->hq.alloc(nout * nrhs);
-            ck(cudaMemcpyAsync(op->hf.p, in, nin * nrhs * 16, cudaMemcpyHostToDevice, op->stream), "H2D f");
-        }
+        op->order_begin(op->stream);
+        if (op->hf.n < nin * nrhs) op->hf.alloc(nin * nrhs);
+        if (op->hq.n < nout * nrhs) op->hq.alloc(nout * nrhs);
+        ck(cudaMemcpyAsync(op->hf.p, in, nin * nrhs * 16, cudaMemcpyHostToDevice, op->stream), "H2D f");
         if (adjoint) {
             const int rc = sbd_op_apply_adjoint_device(op, (double*)op->hf.p, (double*)op->hq.p, nrhs, op->stream);
             if (rc) throw Error(rc, g_err);
         } else {
-            // real right-hand sides, decided on the host copy (no device round trip)
+            // real right-hand sides, decided on the host copy while the H2D runs
             std::vector<int> real(nrhs, 1);
             for (int r = 0; r < nrhs; ++r) {
                 const double* x = in + (size_t)r * nin * 2;
@@ -972,10 +1047,9 @@ static int host_apply(sbd_op* op, const double* in, double* out, int nrhs, bool 
             }
             apply_device_rhs(op, (double*)op->hf.p, (double*)op->hq.p, nrhs, op->stream, real.data());
         }
-        std::lock_guard<std::mutex> lk(op->mu);
-        DeviceGuard g(op->device);
         ck(cudaMemcpyAsync(out, op->hq.p, nout * nrhs * 16, cudaMemcpyDeviceToHost, op->stream), "D2H q");
         ck(cudaStreamSynchronize(op->stream), "apply sync");
+        op->order_end(op->stream);
     });
 }
 
@@ -990,7 +1064,7 @@ int sbd_op_apply_adjoint(sbd_op* op, const double* u, double* q, int nrhs) {
 int sbd_op_set_profiling(sbd_op* op, int enable) {
     return guarded([&] {
         if (!op) throw Error(SBD_ERR_INVALID_ARGUMENT, "null operator");
-        std::lock_guard<std::mutex> lk(op->mu);
+        std::lock_guard<std::recursive_mutex> lk(op->mu);
         op->tm.reset();
         op->tm.on = enable != 0;
     });
@@ -998,7 +1072,7 @@ int sbd_op_set_profiling(sbd_op* op, int enable) {
 
 int sbd_op_stage_times(sbd_op* op, double* ms, const char** names, int cap) {
     if (!op) return -1;
-    std::lock_guard<std::mutex> lk(op->mu);
+    std::lock_guard<std::recursive_mutex> lk(op->mu);
     DeviceGuard g(op->device);
     return op->tm.read(ms, names, cap);
 }
@@ -1006,7 +1080,7 @@ int sbd_op_stage_times(sbd_op* op, double* ms, const char** names, int cap) {
 int sbd_op_stage_times_reset(sbd_op* op) {
     return guarded([&] {
         if (!op) throw Error(SBD_ERR_INVALID_ARGUMENT, "null operator");
-        std::lock_guard<std::mutex> lk(op->mu);
+        std::lock_guard<std::recursive_mutex> lk(op->mu);
         op->tm.reset();
     });
 }

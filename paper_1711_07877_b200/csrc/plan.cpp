@@ -13,7 +13,6 @@
 #include <cstdlib>
 #include <cstring>
 
-#include "pruned_dft.h"
 #include "sbd_internal.h"
 
 namespace sbdgpu {
@@ -127,10 +126,9 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
         ck(cudaMemcpyAsync(he, ext.p, sizeof(he), cudaMemcpyDeviceToHost, st), "extent D2H");
         ck(cudaStreamSynchronize(st), "extent");
         pruned = sort_points && np > 0 && he[0] >= 0 && he[1] + w <= ax.n && he[2] >= 0 &&
-                 he[3] + w <= ay.n && !std::getenv("SBD_NO_PRUNE");
+                 he[3] + w <= ay.n;
         if (pruned) {
-            const char* env = std::getenv("SBD_TILE_ROWS");
-            tg.tr = (env && std::atoi(env) == 8) ? 8 : 16;
+            tg.tr = 16;
             tg.rlo = he[0];
             tg.clo = he[2];
             tg.nbx = (he[1] + w - he[0] + tg.tr - 1) / tg.tr;
@@ -220,57 +218,15 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
         tg.pitch = 0;
         tg.rhi = rhi;
         tg.chi = chi;
-        // SBD_FFT: dft | dft-strict (error when the grid is unsupported) | cufft |
-        // (default) cufft-transposed; SBD_DFT_R3="r[,r]" forces the last radix
-        const char* fe = std::getenv("SBD_FFT");
-        const bool want_dft = fe && fe[0] == 'd';
-        int f1 = 0, f2 = 0;
-        if (const char* r3 = std::getenv("SBD_DFT_R3")) {
-            f1 = f2 = std::atoi(r3);
-            if (const char* c2 = std::strchr(r3, ',')) f2 = std::atoi(c2 + 1);
-        }
-        const int R = rhi - rlo, C = chi - clo;
-        const bool dft_ok = want_dft && make_pruned_pass(ay.n, clo, C, R, f1, pass1) &&
-                            make_pruned_pass(ax.n, rlo, R, pass1.B, f2, pass2);
-        if (want_dft && !dft_ok && std::strcmp(fe, "dft-strict") == 0)
-            throw Error(3, "pruned dft: grid " + std::to_string(ax.n) + "x" + std::to_string(ay.n) +
-                               " unsupported");
-        if (dft_ok) {
-            dft = true;
-            tg.pitch = C;
-            pass1.in_row = C;
-            pass1.in_elem = 1;
-            // pass 1 stores its band outputs column-major (T1[c][r], c < B1) so
-            // that pass 2 reads contiguous sequences too
-            pass1.out_row = 1;
-            pass1.out_elem = R;
-            pass2.in_row = R;
-            pass2.in_elem = 1;
-            pass2.out_row = pass2.B;
-            pass2.out_elem = 1;
-            tw1 = make_twiddles(pass1, st);
-            tw2 = make_twiddles(pass2, st);
-            band1 = pass2.b;
-            b1c = pass2.B;
-            std::vector<double> hb(b1c);
-            for (int r = 0; r < b1c; ++r) hb[r] = hx[r <= band1 ? r : ax.n + r - b1c];
-            dx_band.upload(hb.data(), b1c, st);
-        }
     }
-    if (pruned && !dft) {
+    if (pruned) {
+        // rows: cuFFT over the populated rows; columns: the band columns
+        // transposed (k_band_transpose), then contiguous length-n1 transforms
         int n2[1] = {ay.n}, n1[1] = {ax.n};
         ckfft(cufftPlanMany(&fft_row, 1, n2, n2, 1, ay.n, n2, 1, ay.n, CUFFT_Z2Z, rhi - rlo),
               "cufftPlanMany rows");
-        const char* fe = std::getenv("SBD_FFT");
-        if (fe && fe[0] == 'c') {  // strided column transforms straight from T
-            ckfft(cufftPlanMany(&fft_colA, 1, n1, n1, ay.n, 1, n1, bc, 1, CUFFT_Z2Z, band2 + 1),
-                  "cufftPlanMany cols A");
-            ckfft(cufftPlanMany(&fft_colB, 1, n1, n1, ay.n, 1, n1, bc, 1, CUFFT_Z2Z, band2),
-                  "cufftPlanMany cols B");
-        } else {  // band columns transposed, then contiguous length-n1 transforms
-            ckfft(cufftPlanMany(&fft_colT, 1, n1, n1, 1, ax.n, n1, 1, ax.n, CUFFT_Z2Z, bc),
-                  "cufftPlanMany cols T");
-        }
+        ckfft(cufftPlanMany(&fft_colT, 1, n1, n1, 1, ax.n, n1, 1, ax.n, CUFFT_Z2Z, bc),
+              "cufftPlanMany cols T");
     }
     ck(cudaStreamSynchronize(st), "plan build");
 }
@@ -278,8 +234,6 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
 Plan::~Plan() {
     if (fft) cufftDestroy(fft);
     if (fft_row) cufftDestroy(fft_row);
-    if (fft_colA) cufftDestroy(fft_colA);
-    if (fft_colB) cufftDestroy(fft_colB);
     if (fft_colT) cufftDestroy(fft_colT);
     if (hp1) cufftDestroy(hp1);
     if (hp2) cufftDestroy(hp2);
@@ -288,7 +242,7 @@ Plan::~Plan() {
 // Radix r of a first pass folded into the producer of a length-n transform
 // (n = r M, r in {3, 5, 9}, M <= 4096 a multiple of 8: cuFFT then runs one
 // length-M pass instead of two length-n passes). 1: none. Used for n > 4096;
-// SBD_RADIX=0 turns it off, SBD_RADIX=force uses it for any such n (tests).
+// opts.radix = 0 turns it off, 1 uses it for any such n (tests).
 // tw[m] = e^{+2 pi i m / n}, m < n (long double arguments)
 static void upload_twiddles(DevBuf<double2>& tw, int n, cudaStream_t st) {
     std::vector<double2> h(n);
@@ -300,10 +254,9 @@ static void upload_twiddles(DevBuf<double2>& tw, int n, cudaStream_t st) {
     ck(cudaStreamSynchronize(st), "twiddles");
 }
 
-static int pick_radix(int n) {
-    const char* e = std::getenv("SBD_RADIX");
-    if (e && e[0] == '0') return 1;
-    const bool force = e && e[0] == 'f';
+static int pick_radix(int n, int mode) {
+    if (mode == 0) return 1;
+    const bool force = mode == 1;
     if (!force && n <= 4096) return 1;
     for (int r : {3, 5, 9})
         if (n % r == 0 && n / r <= 4096 && (n / r) % 8 == 0) return r;
@@ -311,7 +264,7 @@ static int pick_radix(int n) {
 }
 
 bool Plan::enable_hfft(int role, cudaStream_t st) {
-    if (!fast || !pruned || dft) return false;
+    if (!fast || !pruned) return false;
     const int n1 = ax.n, n2 = ay.n, R = rhi - rlo;
     if (role == 1) {
         // the spread grid is real only when the prephase is (fcenter exactly 0)
@@ -326,7 +279,7 @@ bool Plan::enable_hfft(int role, cudaStream_t st) {
         hC.alloc((size_t)hcols * n1);
         int nr[1] = {n2}, nc[1] = {n1};
         ckfft(cufftPlanMany(&hp1, 1, nr, nr, 1, n2, nr, 1, n2, CUFFT_Z2Z, R / 2), "hfft Z2Z rows");
-        hrad = pick_radix(n1);
+        hrad = pick_radix(n1, opts.radix);
         if (hrad > 1) {
             // the untangle does the radix-hrad first pass; cuFFT one length-M pass
             const int M = n1 / hrad;
@@ -390,7 +343,7 @@ bool Plan::enable_hfft(int role, cudaStream_t st) {
         hdx_band.upload(hb.data(), hB1, st);
         int nc[1] = {n1}, nr[1] = {n2};
         ckfft(cufftPlanMany(&hp1, 1, nc, nc, 1, n1, nc, 1, n1, CUFFT_Z2Z, hnm), "hfft Z2Z cols");
-        hrad = pick_radix(n2);
+        hrad = pick_radix(n2, opts.radix);
         if (hrad > 1) {
             // the packing does the radix-hrad first pass; cuFFT one length-M pass
             const int M = n2 / hrad;
@@ -425,11 +378,6 @@ void FftWork::ensure(int n1_, int n2_, int bc_, cudaStream_t st) {
 
 void Plan::ensure_work(FftWork& wk, cudaStream_t st) const {
     if (fast) wk.ensure(std::max(wk.n1, ax.n), std::max(wk.n2, ay.n), std::max(wk.bc, bc), st);
-    if (dft) {
-        const size_t t1 = (size_t)pass1.rows * pass1.B, bt = (size_t)pass2.rows * pass2.B;
-        if (wk.T1.n < t1) wk.T1.alloc(t1);
-        if (wk.bandT.n < bt) wk.bandT.alloc(bt);
-    }
     if (fft_colT) {
         const size_t need = (size_t)bc * ax.n;
         if (wk.T1.n < need) {
@@ -507,7 +455,8 @@ void Plan::apply(const double2* in, double2* out, FftWork& wk, cudaStream_t st, 
     if (tm) tm->stop();
     if (tm) tm->start(tag_interp);
     launch_interp(w, win, g, nf, s.p, post.p, mult, dx.p, dy.p, wk.grid.p,
-                  perm_s.n ? perm_s.p : nullptr, out, 0, 0, st);
+                  perm_s.n ? perm_s.p : nullptr, out, 0, 0, st, nullptr, false, nullptr, nullptr,
+                  opts.interp_kernel);
     if (tm) tm->stop();
     wk.gr0 = 0;
     wk.gr1 = ax.n;
@@ -572,7 +521,8 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         so.cend = chi;
         so.nby_run = tg.nby;
         so.lists = lists(false);
-        launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, nullptr, st, bs2, hflag, &so);
+        launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, nullptr, st, bs2, hflag, &so, nullptr,
+                            opts.spread_kernel);
         if (tm) tm->stop();
         if (tm) tm->start(tag_fft);
         ckfft(cufftSetStream(hp1, st), "cufftSetStream");
@@ -599,7 +549,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         }
         // with the radix pass the column factors are already in the band
         launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx.p, hrad > 1 ? nullptr : dy_band.p, hC.p, perm_p,
-                      out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles, hp);
+                      out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles, hp, opts.interp_kernel);
         if (tm) tm->stop();
         return;
     }
@@ -619,7 +569,8 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         // partner's (only images near the m2 = n2/2 line are ever read)
         so.src2 = hv_src.p;
         so.lists = lists(true);
-        launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, hA.p, st, hv_bins.p, nullptr, &so);
+        launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, hA.p, st, hv_bins.p, nullptr, &so, nullptr,
+                            opts.spread_kernel);
         if (tm) tm->stop();
         if (tm) tm->start(tag_fft);
         ckfft(cufftSetStream(hp1, st), "cufftSetStream");
@@ -647,32 +598,8 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
             gr.rad_magic = (unsigned)((0x100000000ull + hrad - 1) / hrad);
         }
         launch_interp_real(w, win, gr, nout, s_p, post_p, hdx_band.p, dy.p,
-                           reinterpret_cast<const double*>(hD.p), perm_p, add_p, out_p, st, &otiles);
-        if (tm) tm->stop();
-        return;
-    }
-    if (dft) {
-        // compact support grid -> rows pass -> band-columns pass -> transposed band
-        {
-            const SpreadLists sl = lists(false);
-            launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, wk.grid.p, st, bs2, hflag, nullptr, &sl);
-        }
-        if (tm) tm->stop();
-        if (tm) tm->start(tag_fft);
-        launch_pruned_dft(pass1, wk.grid.p, wk.T1.p, tw1.p, st);
-        launch_pruned_dft(pass2, wk.T1.p, wk.bandT.p, tw2.p, st);
-        if (tm) tm->stop();
-        // the full-layout invariants of the cuFFT path no longer hold
-        wk.gr0 = 0;
-        wk.gr1 = wk.n1;
-        wk.gc0 = 0;
-        wk.gc1 = wk.n2;
-        wk.g_pitch = wk.n2;
-        if (before_interp) ck(cudaStreamWaitEvent(st, before_interp, 0), "wait");
-        if (tm) tm->start(tag_interp);
-        const GridGeom gt{b1c, bc, 0.5 * w};
-        launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx_band.p, dy_band.p, wk.bandT.p, perm_p,
-                      out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles, hp);
+                           reinterpret_cast<const double*>(hD.p), perm_p, add_p, out_p, st, &otiles,
+                           opts.interp_kernel);
         if (tm) tm->stop();
         return;
     }
@@ -681,7 +608,8 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
     else if (wk.g_pitch)  // written by a plan of another grid size: clear all of it
         zero_rect_minus(wk.grid.p, wk.g_pitch, wk.gr0, wk.gr1, wk.gc0, wk.gc1, 0, 0, 0, 0, st);
     const SpreadLists sl = lists(false);
-    launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, wk.grid.p, st, bs2, hflag, nullptr, &sl);
+    launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, wk.grid.p, st, bs2, hflag, nullptr, &sl,
+                        opts.spread_kernel);
     wk.gr0 = rlo;
     wk.gr1 = rhi;
     wk.gc0 = clo;
@@ -696,13 +624,12 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         zero_rect_minus(wk.T.p, wk.t_pitch, wk.tr0, wk.tr1, 0, wk.t_pitch, 0, 0, 0, 0, st);
     auto* G = reinterpret_cast<cufftDoubleComplex*>(wk.grid.p);
     auto* T = reinterpret_cast<cufftDoubleComplex*>(wk.T.p);
-    auto* B = reinterpret_cast<cufftDoubleComplex*>(wk.band.p);
     ckfft(cufftSetStream(fft_row, st), "cufftSetStream");
     ckfft(cufftExecZ2Z(fft_row, G + (size_t)rlo * n2, T + (size_t)rlo * n2, CUFFT_INVERSE), "fft rows");
     wk.tr0 = rlo;
     wk.tr1 = rhi;
     wk.t_pitch = n2;
-    if (fft_colT) {
+    {
         // Tt[c'][x] (pitch n1) holds band column c' over the populated rows only;
         // every other row x of Tt stays zero (strips a previous plan left are cleared).
         if (wk.tt_r1 > wk.tt_r0) {
@@ -726,23 +653,10 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         if (tm) tm->start(tag_interp);
         const GridGeom gt{ax.n, bc, 0.5 * w};
         launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx.p, dy_band.p, wk.bandT.p, perm_p,
-                      out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles, hp);
+                      out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles, hp, opts.interp_kernel);
         if (tm) tm->stop();
         return;
     }
-    // band columns of T -> band buffer (n1 x bc, columns in mode order mod bc)
-    ckfft(cufftSetStream(fft_colA, st), "cufftSetStream");
-    ckfft(cufftExecZ2Z(fft_colA, T, B, CUFFT_INVERSE), "fft cols A");
-    ckfft(cufftSetStream(fft_colB, st), "cufftSetStream");
-    ckfft(cufftExecZ2Z(fft_colB, T + (n2 - band2), B + (band2 + 1), CUFFT_INVERSE), "fft cols B");
-    count_launch(3);
-    if (tm) tm->stop();
-    if (before_interp) ck(cudaStreamWaitEvent(st, before_interp, 0), "wait");
-        if (tm) tm->start(tag_interp);
-    const GridGeom gb{ax.n, bc, 0.5 * w};
-    launch_interp(w, win, gb, nout, s_p, post_p, mult_p, dx.p, dy_band.p, wk.band.p, perm_p, out_p, 0,
-                  0, st, add_p, false, &otiles, hp);
-    if (tm) tm->stop();
 }
 
 // nufft.cpp:295-367
@@ -778,7 +692,8 @@ void Plan::apply_transpose(const double2* in, double2* out, FftWork& wk, cudaStr
     if (tm) tm->stop();
     if (tm) tm->start("interp_T");
     launch_interp(w, win, g, np, t.p, pre.p, mult, nullptr, nullptr, wk.grid.p,
-                  perm_t.n ? perm_t.p : nullptr, out, 0, conj_out, st);
+                  perm_t.n ? perm_t.p : nullptr, out, 0, conj_out, st, nullptr, false, nullptr, nullptr,
+                  opts.interp_kernel);
     if (tm) tm->stop();
     wk.gr0 = 0;
     wk.gr1 = ax.n;

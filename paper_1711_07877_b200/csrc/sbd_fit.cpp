@@ -238,7 +238,7 @@ class Workspace {
         gram_ = assemble_gram(basis_, a_, bc_ == 1 ? H_ : 0.0);
         chol_ = gram_;
         chol_ok_ = gpu_cholesky(chol_, cap_, device_);
-        if (std::getenv("SBD_VERBOSE"))
+        if (g_verbose)
             std::fprintf(stderr, "[sbd fit] ensure(P=%d) %.3f s\n", cap_,
                          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
     }

@@ -29,6 +29,9 @@ inline void ckfft(cufftResult r, const char* what) {
     if (r != CUFFT_SUCCESS) throw_cufft(r, what);
 }
 void count_launch(int n = 1);
+// setup diagnostics on stderr for the calling thread's current entry point
+// (sbd_op_options::verbose; no environment switches)
+extern thread_local bool g_verbose;
 
 // ---------------------------------------------------------------- buffers
 template <typename T>
@@ -105,6 +108,11 @@ struct NufftOpts {
     int mode = 0; // 0 auto, 1 direct, 2 fast
     uint64_t direct_threshold = uint64_t(1) << 20;
     uint64_t max_grid_bytes = uint64_t(4) << 30;
+    // kernel / pipeline selection (sbd_op_options in include/sbd_b200.h; every
+    // choice stays within the parity bar)
+    int radix = -1;        // radix first pass folded into the untangle/pack: -1 auto (n > 4096), 0 off, 1 force
+    int spread_kernel = 0; // 0 CTA spread over region lists, 1 CTA over bins, 2 per-warp DMMA, 3 scalar tiles
+    int interp_kernel = 0; // 0 auto, 1 staged DMMA tiles, 2 DMMA per warp, 3 scalar
 };
 
 int width_for_tol(double tol);  // nufft.cpp:47-52
@@ -128,7 +136,7 @@ struct StageTimer {
 // dirty rectangles", so no full-grid memset is needed per apply.
 struct FftWork {
     DevBuf<double2> grid, T, band;
-    DevBuf<double2> T1, bandT; // row-pass output / transposed band (custom or cuFFT-T path)
+    DevBuf<double2> T1, bandT; // transposed band columns before / after the column transform
     int tt_r0 = 0, tt_r1 = 0;  // rows (x) possibly nonzero in every Tt row (cuFFT-T path) ...
     int tt_pitch = 0, tt_rows = 0; // ... for a Tt of this pitch (n1) and row count (bc)
     DevBuf<double2> bbuf; // spread coefficients b = c * prephase, sorted point order
@@ -149,18 +157,6 @@ struct TileGeom {
     int tr;              // rows per tile (8 or 16)
     int pitch;           // 0: write the full n1 x n2 grid; else compact region layout
     int rhi, chi;        // region end (writes clipped here)
-};
-
-// One band-pruned DFT pass (pruned_dft.cu): `rows` sequences, element m
-// (m in [lo, lo+L)) of sequence r at in[r * in_row + (m - lo) * in_elem];
-// output mode j (|j| <= b) at out[r * out_row + (j mod B) * out_elem].
-struct PrunedPass {
-    int n = 0, lo = 0, L = 0, rows = 0;
-    int b = 0, B = 0;  // band half-width n/4 and band size 2b+1
-    int D = 0, N = 0;  // output decimation and sub-FFT length n / D
-    int nstages = 0;
-    int radix[32] = {0};
-    int64_t in_row = 0, in_elem = 1, out_row = 0, out_elem = 1;
 };
 
 // A type-III NUFFT plan on one device (reference NufftPlan, nufft.hpp:30-56).
@@ -213,7 +209,6 @@ class Plan {
     // the populated region; row FFTs over the populated rows only, column FFTs
     // over the band columns only (the only modes the interpolation reads).
     bool pruned = false;
-    bool dft = false;  // custom band-pruned DFT passes (else cuFFT row/column plans)
     int rlo = 0, rhi = 0, clo = 0, chi = 0; // region written by the spread tiles
     TileGeom tg{};
     DevBuf<uint32_t> bin_start;
@@ -227,13 +222,8 @@ class Plan {
     int out_shift = 0;
     int band2 = 0, bc = 0;
     DevBuf<double> dy_band;
-    cufftHandle fft_row = 0, fft_colA = 0, fft_colB = 0;
+    cufftHandle fft_row = 0;
     cufftHandle fft_colT = 0;  // contiguous transforms of the transposed band columns
-    // custom passes: rows of the compact grid (n2, band B2) then band columns (n1, band B1)
-    int band1 = 0, b1c = 0;
-    DevBuf<double> dx_band;
-    DevBuf<double2> tw1, tw2;  // e^{+2 pi i q / n} tables for the two axes
-    PrunedPass pass1{}, pass2{};
 
     // Hermitian-FFT mode for a real input (op.cpp). Role 1 (fwd_in): the
     // spread grid is real; its rows are packed in pairs into complex rows ->
@@ -373,11 +363,12 @@ void launch_bin_bounds(const uint32_t* sorted_keys, uint64_t n, uint32_t nbins, 
 // Tile-owned spread: writes every cell of the tiles (no atomics, no memset).
 // bin_start2 (optional): a second bin set over the same tiles (tag-1 points),
 // skipped when *herm is nonzero
+// variant: NufftOpts::spread_kernel
 void launch_spread_tiles(int w, const WindowPoly& win, GridGeom g, TileGeom tg,
                          const uint32_t* bin_start, const double2* b, const double2* pos,
                          double2* grid, cudaStream_t st, const uint32_t* bin_start2 = nullptr,
                          const int* herm = nullptr, const SpreadOut* out = nullptr,
-                         const SpreadLists* lists = nullptr);
+                         const SpreadLists* lists = nullptr, int variant = 0);
 // SpreadLists of n points (tile-geometry grid coordinates), entries (base + k) | tagbit
 void build_region_lists(const double2* pos, uint64_t n, int w, TileGeom tg, uint32_t base, uint32_t tagbit,
                         DevBuf<uint32_t>& start, DevBuf<uint32_t>& ent, cudaStream_t st);
@@ -410,7 +401,7 @@ void launch_pack_dif(const double2* Y, int n1, int m0, int n2, int b1, int B1, d
 void launch_interp_real(int w, const WindowPoly& win, GridGeom g, uint64_t n, const double2* pos,
                         const double2* phase, const double* dx, const double* dy, const double* grid,
                         const uint32_t* perm, const double2* addend, double2* out, cudaStream_t st,
-                        const struct InterpTiles* tiles = nullptr);
+                        const struct InterpTiles* tiles = nullptr, int variant = 0);
 // b[k] = in[perm[k]] phase[k] for k in [lo, hi) (zero elsewhere); raw[k] = in[perm[k]].
 // clear (optional): set to 0 when some in[k] has a nonzero imaginary part.
 void launch_gather_mul(const double2* in, const uint32_t* perm, const double2* phase, double2* b,
@@ -457,7 +448,7 @@ void launch_interp(int w, const WindowPoly& win, GridGeom g, uint64_t n, const d
                    const double2* grid, const uint32_t* perm, double2* out, int accumulate,
                    int conj_out, cudaStream_t st, const double2* addend = nullptr,
                    bool transposed = false, const InterpTiles* tiles = nullptr,
-                   const HermArgs* herm = nullptr);
+                   const HermArgs* herm = nullptr, int variant = 0);  // variant: NufftOpts::interp_kernel
 // sorted keys -> starts of the runs of equal key >> bits
 void build_tile_starts(const uint32_t* sorted_keys, uint64_t n, int bits, DevBuf<uint32_t>& start,
                        uint32_t& ntiles, cudaStream_t st);

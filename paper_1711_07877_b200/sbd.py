@@ -98,8 +98,29 @@ def make_cloud(points) -> PointCloud:
 
 
 @dataclasses.dataclass
+class OpOptions:
+    """sbd_op_options (include/sbd_b200.h): the pipeline choices of one
+    operator. Every combination computes the same operator within the parity
+    bar; the defaults are the fastest path."""
+    real_input_split: bool = True
+    hermitian_fft: bool = True
+    radix_first_pass: int = -1   # -1 auto, 0 off, 1 force
+    spread_kernel: str = "lists"  # lists | bins | warp | scalar
+    interp_kernel: str = "auto"   # auto | tile | mma | scalar
+    fused: bool = True
+    verbose: bool = False
+
+    def _c(self) -> _capi.OpOptionsC:
+        sk = {"lists": 0, "bins": 1, "warp": 2, "scalar": 3}[self.spread_kernel]
+        ik = {"auto": 0, "tile": 1, "mma": 2, "scalar": 3}[self.interp_kernel]
+        return _capi.OpOptionsC(int(self.real_input_split), int(self.hermitian_fft),
+                                int(self.radix_first_pass), sk, ik, int(self.fused), int(self.verbose))
+
+
+@dataclasses.dataclass
 class AssembleOptions:
-    """conv_operator.hpp:24-31 plus the CUDA device ordinal."""
+    """conv_operator.hpp:24-31 plus the CUDA device ordinal and the pipeline
+    options."""
     eps: float = 1e-6
     alpha: float = 0.0
     a_override: float = 0.0
@@ -107,11 +128,12 @@ class AssembleOptions:
     nufft_direct_threshold: int = 1 << 20
     max_grid_bytes: int = 4 << 30
     device: int = 0
+    pipeline: OpOptions = dataclasses.field(default_factory=OpOptions)
 
     def _c(self) -> _capi.AssembleOptionsC:
         return _capi.AssembleOptionsC(self.eps, self.alpha, self.a_override, self.small_k_factor,
                                       self.nufft_direct_threshold, self.max_grid_bytes,
-                                      self.device)
+                                      self.device, self.pipeline._c())
 
 
 @dataclasses.dataclass
@@ -169,11 +191,13 @@ class CompressedOperator:
         return CompressedOperator(h)
 
     @staticmethod
-    def load(path: str, device: int = 0, max_grid_bytes: int = 0) -> "CompressedOperator":
+    def load(path: str, device: int = 0, max_grid_bytes: int = 0,
+             options: Optional[OpOptions] = None) -> "CompressedOperator":
         """conv_operator.cpp:449-490 (max_grid_bytes 0 = the reference's 4 GiB)."""
         h = ctypes.c_void_p()
-        check(lib.sbd_op_load(str(path).encode(), int(device), int(max_grid_bytes),
-                              ctypes.byref(h)))
+        oc = (options or OpOptions())._c()
+        check(lib.sbd_op_load_ex(str(path).encode(), int(device), int(max_grid_bytes),
+                                 ctypes.byref(oc), ctypes.byref(h)))
         return CompressedOperator(h)
 
     def save(self, path: str) -> None:
@@ -270,11 +294,20 @@ class CompressedOperator:
                  out.view(np.float64).ctypes.data_as(_dp), nrhs))
         return out if batched else out[0]
 
-    def apply_device(self, f_ptr: int, q_ptr: int, nrhs: int = 1, stream: int = 0) -> None:
+    def apply_device(self, f_ptr: int, q_ptr: int, nrhs: int = 1, stream: int = 0,
+                     f_is_real=None) -> None:
         """Device-buffer apply (interleaved complex128, nrhs x n). Enqueued on
-        `stream` (a cudaStream_t as int; 0 = the legacy default stream)."""
-        check(lib.sbd_op_apply_device(self._h, ctypes.c_void_p(f_ptr), ctypes.c_void_p(q_ptr),
-                                      int(nrhs), ctypes.c_void_p(stream or None)))
+        `stream` (a cudaStream_t as int; 0 = the legacy default stream); never
+        synchronises. f_is_real: None (unknown, decided on the device), a bool
+        for every column, or a list of nrhs bools (sbd_op_apply_device_ex)."""
+        if f_is_real is None:
+            check(lib.sbd_op_apply_device(self._h, ctypes.c_void_p(f_ptr), ctypes.c_void_p(q_ptr),
+                                          int(nrhs), ctypes.c_void_p(stream or None)))
+            return
+        flags = [f_is_real] * nrhs if isinstance(f_is_real, (bool, int)) else list(f_is_real)
+        arr = (ctypes.c_int * nrhs)(*[1 if x else 0 for x in flags])
+        check(lib.sbd_op_apply_device_ex(self._h, ctypes.c_void_p(f_ptr), ctypes.c_void_p(q_ptr),
+                                         int(nrhs), ctypes.c_void_p(stream or None), arr))
 
     def apply_host(self, f_ptr: int, q_ptr: int, nrhs: int = 1) -> None:
         """sbd_op_apply on raw host pointers (e.g. pinned torch buffers)."""

@@ -46,3 +46,27 @@ def reflib():
     if not os.path.exists(REF_SO):
         pytest.skip("oracle/_ref/libsbdref.so not built (needs /root/reference at build time)")
     return RefLib()
+
+
+def config1_operator():
+    """(path, golden arrays) of BASELINE configs[0] (N = 1e4 Laplace disk): the
+    reference's own operator file, rebuilt by the reference's assemble
+    (oracle/_ref) when absent and checked bit-for-bit against the SHA-256 the
+    golden generator recorded (tests/golden/make_golden.py config1)."""
+    import hashlib
+    name = "cfg1_lap_disk_n10000"
+    with open(os.path.join(GOLDEN, "manifest.json")) as fh:
+        meta = json.load(fh)["config1"]
+    path = os.path.join(GOLDEN, name + ".sbdop")
+    g = dict(np.load(os.path.join(GOLDEN, name + ".npz")))
+    if not os.path.exists(path):
+        from oracle.oracle import REF_SO, RefLib
+        if not os.path.exists(REF_SO):
+            pytest.skip("config-1 operator needs oracle/_ref (the reference) to rebuild")
+        ref = RefLib()
+        tmp = path + f".{os.getpid()}.tmp"
+        ref.assemble_save(tmp, g["points"], a_override=meta["a_override"])
+        os.replace(tmp, path)
+    sha = hashlib.sha256(open(path, "rb").read()).hexdigest()
+    assert sha == meta["sha256"], "rebuilt config-1 operator differs from the golden's"
+    return path, g

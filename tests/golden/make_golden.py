@@ -50,6 +50,44 @@ def case(ref, name, src, tgt=None, kind=0, k=0.0, eps=1e-6, a_override=0.0, f_co
     return info
 
 
+CFG1 = "cfg1_lap_disk_n10000"
+
+
+def config1(ref, path=None):
+    """BASELINE.json configs[0] exactly: Laplace, N = 1e4 i.i.d. uniform in the
+    disk of diameter 1, eps = 1e-6, delta_min = 2.74/sqrt(N), real f. The
+    reference's operator file (7.8 MB) is not committed: the reference's own
+    assemble rebuilds it bit-identically in ~1 s (tests/conftest.py
+    config1_operator checks its SHA-256 against the manifest); the points, f,
+    u and the reference's outputs are committed."""
+    import hashlib
+    rng = np.random.default_rng(10_000)
+    src = disk_cloud(10_000, rng)
+    d = ref.diameter(src)
+    path = path or os.path.join(HERE, CFG1 + ".sbdop")
+    a = (2.74 / np.sqrt(10_000)) / d
+    info = ref.assemble_save(path, src, a_override=a)
+    sha = hashlib.sha256(open(path, "rb").read()).hexdigest()
+    return src, a, info, sha
+
+
+def config1_case(ref):
+    src, a, info, sha = config1(ref)
+    rng = np.random.default_rng(11)
+    n = len(src)
+    f = rng.standard_normal(n) + 0j
+    u = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    path = os.path.join(HERE, CFG1 + ".sbdop")
+    op = ref.load(path)
+    q = op.apply(f, n)
+    qa = op.apply_adjoint(u, n)
+    np.savez_compressed(os.path.join(HERE, CFG1 + ".npz"), points=src, f=f, q=q, u=u, qa=qa)
+    info.update(name=CFG1, n_src=n, n_tgt=n, kind=0, k=0.0, eps=1e-6, a_override=a, sha256=sha,
+                committed_operator=False)
+    print(json.dumps(info))
+    return info
+
+
 def nufft_kats(ref):
     rng = np.random.default_rng(17)
     out = {}
@@ -109,8 +147,9 @@ def main():
     cases.append(case(ref, "helm_far_clouds", s, t, kind=1, k=0.3, eps=1e-4, f_complex=True,
                       seed=6))
     kat = nufft_kats(ref)
+    cfg1 = config1_case(ref)
     with open(os.path.join(HERE, "manifest.json"), "w") as fh:
-        json.dump({"cases": cases, "nufft_kat": kat,
+        json.dump({"cases": cases, "config1": cfg1, "nufft_kat": kat,
                    "generator": "tests/golden/make_golden.py via oracle/_ref/libsbdref.so"},
                   fh, indent=1)
 

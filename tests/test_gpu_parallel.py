@@ -16,14 +16,12 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("name", ["lap_disk_n1000", "helm_disk_n800", "lap_two_clouds",
                                   "lap_star_n1500"])
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
-def test_sharded_halves_reproduce_apply(name, world, monkeypatch):
+def test_sharded_halves_reproduce_apply(name, world):
     path, g = golden(name)
     # the full-path operator (every xi node) and the default one (the
     # real-input half split for a real f) are sharded alike; each must
     # reproduce its own single-device apply
-    monkeypatch.setenv("SBD_NO_HERM", "1")
-    op_full = sbd.CompressedOperator.load(path)
-    monkeypatch.delenv("SBD_NO_HERM")
+    op_full = sbd.CompressedOperator.load(path, options=sbd.OpOptions(real_input_split=False))
     op_default = sbd.CompressedOperator.load(path)
     f = torch.from_numpy(np.ascontiguousarray(g["f"], dtype=np.complex128).view(np.float64)).cuda()
     for op in (op_full, op_default):

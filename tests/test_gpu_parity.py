@@ -48,6 +48,22 @@ def test_apply_random_rhs_vs_oracle(ops, oracle, name):
     assert rel_l2(ops[name].apply(f), oracle.op(path).apply(f)) <= PARITY
 
 
+def test_config1_matches_reference_golden():
+    # BASELINE configs[0] exactly: Laplace, N = 1e4 uniform disk, eps 1e-6,
+    # delta_min = 2.74/sqrt(N) -- the reference's operator file and its own
+    # apply / apply_adjoint outputs (tests/golden/make_golden.py config1)
+    from tests.conftest import config1_operator
+    path, g = config1_operator()
+    op = sbd.CompressedOperator.load(path)
+    assert rel_l2(op.apply(g["f"]), g["q"]) <= PARITY
+    assert rel_l2(op.apply_adjoint(g["u"]), g["qa"]) <= PARITY
+    # a complex right-hand side (full path, every xi node) against the reference itself
+    from oracle.oracle import REF_SO, RefLib
+    if os.path.exists(REF_SO):
+        fc = np.random.default_rng(12).standard_normal(10_000) + 1j * np.random.default_rng(13).standard_normal(10_000)
+        assert rel_l2(op.apply(fc), RefLib().load(path).apply(fc, 10_000)) <= PARITY
+
+
 def test_batched_rhs_equals_single(ops):
     _, g = golden("lap_disk_n1000")
     rng = np.random.default_rng(5)
@@ -187,17 +203,13 @@ def test_nufft_auto_direct_and_guards():
 
 
 @pytest.mark.parametrize("name", ["lap_disk_n1000", "helm_disk_n800", "lap_two_clouds"])
-def test_fused_and_unfused_paths_agree(name, monkeypatch):
+def test_fused_and_unfused_paths_agree(name):
     # The fused forward path (renumbered D, kappa-weighted xi interpolation)
     # against the plain stage-by-stage path on the same operator file.
     # (The real-input half split is off here: it is compared in its own test.)
     path, g = golden(name)
-    monkeypatch.setenv("SBD_NO_HERM", "1")
-    fused = sbd.CompressedOperator.load(path)
-    monkeypatch.setenv("SBD_NO_FUSED", "1")
-    plain = sbd.CompressedOperator.load(path)
-    monkeypatch.delenv("SBD_NO_FUSED")
-    monkeypatch.delenv("SBD_NO_HERM")
+    fused = sbd.CompressedOperator.load(path, options=sbd.OpOptions(real_input_split=False))
+    plain = sbd.CompressedOperator.load(path, options=sbd.OpOptions(real_input_split=False, fused=False))
     assert rel_l2(fused.apply(g["f"]), plain.apply(g["f"])) <= 1e-13
     assert rel_l2(plain.apply(g["f"]), g["q"]) <= PARITY
 
@@ -210,25 +222,13 @@ def test_apply_is_deterministic(ops):
     assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("name", ["lap_disk_n1000", "helm_disk_n800", "lap_star_n1500"])
-def test_pruned_dft_and_cufft_paths_agree(name, monkeypatch):
-    # the custom band-pruned DFT passes against the cuFFT row/column path
-    path, g = golden(name)
-    dft = sbd.CompressedOperator.load(path)
-    monkeypatch.setenv("SBD_FFT", "cufft")
-    cuf = sbd.CompressedOperator.load(path)
-    monkeypatch.delenv("SBD_FFT")
-    assert rel_l2(dft.apply(g["f"]), cuf.apply(g["f"])) <= 1e-13
-
-
-@pytest.mark.parametrize("mode", ["cufft", "dft"])
-def test_fft_variants_agree_on_two_clouds(mode, monkeypatch):
-    # plans of different grid sizes sharing the operator's scratch buffers
+@pytest.mark.parametrize("interp", ["tile", "mma", "scalar"])
+def test_interp_variants_agree_on_two_clouds(interp):
+    # plans of different grid sizes sharing the operator's scratch buffers,
+    # with every interpolation kernel
     path, g = golden("lap_two_clouds")
     base = sbd.CompressedOperator.load(path)
-    monkeypatch.setenv("SBD_FFT", mode)
-    other = sbd.CompressedOperator.load(path)
-    monkeypatch.delenv("SBD_FFT")
+    other = sbd.CompressedOperator.load(path, options=sbd.OpOptions(interp_kernel=interp))
     for _ in range(2):
         assert rel_l2(other.apply(g["f"]), base.apply(g["f"])) <= 1e-13
     assert rel_l2(base.apply(g["f"]), g["q"]) <= PARITY
@@ -244,62 +244,6 @@ def test_cpp_api_example():
     assert r.returncode == 0 and "PASS" in r.stdout
 
 
-def _grid_plan_inputs(nx, ny, tol, rng, n=20000):
-    # points in [-1, 1]^2 (X = 1, gamma = 2 / pi) and frequency half-extents S
-    # chosen so that ceil(2 sigma (gamma S + w/2 + 1)) = n_axis - 4, which
-    # next_fast_even rounds up to n_axis for the sizes used below
-    w = min(max(int(np.ceil(-np.log10(tol))) + 2, 4), 17)
-    gamma = 2.0 / np.pi
-
-    def s_for(na):
-        return ((na - 4) / 4.0 - 0.5 * w - 1.0 - 1e-3) / gamma
-
-    sx, sy = s_for(nx), s_for(ny)
-    pts = rng.uniform(-1, 1, (n, 2))
-    pts[:4] = [[-1, -1], [1, 1], [-1, 1], [1, -1]]
-    frq = np.stack([rng.uniform(-sx, sx, n + 7), rng.uniform(-sy, sy, n + 7)], 1)
-    frq[:2] = [[-sx, -sy], [sx, sy]]
-    c = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
-    return pts, frq, c
-
-
-@pytest.mark.parametrize("nx,ny,r3", [(2304, 2304, "9"), (2304, 2304, "3"), (7680, 12288, "16,10"),
-                                      (7680, 12288, "12,15"), (7680, 12288, "8,6"),
-                                      (7680, 12288, "4,5"), (7680, 12288, "2,2"),
-                                      (7680, 12288, ""), (4608, 4608, "18")])
-def test_band_dft_radix_variants(nx, ny, r3, monkeypatch):
-    # every k_band_dft instantiation (N = 256 R3, decimation D = n / N) against
-    # the cuFFT row/column path and the direct sum
-    rng = np.random.default_rng(nx + ny + len(r3))
-    tol = 1e-8
-    pts, frq, c = _grid_plan_inputs(nx, ny, tol, rng)
-    opts = sbd.NufftOptions(tol=tol, mode="fast")
-    for sign in (1, -1):
-        base = sbd.NufftPlan(pts, frq, sign, opts)
-        assert base._meta()[2:] == (nx, ny)
-        monkeypatch.setenv("SBD_FFT", "dft-strict")
-        if r3:
-            monkeypatch.setenv("SBD_DFT_R3", r3)
-        plan = sbd.NufftPlan(pts, frq, sign, opts)
-        monkeypatch.delenv("SBD_FFT")
-        monkeypatch.delenv("SBD_DFT_R3", raising=False)
-        got, want = plan.apply(c), base.apply(c)
-        assert rel_l2(got, want) <= 1e-13
-        sub = rng.choice(len(frq), 2000, replace=False)
-        d = sbd.ndft_direct(pts, frq[sub], c, sign)
-        assert np.max(np.abs(got[sub] - d)) <= tol * np.abs(c).sum()
-
-
-def test_band_dft_strict_rejects_unsupported_grid(monkeypatch):
-    rng = np.random.default_rng(5)
-    pts, frq, _ = _grid_plan_inputs(2304, 2304, 1e-8, rng, n=100)
-    monkeypatch.setenv("SBD_FFT", "dft-strict")
-    monkeypatch.setenv("SBD_DFT_R3", "16")  # 4096 does not divide 2304
-    with pytest.raises(sbd.SbdError, match="unsupported"):
-        sbd.NufftPlan(pts, frq, 1, sbd.NufftOptions(tol=1e-8, mode="fast"))
-
-
-# ------------------------------------------------------- real-input half split
 def _close_times(op, f):
     # D f on the host from the operator's own close matrix (row k = target k)
     m = op.close_matrix()
@@ -314,7 +258,7 @@ HALF_CASES = ["lap_disk_n1000", "lap_star_n1500", "lap_two_clouds"]
 
 
 @pytest.mark.parametrize("name", HALF_CASES)
-def test_real_input_half_split(ops, oracle, name, monkeypatch):
+def test_real_input_half_split(ops, oracle, name):
     # real omega-hat, antipodal rings, real f: only half of the xi nodes are
     # interpolated / spread and the far field is 2 Re(.) (op.cpp herm_pairs);
     # the result must match the full computation and the reference
@@ -327,9 +271,7 @@ def test_real_input_half_split(ops, oracle, name, monkeypatch):
     # window's asymmetry, ~1e-10 relative); the full path carries them
     df = _close_times(ops[name], f)
     assert np.abs(q.imag).max() == 0.0
-    monkeypatch.setenv("SBD_NO_HERM", "1")
-    full = sbd.CompressedOperator.load(path)
-    monkeypatch.delenv("SBD_NO_HERM")
+    full = sbd.CompressedOperator.load(path, options=sbd.OpOptions(real_input_split=False))
     qf = full.apply(f)
     if name != "lap_two_clouds":  # (its full-path asymmetry is at rounding level)
         assert np.abs(qf.imag - df.imag).max() > 1e-14 * np.abs(qf).max()
@@ -367,78 +309,131 @@ def test_helmholtz_real_input_takes_full_path(ops, oracle):
 
 
 @pytest.mark.parametrize("name", HALF_CASES)
-def test_hermitian_fft_mode_device_and_host_agree(ops, name, monkeypatch):
-    # Real f: the Hermitian-FFT pipelines (real-grid D2Z, mirrored spread +
-    # Z2D) are chosen by a host scan (sbd_op_apply) or a device check
-    # (sbd_op_apply_device); both must equal the half split without them.
+def test_hermitian_fft_mode_device_and_host_agree(ops, name):
+    # Real f: the Hermitian-FFT pipelines are chosen by a host scan
+    # (sbd_op_apply) or the caller's hint (sbd_op_apply_device_ex); the plain
+    # device call (sbd_op_apply_device, realness unknown) takes the device-flag
+    # half split without them. All must equal the half split without them.
     import torch
     path, g = golden(name)
     f = np.random.default_rng(31).standard_normal(len(g["f"])) + 0j
     q = ops[name].apply(f)
     fd = torch.from_numpy(f.view(np.float64).copy()).cuda()
-    qd = torch.zeros(2 * len(q), dtype=torch.float64, device="cuda")
-    ops[name].apply_device(fd.data_ptr(), qd.data_ptr(), 1, torch.cuda.current_stream().cuda_stream)
-    torch.cuda.synchronize()
-    assert rel_l2(qd.cpu().numpy().view(np.complex128), q) <= 1e-14
-    monkeypatch.setenv("SBD_NO_HFFT", "1")
-    plain = sbd.CompressedOperator.load(path)
-    monkeypatch.delenv("SBD_NO_HFFT")
+    st = torch.cuda.current_stream().cuda_stream
+    for hint in (None, True, False):
+        qd = torch.zeros(2 * len(q), dtype=torch.float64, device="cuda")
+        ops[name].apply_device(fd.data_ptr(), qd.data_ptr(), 1, st, f_is_real=hint)
+        torch.cuda.synchronize()
+        qh = qd.cpu().numpy().view(np.complex128)
+        # without the real hint the CSR pass keeps Im(D) (the reference's own
+        # window-asymmetry term, ~1e-10 |D|), which the real-f path drops
+        assert rel_l2(qh.real, q.real) <= 1e-13, hint
+        assert rel_l2(qh, q) <= (1e-13 if hint else 1e-10), hint
+    plain = sbd.CompressedOperator.load(path, options=sbd.OpOptions(hermitian_fft=False))
     qp = plain.apply(f)
     assert rel_l2(q.real, qp.real) <= 1e-13 and rel_l2(q, qp) <= 1e-13
 
 
-_SPREAD_SCRIPT = """
-import sys, numpy as np
-sys.path.insert(0, {root!r})
-import paper_1711_07877_b200 as sbd
-from tests.conftest import golden
-out = []
-for name in {names!r}:
-    path, g = golden(name)
-    op = sbd.CompressedOperator.load(path)
-    f = np.random.default_rng(5).standard_normal(len(g["f"])) + 0j
-    out += [op.apply(g["f"]), op.apply(f)]
-np.save({dst!r}, np.concatenate(out))
-"""
-
-
-@pytest.mark.gpu
-def test_spread_variants_agree(tmp_path):
-    # The spread kernel is chosen once per process (SBD_SPREAD): the default
-    # CTA spread over plan-time region lists, the CTA spread scanning bins
-    # ('c') and the per-warp DMMA spread ('w') must agree on the complex path
-    # (Helmholtz), the real-input Hermitian pipelines and two-cloud plans.
-    import subprocess
-    import sys
-    from tests.conftest import ROOT
-    names = ["lap_star_n1500", "helm_disk_n800", "lap_two_clouds"]
-    res = {}
-    for v in ["", "c", "w"]:
-        dst = str(tmp_path / f"q_{v or 'default'}.npy")
-        env = dict(os.environ)
-        env.pop("SBD_SPREAD", None)
-        if v:
-            env["SBD_SPREAD"] = v
-        subprocess.run([sys.executable, "-c", _SPREAD_SCRIPT.format(root=ROOT, names=names, dst=dst)],
-                       check=True, env=env, cwd=ROOT)
-        res[v] = np.load(dst)
-    for v in ["c", "w"]:
-        assert rel_l2(res[v], res[""]) <= 1e-13, v
+@pytest.mark.parametrize("spread", ["bins", "warp", "scalar"])
+def test_spread_variants_agree(spread):
+    # the default CTA spread over plan-time region lists against the CTA
+    # spread scanning bins, the per-warp DMMA spread and the scalar tiles, on
+    # the complex path (Helmholtz), the real-input Hermitian pipelines and
+    # two-cloud plans (the scalar tiles cannot write the Hermitian modes'
+    # packed/transposed grids, so that operator runs without them)
+    for name in ["lap_star_n1500", "helm_disk_n800", "lap_two_clouds"]:
+        path, g = golden(name)
+        base = sbd.CompressedOperator.load(path)
+        o = sbd.OpOptions(spread_kernel=spread)
+        if spread == "scalar":
+            o.hermitian_fft = False
+        other = sbd.CompressedOperator.load(path, options=o)
+        f = np.random.default_rng(5).standard_normal(len(g["f"])) + 0j
+        for x in (g["f"], f):
+            assert rel_l2(other.apply(x), base.apply(x)) <= 1e-13, (name, spread)
 
 
 @pytest.mark.parametrize("name", HALF_CASES)
-def test_radix_first_pass_agrees(ops, name, monkeypatch):
+def test_radix_first_pass_agrees(ops, name):
     # Hermitian source side: the radix-r first pass of the column transform
     # folded into the untangle (k_untangle_dif + length-M cuFFT, band read in
     # (j mod r) M + j / r order) against the plain length-n1 transform.
     # Used by default above n1 = 4096 (config 4: 18432 = 9 x 2048); forced here.
     path, g = golden(name)
     f = np.random.default_rng(41).standard_normal(len(g["f"])) + 0j
-    monkeypatch.setenv("SBD_RADIX", "force")
-    rad = sbd.CompressedOperator.load(path)
-    monkeypatch.setenv("SBD_RADIX", "0")
-    plain = sbd.CompressedOperator.load(path)
-    monkeypatch.delenv("SBD_RADIX")
+    rad = sbd.CompressedOperator.load(path, options=sbd.OpOptions(radix_first_pass=1))
+    plain = sbd.CompressedOperator.load(path, options=sbd.OpOptions(radix_first_pass=0))
     q = rad.apply(f)
     assert rel_l2(q, plain.apply(f)) <= 1e-13
     assert rel_l2(q, ops[name].apply(f)) <= 1e-13
+
+
+def test_concurrent_host_applies_same_operator(ops):
+    # reference contract: apply is const and may be called concurrently
+    # (conv_operator.hpp:33-36). Two host threads on one operator must each
+    # get their own result (the staging copies are inside the operator lock).
+    import threading
+    _, g = golden("lap_disk_n1000")
+    op = ops["lap_disk_n1000"]
+    rng = np.random.default_rng(77)
+    fs = [rng.standard_normal(len(g["f"])) + 1j * rng.standard_normal(len(g["f"])),
+          rng.standard_normal(len(g["f"])) + 0j]
+    want = [op.apply(f) for f in fs]
+    errs = []
+
+    def work(i):
+        for _ in range(20):
+            if rel_l2(op.apply(fs[i]), want[i]) > 1e-14:
+                errs.append(i)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs
+
+
+def test_device_applies_on_two_streams_are_ordered(ops):
+    # successive device calls on different streams share the operator's
+    # scratch; the operator event orders them
+    import torch
+    _, g = golden("lap_star_n1500")
+    op = ops["lap_star_n1500"]
+    rng = np.random.default_rng(78)
+    n = len(g["f"])
+    fs = [rng.standard_normal(n) + 1j * rng.standard_normal(n) for _ in range(4)]
+    want = [op.apply(f) for f in fs]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    fd = [torch.from_numpy(f.view(np.float64).copy()).cuda() for f in fs]
+    qd = [torch.zeros(2 * n, dtype=torch.float64, device="cuda") for _ in fs]
+    torch.cuda.synchronize()
+    for i in range(4):
+        op.apply_device(fd[i].data_ptr(), qd[i].data_ptr(), 1, streams[i % 2].cuda_stream)
+    torch.cuda.synchronize()
+    for i in range(4):
+        assert rel_l2(qd[i].cpu().numpy().view(np.complex128), want[i]) <= 1e-14, i
+
+
+def test_device_apply_is_graph_capturable(ops):
+    # sbd_op_apply_device never synchronises, so an apply (with the caller's
+    # realness hint) can be captured into a CUDA graph and replayed
+    import torch
+    _, g = golden("lap_disk_n1000")
+    op = ops["lap_disk_n1000"]
+    n = len(g["f"])
+    f = np.random.default_rng(79).standard_normal(n) + 0j
+    want = op.apply(f)
+    fd = torch.from_numpy(f.view(np.float64).copy()).cuda()
+    qd = torch.zeros(2 * n, dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        op.apply_device(fd.data_ptr(), qd.data_ptr(), 1, s.cuda_stream, f_is_real=True)  # warm
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        op.apply_device(fd.data_ptr(), qd.data_ptr(), 1, s.cuda_stream, f_is_real=True)
+    qd.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert rel_l2(qd.cpu().numpy().view(np.complex128), want) <= 1e-14

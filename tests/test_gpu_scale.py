@@ -4,8 +4,9 @@ real-input half split, the Hermitian-FFT mode with the radix-9 first passes
 
 N = 6e5 points of the config-4 distribution (Laplace, uniform disk, eps 1e-6,
 delta_min = 2.74/sqrt(N)), assembled on the GPU, then
-  * against the C restatement (oracle/) applying the same SBDOPv1 file:
-    relative l2 <= 1e-9 (north_star parity bar);
+  * against the unmodified reference (oracle/_ref RefRaw: its own NufftPlan +
+    SparsePairMatrix) applying the same SBDOPv1 file: relative l2 <= 1e-9
+    (north_star parity bar), and against the C restatement;
   * against the direct O(N^2) sum at 1000 random targets: <= eps sum|f| (the
     reference's contract, conv_operator.hpp:50-51).
 The direct-sum check is what caught a stream race in the GPU assembly (the
@@ -41,12 +42,35 @@ def test_big_pipeline_geometry(big):
     assert info["n1_in"] > 4096 and info["n2_in"] > 4096  # radix first passes on
 
 
-def test_big_apply_vs_oracle(big, oracle):
+def test_big_apply_vs_reference(big, reflib, oracle):
     op, _, f, path = big
     q = op.apply(f)
     assert np.abs(q.imag).max() == 0.0  # real input, real omega-hat: exactly real
-    q_orc = oracle.op(path).apply(f)
-    assert rel_l2(q, q_orc) <= 1e-9
+    q_ref = reflib.raw(path, max_grid_bytes=16 << 30).apply(f, len(f))
+    assert rel_l2(q, q_ref) <= 1e-9
+    assert rel_l2(q, oracle.op(path).apply(f)) <= 1e-9
+
+
+def test_config3_helmholtz_vs_reference(tmp_path, reflib):
+    # BASELINE configs[2] exactly: Helmholtz kappa = k dmax = 2 pi 100, N = 1e6
+    # uniform in the unit-diameter disk, complex f, eps 1e-6, delta_min =
+    # 2.74/sqrt(N): the complex path (every xi node, complex D, 5120^2 grid),
+    # assembled on the GPU, against the reference applying the same file.
+    n = 1_000_000
+    z = disk_cloud(n, np.random.default_rng(303))
+    dmax = sbd.cloud_diameter(z)
+    op = sbd.CompressedOperator.assemble(
+        sbd.kernel_helmholtz(2 * np.pi * 100 / dmax), z,
+        opts=sbd.AssembleOptions(eps=1e-6, a_override=(2.74 / np.sqrt(n)) / dmax))
+    info = op.info()
+    assert (info["n1_in"], info["n2_in"], info["w"]) == (5120, 5120, 10)
+    path = str(tmp_path / "helm_cfg3.sbdop")
+    op.save(path)
+    rng = np.random.default_rng(304)
+    f = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    q = op.apply(f)
+    q_ref = reflib.raw(path, max_grid_bytes=16 << 30).apply(f, n)
+    assert rel_l2(q, q_ref) <= 1e-9
 
 
 def test_big_direct_sum_1000_targets(big):

@@ -80,3 +80,13 @@ def test_grid_guard(oracle):
     pts, frq = rng.uniform(-.5, .5, (64, 2)), rng.uniform(-2500, 2500, (64, 2))
     with pytest.raises(RuntimeError):
         oracle.plan(pts, frq, +1, 1e-9, mode=2, max_grid_bytes=1024)
+
+
+def test_config1_oracle_vs_reference_golden(oracle):
+    # BASELINE configs[0] exactly (N = 1e4): the C restatement against the
+    # reference's own apply / apply_adjoint on the reference's operator file
+    from tests.conftest import config1_operator
+    path, g = config1_operator()
+    op = oracle.op(path)
+    assert rel_l2(op.apply(g["f"]), g["q"]) <= 1e-12
+    assert rel_l2(op.apply_adjoint(g["u"]), g["qa"]) <= 1e-12
