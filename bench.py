@@ -37,7 +37,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from tests.clouds import disk_cloud, star_curve_cloud  # noqa: E402
+from tests.clouds import disk_cloud, star_curve_cloud, star_interior_cloud  # noqa: E402
 
 METRIC = "SBD apply points/s (N=1e6–1e7, ε=1e-6) at 1/2/4/8 B200; % HBM roofline"
 SEED = 20261019
@@ -63,6 +63,18 @@ def workload(name: str, scale: float = 1.0):
         z = disk_cloud(n, rng)
         return dict(desc=f"config1: Laplace, N={n} uniform disk d=1, eps=1e-6, delta_min=2.74/sqrt(N)",
                     z=z, kind=0, kappa=0.0, eps=1e-6, dmin=2.74 / np.sqrt(n), f_complex=False)
+    if name == "5":
+        # BASELINE configs[4] is 1.1e7 points with D row-sharded over several
+        # GPUs (>= 100 GB of D at any feasible delta_min); one
+        # GPU runs its shape at N/8: 1.25e6 on the star curve + 1.25e5 inside,
+        # Helmholtz k dmax = 2 pi 300, eps 1e-4, complex f, 8 right-hand sides
+        # per apply; delta_min is unspecified there: a = 5e-4 (P ~ 4200)
+        nc, ni = int(1.25e6 * scale), int(1.25e5 * scale)
+        z = np.concatenate([star_curve_cloud(nc, rng), star_interior_cloud(ni, rng)])
+        return dict(desc=f"config5 at N/8: Helmholtz k*dmax=2pi*300, N={nc}+{ni} star curve + interior, "
+                         "eps=1e-4, a=delta_min/delta_max=5e-4, complex f, 8 RHS per apply",
+                    z=z, kind=1, kappa=2 * np.pi * 300, eps=1e-4, dmin=None, a=5e-4, f_complex=True,
+                    nrhs=8)
     if name == "2s":
         n = int(1e6 * scale)
         z = star_curve_cloud(n, rng)
@@ -162,6 +174,9 @@ def reference_sample(w, sample_n):
     rng = np.random.default_rng(SEED + 1)
     if w["desc"].startswith("config2"):
         z = star_curve_cloud(sample_n, rng)
+    elif w["desc"].startswith("config5"):
+        z = np.concatenate([star_curve_cloud(sample_n - sample_n // 11, rng),
+                            star_interior_cloud(sample_n // 11, rng)])
     else:
         z = disk_cloud(sample_n, rng)
     path = f"/tmp/sbd_ref_sample_{os.getpid()}.sbdop"
@@ -169,7 +184,7 @@ def reference_sample(w, sample_n):
     if kind == "reference":
         lib = RefLib()
         d = lib.diameter(z)
-        a = (2.74 / np.sqrt(sample_n)) / d if w["dmin"] is not None else 0.0
+        a = (2.74 / np.sqrt(sample_n)) / d if w["dmin"] is not None else w.get("a", 0.0)
         lib.assemble_save(path, z, kind=w["kind"], k=w["kappa"] / d, eps=w["eps"], a_override=a)
         op = lib.load(path)
         apply = lambda f: op.apply(f, sample_n)  # noqa: E731
@@ -177,7 +192,7 @@ def reference_sample(w, sample_n):
         import paper_1711_07877_b200 as sbd  # only to build the operator file for the port
         d = sbd.cloud_diameter(z)
         kern = sbd.kernel_helmholtz(w["kappa"] / d) if w["kind"] else sbd.kernel_laplace()
-        a = (2.74 / np.sqrt(sample_n)) / d if w["dmin"] is not None else 0.0
+        a = (2.74 / np.sqrt(sample_n)) / d if w["dmin"] is not None else w.get("a", 0.0)
         o = sbd.CompressedOperator.assemble(kern, z, opts=sbd.AssembleOptions(eps=w["eps"],
                                                                                a_override=a))
         o.save(path)
@@ -308,17 +323,20 @@ def run_b200(args, w):
     t0 = time.perf_counter()
     dmax = sbd.cloud_diameter(z)
     kern = sbd.kernel_helmholtz(w["kappa"] / dmax) if w["kind"] else sbd.kernel_laplace()
-    a = w["dmin"] / dmax if w["dmin"] else 0.0
+    a = w["dmin"] / dmax if w["dmin"] else w.get("a", 0.0)
     opts = sbd.AssembleOptions(eps=w["eps"], a_override=a, max_grid_bytes=96 << 30, device=local)
     op = sbd.CompressedOperator.assemble(kern, z, opts=opts)
     t_offline = time.perf_counter() - t0
     info = op.info()
 
     rng = np.random.default_rng(SEED + 3)
-    f = rhs(w, n, rng)
+    R = w.get("nrhs", 1)  # right-hand sides per apply (config 5: a GMRES-style block of 8)
+    if R > 1 and world > 1:
+        raise SystemExit("bench: the sharded apply takes one right-hand side per step")
+    f = np.stack([rhs(w, n, rng) for _ in range(R)]) if R > 1 else rhs(w, n, rng)
     f_real = not w["f_complex"]
-    f_dev = torch.from_numpy(f.view(np.float64).copy()).cuda()
-    q_dev = torch.zeros(2 * n, dtype=torch.float64, device="cuda")
+    f_dev = torch.from_numpy(f.reshape(-1).view(np.float64).copy()).cuda()
+    q_dev = torch.zeros(2 * n * R, dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
 
@@ -331,7 +349,7 @@ def run_b200(args, w):
             sharded.apply(f_dev, q_dev)
     else:
         def step():  # the caller knows its f is real (sbd_op_apply_device_ex)
-            op.apply_device(f_dev.data_ptr(), q_dev.data_ptr(), 1, sh, f_is_real=f_real)
+            op.apply_device(f_dev.data_ptr(), q_dev.data_ptr(), R, sh, f_is_real=f_real)
 
     for _ in range(args.warmup):
         step()
@@ -361,7 +379,7 @@ def run_b200(args, w):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    value = n / (ms_step / 1e3)  # one apply of N points per step, whole job
+    value = n * R / (ms_step / 1e3)  # one apply of N points (x R right-hand sides) per step, whole job
 
     # per-stage averages over the timed region (CUDA events on the launch stream)
     agg = {}
@@ -380,11 +398,11 @@ def run_b200(args, w):
                                 for k in cand}}
 
     # end to end: host f (pinned) in, host q out, copies inside the timed region
-    fh = torch.from_numpy(f.view(np.float64).copy()).pin_memory()
-    qh = torch.empty(2 * n, dtype=torch.float64).pin_memory()
+    fh = torch.from_numpy(f.reshape(-1).view(np.float64).copy()).pin_memory()
+    qh = torch.empty(2 * n * R, dtype=torch.float64).pin_memory()
     if world == 1:
         def e2e_step():  # the reference-facing host-buffer C-ABI call (sbd_op_apply)
-            op.apply_host(fh.data_ptr(), qh.data_ptr(), 1)
+            op.apply_host(fh.data_ptr(), qh.data_ptr(), R)
     else:
         def e2e_step():
             f_dev.copy_(fh, non_blocking=True)
@@ -404,6 +422,26 @@ def run_b200(args, w):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
+    # pipelined host applies (sbd_op_apply_async): every step still copies its
+    # f in and its q out, but the copies overlap the neighbouring steps' device
+    # work (two staging slots, two copy streams) -- the batch-serving mode
+    e2e_pipe = None
+    if world == 1:
+        qh2 = torch.empty_like(qh).pin_memory()
+        qhs = [qh, qh2]
+        tk = [op.apply_async(fh.data_ptr(), qhs[k % 2].data_ptr(), R) for k in range(2)]
+        for t in tk:
+            op.wait(t)
+        t1 = time.perf_counter()
+        tk = [op.apply_async(fh.data_ptr(), qhs[k % 2].data_ptr(), R) for k in range(args.steps)]
+        for t in tk[-2:]:
+            op.wait(t)
+        ep = (time.perf_counter() - t1) / args.steps
+        e2e_pipe = {"value": n * R / ep, "unit": "points/s", "ms_per_step": round(ep * 1e3, 3),
+                    "h2d_bytes_per_step": 16 * n * R, "d2h_bytes_per_step": 16 * n * R,
+                    "note": "sbd_op_apply_async: host f in / host q out every step, copies overlapped "
+                            "with the neighbouring steps' device work"}
+
     # the reference's accuracy contract on this workload (conv_operator.hpp:50-51,
     # north_star: <= eps at 1,000 random targets): |q_k - sum_{l != k} G f_l| <=
     # eps sum|f|, the direct sum in fp64 on the GPU (torch)
@@ -416,11 +454,12 @@ def run_b200(args, w):
     if dist:
         dist.all_reduce(q_dev)
     qv = q_dev.view(-1, 2).cpu().numpy()
-    qv = qv[:, 0] + 1j * qv[:, 1]
+    qv = (qv[:, 0] + 1j * qv[:, 1])[:n]  # the first right-hand side
+    f0 = f[0] if R > 1 else f
     if rank == 0:
         rows = np.random.default_rng(SEED + 7).choice(n, 1000, replace=False)
         zt = torch.from_numpy(z).cuda()
-        ft = torch.from_numpy(f).cuda()
+        ft = torch.from_numpy(f0).cuda()
         want = torch.zeros(len(rows), dtype=torch.complex128, device="cuda")
         zr = zt[torch.from_numpy(rows).cuda()]
         kk = w["kappa"] / dmax
@@ -435,13 +474,13 @@ def run_b200(args, w):
             g = torch.where(m, g, torch.zeros_like(g))
             want += g @ ft[s0:s0 + 200_000]
         err = float(np.max(np.abs(qv[rows] - want.cpu().numpy())))
-        bound = w["eps"] * float(np.abs(f).sum())
+        bound = w["eps"] * float(np.abs(f0).sum())
         contract = {"targets": 1000, "max_abs_err": err, "bound_eps_sum_abs_f": bound, "ok": err <= bound}
 
     # batched right-hand sides (GMRES-style blocks, BASELINE config 5's "batch of
     # 8"): one apply of nrhs columns, D read once for all of them (k_spmm)
     batched = None
-    if world == 1 and args.nrhs > 1:
+    if world == 1 and args.nrhs > 1 and R == 1:
         fb = np.stack([rhs(w, n, np.random.default_rng(SEED + 10 + r)) for r in range(args.nrhs)])
         fb_dev = torch.from_numpy(fb.view(np.float64).reshape(-1).copy()).cuda()
         qb_dev = torch.empty(2 * n * args.nrhs, dtype=torch.float64, device="cuda")
@@ -467,10 +506,36 @@ def run_b200(args, w):
                    "note": "one apply of nrhs right-hand sides; D' streamed once for up to 8 columns"}
         del fb_dev, qb_dev
 
+    # the adjoint (conv_operator.cpp:311-324; GMRES / gradient callers): one
+    # apply_adjoint per step on device buffers, 3 steps after a warm-up
+    adjoint = None
+    if world == 1 and R == 1 and args.adjoint:
+        u_dev = torch.from_numpy((rng.standard_normal(n) + 1j * rng.standard_normal(n)).view(np.float64).copy()).cuda()
+        p_dev = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+        op.apply_adjoint_device(u_dev.data_ptr(), p_dev.data_ptr(), 1, sh)
+        torch.cuda.synchronize()
+        op.set_profiling(True)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(3):
+            op.apply_adjoint_device(u_dev.data_ptr(), p_dev.data_ptr(), 1, sh)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ast = op.stage_times()
+        op.set_profiling(False)
+        ams = a0.elapsed_time(a1) / 3
+        agg_a = {}
+        for nm, ms in ast:
+            agg_a[nm] = agg_a.get(nm, 0.0) + ms / 3
+        adjoint = {"value": n / (ams / 1e3), "unit": "points/s", "ms_per_apply": round(ams, 3),
+                   "stages_ms": {k: round(v, 3) for k, v in agg_a.items()},
+                   "note": "apply_adjoint of a complex u on device buffers"}
+        del u_dev, p_dev
+
     cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         if args.ref_full:
-            parity, cpu = reference_same_config(op, f, qv, 96 << 30)
+            parity, cpu = reference_same_config(op, f0, qv, 96 << 30)
         if cpu is None:
             kind, apply, fs, path = reference_sample(w, args.sample_n)
             per = min(time_reference(apply, fs, 1, 1) for _ in range(2))
@@ -486,7 +551,7 @@ def run_b200(args, w):
             "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded clouds/RHS of the BASELINE.json shape)",
-            "config": {"workload": w["desc"], "N": n, "n_xi": info["n_xi"], "nnz": info["nnz"],
+            "config": {"workload": w["desc"], "N": n, "nrhs": R, "n_xi": info["n_xi"], "nnz": info["nnz"],
                        "P": info["P"], "w": info["w"], "grid": [info["n1_in"], info["n2_in"]],
                        "nufft_tol": info["nufft_tol"],
                        "l2": "inputs larger than L2 (grid + xi + D >> 126 MB)",
@@ -497,11 +562,13 @@ def run_b200(args, w):
                        "offline_s": round(t_offline, 2)},
             "roofline": roofline,
             "cpu_baseline": cpu,
-            "e2e": {"value": n / e2e_s, "unit": "points/s",
-                    "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n},
+            "e2e": {"value": n * R / e2e_s, "unit": "points/s",
+                    "h2d_bytes_per_step": 16 * n * R, "d2h_bytes_per_step": 16 * n * R},
+            "e2e_pipelined": e2e_pipe,
             "gpu_launches": launches,
             "clocks": clk,
             "batched_rhs": batched,
+            "adjoint": adjoint,
             "contract": contract,
             "parity": parity,
         }
@@ -523,6 +590,7 @@ def main():
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nrhs", type=int, default=8, help="also time one batched apply of this many RHS (1: off)")
+    ap.add_argument("--adjoint", type=int, default=1, help="1: also time apply_adjoint")
     ap.add_argument("--ref-full", type=int, default=1,
                     help="1: one reference apply of the full config on one core after the timed region "
                          "(parity + same-config cpu_baseline; ~5 min at config 4); 0: the N=5e4 sample only")

@@ -131,6 +131,14 @@ int sbd_op_get(const sbd_op* op, int which, void* dst, uint64_t* count);
  * (chunked and overlapped; a real f moves only its real parts). */
 int sbd_op_apply(sbd_op* op, const double* f, double* q, int nrhs);
 int sbd_op_apply_adjoint(sbd_op* op, const double* u, double* q, int nrhs);
+/* Pipelined host-buffer apply (no reference analogue): enqueues the H2D of f,
+ * the apply and the D2H of q, and returns a ticket; sbd_op_wait(ticket) blocks
+ * until q is in host memory. Consecutive calls overlap the copies of one call
+ * with the device work of its neighbours (two staging slots, two copy
+ * streams). f must stay unchanged and q untouched until the wait; pinned
+ * host memory gives asynchronous copies. */
+int sbd_op_apply_async(sbd_op* op, const double* f, double* q, int nrhs, uint64_t* ticket);
+int sbd_op_wait(sbd_op* op, uint64_t ticket);
 /* Same on device buffers, enqueued on `stream` (a cudaStream_t; NULL is the
  * legacy default stream, as everywhere in CUDA). Returns without
  * synchronising (and is CUDA-graph capturable). Whether f is real is decided

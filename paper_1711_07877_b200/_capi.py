@@ -70,6 +70,8 @@ _sig("sbd_op_info", _int, _vp, ctypes.POINTER(OpInfoC))
 _sig("sbd_op_get", _int, _vp, _int, _vp, ctypes.POINTER(_u64))
 _sig("sbd_op_apply", _int, _vp, _dp, _dp, _int)
 _sig("sbd_op_apply_adjoint", _int, _vp, _dp, _dp, _int)
+_sig("sbd_op_apply_async", _int, _vp, _dp, _dp, _int, ctypes.POINTER(_u64))
+_sig("sbd_op_wait", _int, _vp, _u64)
 _sig("sbd_op_apply_device", _int, _vp, _vp, _vp, _int, _vp)
 _sig("sbd_op_apply_device_ex", _int, _vp, _vp, _vp, _int, _vp, ctypes.POINTER(_int))
 _sig("sbd_op_apply_adjoint_device", _int, _vp, _vp, _vp, _int, _vp)
@@ -98,7 +100,8 @@ _sig("sbd_choose_parameters", _int, _u64, ctypes.c_double, ctypes.c_double, _dp,
 EXPORTED = [
     "sbd_last_error", "sbd_version", "sbd_assemble_options_default", "sbd_op_options_default",
     "sbd_op_assemble", "sbd_op_load", "sbd_op_load_ex", "sbd_op_save", "sbd_op_destroy", "sbd_op_info", "sbd_op_get",
-    "sbd_op_apply", "sbd_op_apply_adjoint", "sbd_op_apply_device", "sbd_op_apply_device_ex",
+    "sbd_op_apply", "sbd_op_apply_adjoint", "sbd_op_apply_async", "sbd_op_wait",
+    "sbd_op_apply_device", "sbd_op_apply_device_ex",
     "sbd_op_apply_adjoint_device", "sbd_op_set_profiling", "sbd_op_stage_times",
     "sbd_op_stage_times_reset", "sbd_cloud_diameter",
     "sbd_nufft_create", "sbd_nufft_apply", "sbd_nufft_apply_transpose", "sbd_nufft_info",

@@ -205,6 +205,16 @@ struct sbd_op {
     FftWork work;
     DevBuf<double2> spec;
     DevBuf<double2> hf, hq; // staging for the host-buffer API
+    // Pipelined host-buffer API (sbd_op_apply_async): two staging slots, the
+    // H2D of f on cp_in, the apply on `stream`, the D2H of q on cp_out, so
+    // the copies of one call overlap the device work of its neighbours.
+    struct Slot {
+        DevBuf<double2> f, q;
+        cudaEvent_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+        bool used = false;
+    } slot[2];
+    cudaStream_t cp_in = nullptr, cp_out = nullptr;
+    uint64_t tickets = 0;
     // Fused forward path (both plans gridded): D renumbered to (sorted target
     // row, sorted source column) so its f gathers are spatially local, and
     // kappa = omega-hat * fwd_out prephase so the xi interpolation emits the
@@ -254,6 +264,11 @@ struct sbd_op {
 
     sbd_op() { sbd_op_options_default(&opt); }
     ~sbd_op() {
+        for (Slot& sl : slot)
+            for (cudaEvent_t e : {sl.h2d, sl.comp, sl.d2h})
+                if (e) cudaEventDestroy(e);
+        if (cp_in) cudaStreamDestroy(cp_in);
+        if (cp_out) cudaStreamDestroy(cp_out);
         if (done) cudaEventDestroy(done);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -1050,6 +1065,70 @@ static int host_apply(sbd_op* op, const double* in, double* out, int nrhs, bool 
         ck(cudaMemcpyAsync(out, op->hq.p, nout * nrhs * 16, cudaMemcpyDeviceToHost, op->stream), "D2H q");
         ck(cudaStreamSynchronize(op->stream), "apply sync");
         op->order_end(op->stream);
+    });
+}
+
+int sbd_op_apply_async(sbd_op* op, const double* f, double* q, int nrhs, uint64_t* ticket) {
+    return guarded([&] {
+        if (!op || !f || !q || nrhs < 1 || !ticket) throw Error(SBD_ERR_INVALID_ARGUMENT, "apply_async: bad argument");
+        std::lock_guard<std::recursive_mutex> lk(op->mu);
+        DeviceGuard g(op->device);
+        const uint64_t nin = op->d.n_src(), nout = op->d.n_tgt();
+        if (!op->cp_in) {
+            ck(cudaStreamCreateWithFlags(&op->cp_in, cudaStreamNonBlocking), "stream");
+            ck(cudaStreamCreateWithFlags(&op->cp_out, cudaStreamNonBlocking), "stream");
+            for (auto& sl : op->slot)
+                for (cudaEvent_t* e : {&sl.h2d, &sl.comp, &sl.d2h})
+                    ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+        }
+        const uint64_t t = op->tickets++;
+        sbd_op::Slot& sl = op->slot[t & 1];
+        if (sl.f.n < nin * nrhs || sl.q.n < nout * nrhs) {
+            // (re)allocating a slot's buffers: its previous call must be done
+            if (sl.used) ck(cudaEventSynchronize(sl.d2h), "apply_async slot");
+            if (sl.f.n < nin * nrhs) sl.f.alloc(nin * nrhs);
+            if (sl.q.n < nout * nrhs) sl.q.alloc(nout * nrhs);
+        }
+        // realness per column, on the host while earlier calls run
+        std::vector<int> real(nrhs, 1);
+        for (int r = 0; r < nrhs; ++r) {
+            const double* x = f + (size_t)r * nin * 2;
+            int any = 0;
+#pragma omp parallel for reduction(| : any) schedule(static)
+            for (int64_t i = 0; i < (int64_t)nin; ++i) any |= x[2 * i + 1] != 0.0;
+            real[r] = !any;
+        }
+        // H2D of f once the slot's previous apply has consumed its input
+        if (sl.used) ck(cudaStreamWaitEvent(op->cp_in, sl.comp, 0), "wait");
+        ck(cudaMemcpyAsync(sl.f.p, f, nin * nrhs * 16, cudaMemcpyHostToDevice, op->cp_in), "H2D f");
+        ck(cudaEventRecord(sl.h2d, op->cp_in), "event");
+        // the apply once f is in and the slot's previous q has left
+        ck(cudaStreamWaitEvent(op->stream, sl.h2d, 0), "wait");
+        if (sl.used) ck(cudaStreamWaitEvent(op->stream, sl.d2h, 0), "wait");
+        apply_device_rhs(op, (const double*)sl.f.p, (double*)sl.q.p, nrhs, op->stream, real.data());
+        ck(cudaEventRecord(sl.comp, op->stream), "event");
+        // D2H of q
+        ck(cudaStreamWaitEvent(op->cp_out, sl.comp, 0), "wait");
+        ck(cudaMemcpyAsync(q, sl.q.p, nout * nrhs * 16, cudaMemcpyDeviceToHost, op->cp_out), "D2H q");
+        ck(cudaEventRecord(sl.d2h, op->cp_out), "event");
+        sl.used = true;
+        *ticket = t;
+    });
+}
+
+int sbd_op_wait(sbd_op* op, uint64_t ticket) {
+    return guarded([&] {
+        if (!op) throw Error(SBD_ERR_INVALID_ARGUMENT, "wait: null operator");
+        cudaEvent_t e = nullptr;
+        {
+            std::lock_guard<std::recursive_mutex> lk(op->mu);
+            if (ticket >= op->tickets) throw Error(SBD_ERR_INVALID_ARGUMENT, "wait: unknown ticket");
+            // a slot's event is re-recorded by the call two tickets later, which
+            // completes after this one: waiting on it is waiting long enough
+            e = op->slot[ticket & 1].d2h;
+        }
+        DeviceGuard g(op->device);
+        ck(cudaEventSynchronize(e), "wait");
     });
 }
 

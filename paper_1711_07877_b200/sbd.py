@@ -314,6 +314,16 @@ class CompressedOperator:
         check(lib.sbd_op_apply(self._h, ctypes.cast(f_ptr, _dp), ctypes.cast(q_ptr, _dp),
                                int(nrhs)))
 
+    def apply_async(self, f_ptr: int, q_ptr: int, nrhs: int = 1) -> int:
+        """sbd_op_apply_async on raw host pointers; returns the ticket for wait()."""
+        t = ctypes.c_uint64()
+        check(lib.sbd_op_apply_async(self._h, ctypes.cast(f_ptr, _dp), ctypes.cast(q_ptr, _dp), int(nrhs),
+                                     ctypes.byref(t)))
+        return t.value
+
+    def wait(self, ticket: int) -> None:
+        check(lib.sbd_op_wait(self._h, int(ticket)))
+
     def apply_adjoint_device(self, u_ptr: int, q_ptr: int, nrhs: int = 1, stream: int = 0) -> None:
         check(lib.sbd_op_apply_adjoint_device(self._h, ctypes.c_void_p(u_ptr),
                                               ctypes.c_void_p(q_ptr), int(nrhs),

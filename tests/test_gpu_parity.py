@@ -437,3 +437,20 @@ def test_device_apply_is_graph_capturable(ops):
     graph.replay()
     torch.cuda.synchronize()
     assert rel_l2(qd.cpu().numpy().view(np.complex128), want) <= 1e-14
+
+
+def test_async_host_applies_pipeline_and_match(ops):
+    # sbd_op_apply_async: several calls in flight over two staging slots, each
+    # result equal to the synchronous apply
+    _, g = golden("lap_star_n1500")
+    op = ops["lap_star_n1500"]
+    rng = np.random.default_rng(80)
+    n = len(g["f"])
+    fs = [np.ascontiguousarray(rng.standard_normal(n) + (1j * rng.standard_normal(n) if i % 2 else 0.0),
+                               dtype=np.complex128) for i in range(5)]
+    qs = [np.zeros(n, np.complex128) for _ in fs]
+    tickets = [op.apply_async(f.ctypes.data, q.ctypes.data, 1) for f, q in zip(fs, qs)]
+    for t in tickets:
+        op.wait(t)
+    for f, q in zip(fs, qs):
+        assert rel_l2(q, op.apply(f)) <= 1e-14

@@ -16,7 +16,7 @@ import numpy as np
 import pytest
 
 import paper_1711_07877_b200 as sbd
-from tests.clouds import disk_cloud
+from tests.clouds import disk_cloud, star_curve_cloud, star_interior_cloud
 from tests.conftest import rel_l2
 
 pytestmark = pytest.mark.gpu
@@ -83,3 +83,27 @@ def test_big_direct_sum_1000_targets(big):
         with np.errstate(divide="ignore"):
             want += np.where(d > 0, np.log(np.where(d > 0, d, 1.0)), 0.0) @ f[s:s + 50_000].real
     assert np.max(np.abs(q[rows] - want)) <= op.eps() * np.abs(f).sum()
+
+
+def test_config5_shape_vs_reference(tmp_path, reflib):
+    # BASELINE configs[4]'s shape at N = 1e5: star curve (jitter 0.1) plus
+    # uniform interior points (10:1), Helmholtz k dmax = 2 pi 300, eps 1e-4,
+    # a block of 8 complex right-hand sides per apply (GMRES-style). The
+    # batched apply against the reference applying the same operator file
+    # column by column, and against this library's own single-column applies.
+    rng = np.random.default_rng(505)
+    z = np.concatenate([star_curve_cloud(90_000, rng), star_interior_cloud(9_000, rng)])
+    dmax = sbd.cloud_diameter(z)
+    op = sbd.CompressedOperator.assemble(
+        sbd.kernel_helmholtz(2 * np.pi * 300 / dmax), z,
+        opts=sbd.AssembleOptions(eps=1e-4, a_override=2e-3))
+    path = str(tmp_path / "helm_cfg5_shape.sbdop")
+    op.save(path)
+    n = len(z)
+    F = rng.standard_normal((8, n)) + 1j * rng.standard_normal((8, n))
+    Q = op.apply(F)
+    raw = reflib.raw(path, max_grid_bytes=16 << 30)
+    for r in (0, 5):
+        assert rel_l2(Q[r], raw.apply(F[r], n)) <= 1e-9, r
+    for r in range(8):
+        assert rel_l2(Q[r], op.apply(F[r])) <= 1e-13, r

@@ -29,6 +29,6 @@ f = bench.rhs(w, len(z), np.random.default_rng(1))
 fd = torch.from_numpy(f.view(np.float64).copy()).cuda()
 qd = torch.empty_like(fd)
 for _ in range(a.applies):
-    op.apply_device(fd.data_ptr(), qd.data_ptr(), 1, 0)
+    op.apply_device(fd.data_ptr(), qd.data_ptr(), 1, 0, f_is_real=not w["f_complex"])
 torch.cuda.synchronize()
 print("ok", op.info()["n_xi"])
