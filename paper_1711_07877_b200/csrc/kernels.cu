@@ -603,12 +603,13 @@ constexpr int kSCS = 18;   // scan segments: 2 point sets x 3 x 3 bins
 
 template <int W>
 struct SCta {
-    static constexpr int L = W + 14;     // padded tap row
+    static constexpr int L = W + 14;     // padded tap row (y taps)
+    static constexpr int LA = W + 15;    // x-tap row: one more cell for the even-base shift
     static constexpr int NP = kSCB + 1;  // staged points + the zero point
     static constexpr int LS = kSCB + 4;  // list stride (room for the padding)
-    static constexpr size_t smem = (size_t)NP * L * (sizeof(double2) + sizeof(double)) +
+    static constexpr size_t smem = (size_t)NP * (LA * sizeof(double2) + L * sizeof(double)) +
                                    (size_t)kSCQ * 2 * sizeof(double2) + (size_t)16 * LS * 4 +
-                                   (size_t)2 * kSCB * 4;
+                                   (size_t)3 * kSCB * 4;
     static constexpr size_t smem_list = smem - (size_t)kSCQ * 2 * sizeof(double2);  // LIST: no ring
 };
 
@@ -624,7 +625,7 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
     constexpr int L = S::L;
     extern __shared__ __align__(16) double smem_sc[];
     double2* sA = reinterpret_cast<double2*>(smem_sc);  // [NP][L]: b * x taps
-    double2* sQt = sA + S::NP * L;                       // queued positions (16-byte aligned)
+    double2* sQt = sA + S::NP * S::LA;                   // queued positions (16-byte aligned)
     double2* sQb = sQt + (LIST ? 0 : kSCQ);              // queued coefficients (scan mode only)
     double* sB = reinterpret_cast<double*>(sQb + (LIST ? 0 : kSCQ));  // [NP][L]: y taps
     uint32_t* sL = reinterpret_cast<uint32_t*>(sB + S::NP * L);  // [4 warps][4 sub-tiles][LS]
@@ -632,6 +633,12 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
     // sub-tile rows (x) / columns (y) its stencil covers
     int* sDX = reinterpret_cast<int*>(sL + 16 * S::LS);
     int* sDY = sDX + kSCB;
+    // A-fragment bank class of each staged point: its x-tap row starts on an
+    // even 16-byte bank group (row shifted by one cell when needed), class =
+    // (start mod 8) / 2. A DMMA group whose 4 points have 4 distinct classes
+    // reads its A fragment (4 points x 8 rows of 16 bytes) without bank
+    // conflicts; the lists below are laid out class by class
+    int* sCls = sDY + kSCB;
     __shared__ int sCnt[4];
     __shared__ uint32_t sSeg[kSCS], sPre[kSCS + 1];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -646,9 +653,9 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
     const int wr = warp >> 1, wc = warp & 1;
     const unsigned lt = (1u << lane) - 1u;
 
-    for (int i = tid; i < S::NP * L; i += 128) {
+    for (int i = tid; i < S::NP * S::LA; i += 128) {
         sA[i] = make_double2(0.0, 0.0);
-        sB[i] = 0.0;
+        if (i < S::NP * L) sB[i] = 0.0;
     }
     // scan segments: (set, bin) -> [first sorted position, size), prefix sums
     if (!LIST && warp == 0) {
@@ -693,14 +700,19 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
                 if (warp < 2) {
                     const int ix0 = (int)ceil(t.x - g.half);
                     const double u = (ix0 - t.x) + g.half;
-                    double2* a = sA + p * L + 7;
+                    const int dx = ix0 - X0;  // in [1 - W, 32)
+                    const int sh = (p * S::LA - dx + 7) & 1;  // even fragment base
+                    double2* a = sA + p * S::LA + sh + 7;
                     auto put = [&](int i, double v) { a[i] = make_double2(b2.x * v, b2.y * v); };
                     if (warp == 0) {
-                        const int dx = ix0 - X0;  // in [1 - W, 32)
                         const int r0 = max(0, ((dx + 64) >> 3) - 8), r1 = min(3, ((dx + W - 1 + 64) >> 3) - 8);
-                        sDX[p] = ((p * L - dx + 7) << 4) | (((2 << r1) - 1) & ~((1 << r0) - 1));
+                        const int base = p * S::LA + sh - dx + 7;
+                        sDX[p] = (base << 4) | (((2 << r1) - 1) & ~((1 << r0) - 1));
+                        sCls[p] = (base & 7) >> 1;
+                        a[-1] = make_double2(0.0, 0.0);  // a previous batch's tap, one cell before
                         kb_taps_slice<W, 0, H, false>(u, P, put);
                     } else {
+                        a[W] = make_double2(0.0, 0.0);   // ... or one cell after
                         kb_taps_slice<W, H, W / 2, true>(u, P, put);
                     }
                 } else {
@@ -720,35 +732,61 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
             }
         }
         __syncthreads();
-        // 2. this warp's four sub-tile lists: fragment row offsets per entry
+        // 2. this warp's four sub-tile lists: fragment row offsets per entry,
+        // laid out as G = ceil(hits / 4) groups x 4 class columns (entry g 4 + c
+        // holds a point of class c when there is one; a class with more than
+        // G hits overflows into the other columns' free slots, in order; the
+        // rest is the zero point at the column's class)
+        static_assert(kSCB == 32, "one point per lane");
         uint32_t* lst = sL + warp * 4 * S::LS;
-        int cnt[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int h = 0; h < (kSCB + 31) / 32; ++h) {
-            const int p = h * 32 + lane;
-            int ex = 0, ey = 0;
+        int cnt[4];
+        {
+            const int p = lane;
+            int ex = 0, ey = 0, cls = 0;
             if (p < n) {
                 ex = sDX[p] >> wr;  // row mask bit 0 = sub-tile row wr
                 ey = sDY[p] >> wc;
                 ex = (ex & 0xf) | ((sDX[p] >> 4) + 8 * wr) << 4;
                 ey = (ey & 0xf) | ((sDY[p] >> 4) + 8 * wc) << 4;
+                cls = sCls[p];
             }
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 const int i = 2 * (t >> 1), j = 2 * (t & 1);  // sub-tile (wr + i, wc + j)
                 const bool hit = (ex >> i) & (ey >> j) & 1;
-                const unsigned m = __ballot_sync(0xffffffffu, hit);
-                if (hit)
-                    lst[t * S::LS + cnt[t] + __popc(m & lt)] =
-                        (uint32_t)((ex >> 4) + 8 * i) | ((uint32_t)((ey >> 4) + 8 * j) << 16);
-                cnt[t] += __popc(m);
-            }
-        }
-        constexpr uint32_t zero = (uint32_t)(kSCB * L) | ((uint32_t)(kSCB * L) << 16);
+                int nc[4], rank = 0, tot = 0;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            if (lane < ((-cnt[t]) & 3)) lst[t * S::LS + cnt[t] + lane] = zero;
-            cnt[t] = (cnt[t] + 3) & ~3;
+                for (int c = 0; c < 4; ++c) {
+                    const unsigned m = __ballot_sync(0xffffffffu, hit && cls == c);
+                    nc[c] = __popc(m);
+                    if (cls == c) rank = __popc(m & lt);
+                    tot += nc[c];
+                }
+                const int G = (tot + 3) >> 2;
+                uint32_t* lt_ = lst + t * S::LS;
+                for (int q = lane; q < 4 * G; q += 32)
+                    lt_[q] = (uint32_t)(kSCB * S::LA + 2 * (q & 3)) | ((uint32_t)(kSCB * L) << 16);
+                __syncwarp();
+                if (hit) {
+                    int pos;
+                    if (rank < G) {
+                        pos = rank * 4 + cls;
+                    } else {
+                        int k = rank - G;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) k += c < cls ? max(nc[c] - G, 0) : 0;
+                        pos = 0;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const int h = max(G - nc[c], 0);
+                            if (k >= 0 && k < h) pos = (nc[c] + k) * 4 + c;
+                            k -= h;
+                        }
+                    }
+                    lt_[pos] = (uint32_t)((ex >> 4) + 8 * i) | ((uint32_t)((ey >> 4) + 8 * j) << 16);
+                }
+                cnt[t] = 4 * G;
+            }
         }
         __syncwarp();
         // 3. G[8 x 8] += A[8 x 4] B[4 x 8] per sub-tile, 4 listed points at a time
@@ -1239,6 +1277,81 @@ __global__ void __launch_bounds__(256) k_interp_real(WindowPoly P, GridGeom g, u
 // real band (deconvolution folded in) in shared memory; each thread then
 // interpolates one output of the block from shared memory. The band is read
 // from L2 once per block instead of W^2 times per output.
+// sum_i wx_i sum_j wy_j base[i PE + j] from a staged real tile, the row taps
+// produced a symmetric pair at a time (rows i and W-1-i share one even/odd
+// split) so that only the column taps stay live: ~half the registers of
+// holding both tap vectors, which keeps the shared-memory loads pipelined.
+template <int W, int PE>
+__device__ __forceinline__ double interp_rows_real(const double* __restrict__ base, double ux, double uy,
+                                                   const WindowPoly& P) {
+    double wy[W];
+    kb_taps<W>(uy, P, wy);
+    const double v = 2.0 * ux - 1.0;
+    const double v2 = v * v;
+    double ar = 0.0;
+#pragma unroll
+    for (int i = 0; i < W / 2; ++i) {
+        double e = P.e[i][kHorner - 1], o = P.o[i][kHorner - 1];
+#pragma unroll
+        for (int h = kHorner - 2; h >= 0; --h) {
+            e = fma(e, v2, P.e[i][h]);
+            o = fma(o, v2, P.o[i][h]);
+        }
+        double r0 = 0.0, r1 = 0.0;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            r0 = fma(base[i * PE + j], wy[j], r0);
+            r1 = fma(base[(W - 1 - i) * PE + j], wy[j], r1);
+        }
+        ar = fma(r0, fma(v, o, e), ar);
+        ar = fma(r1, fma(-v, o, e), ar);
+    }
+    if (W & 1) {
+        constexpr int m = W / 2;
+        double e = P.e[m][kHorner - 1];
+#pragma unroll
+        for (int h = kHorner - 2; h >= 0; --h) e = fma(e, v2, P.e[m][h]);
+        double r0 = 0.0;
+#pragma unroll
+        for (int j = 0; j < W; ++j) r0 = fma(base[m * PE + j], wy[j], r0);
+        ar = fma(r0, e, ar);
+    }
+    return ar;
+}
+
+// The rows i = part, part + K, ... of the same sum (K lanes share an output);
+// each row's tap evaluated on its own (pair index from the row), so every
+// index stays static except the tap-polynomial row (a constant-bank load).
+template <int W, int PE, int K>
+__device__ __forceinline__ double interp_rows_part(const double* __restrict__ base, double ux, double uy,
+                                                   const WindowPoly& P, int part) {
+    double wy[W];
+    kb_taps<W>(uy, P, wy);
+    const double v = 2.0 * ux - 1.0;
+    const double v2 = v * v;
+    const double* b = base + part * PE;
+    double ar = 0.0;
+#pragma unroll
+    for (int m = 0; m < (W + K - 1) / K; ++m) {
+        const int i = part + K * m;
+        if (i < W) {
+            const int p = i < W - 1 - i ? i : W - 1 - i;
+            double e = P.e[p][kHorner - 1], o = P.o[p][kHorner - 1];
+#pragma unroll
+            for (int h = kHorner - 2; h >= 0; --h) {
+                e = fma(e, v2, P.e[p][h]);
+                o = fma(o, v2, P.o[p][h]);
+            }
+            const double tap = 2 * i == W - 1 ? e : (i < W - 1 - i ? fma(v, o, e) : fma(-v, o, e));
+            double rr = 0.0;
+#pragma unroll
+            for (int j = 0; j < W; ++j) rr = fma(b[K * m * PE + j], wy[j], rr);
+            ar = fma(rr, tap, ar);
+        }
+    }
+    return ar;
+}
+
 template <int W>
 __global__ void __launch_bounds__(128, 8) k_interp_real_tile(
     WindowPoly P, GridGeom g, const uint32_t* __restrict__ tstart, uint32_t ntiles, int shift,
@@ -1288,29 +1401,49 @@ __global__ void __launch_bounds__(128, 8) k_interp_real_tile(
             }
         }
         __syncthreads();
-        for (uint64_t va = a0 + threadIdx.x; va < a1; va += blockDim.x) {
+        // one thread per output for whole rounds of 128; the last partial round
+        // splits each remaining output's rows over K = 4 / 2 / 1 lanes, so a
+        // block with a few more outputs than threads (~30% of the blocks at
+        // 0.12 outputs per cell) does not pay a second full output latency
+        const uint32_t cnt = (uint32_t)(a1 - a0);
+        const uint32_t full = cnt & ~127u;
+        auto emit = [&](uint64_t va, double ar) {
             const uint64_t v = va - out_lo;
-            const double2 sv = pos[v];
             const double2 ph = phase[v];
             const double2 ad = addend ? addend[v] : make_double2(0.0, 0.0);
-            const uint32_t dst = perm ? perm[v] : (uint32_t)v;
+            out[perm ? perm[v] : (uint32_t)v] = make_double2(ar * ph.x + ad.x, ad.y);
+        };
+        for (uint32_t k = threadIdx.x; k < full; k += 128) {
+            const double2 sv = pos[a0 + k - out_lo];
             const int ix = (int)ceil(sv.x - g.half), iy = (int)ceil(sv.y - g.half);
-            double wx[W], wy[W];
-            kb_taps<W>((ix - sv.x) + g.half, P, wx);
-            kb_taps<W>((iy - sv.y) + g.half, P, wy);
-            const double* base = S + (ix - X0) * PE + (iy - Y0);
+            emit(a0 + k, interp_rows_real<W, PE>(S + (ix - X0) * PE + (iy - Y0), (ix - sv.x) + g.half,
+                                                 (iy - sv.y) + g.half, P));
+        }
+        const uint32_t rem = cnt - full;
+        if (rem) {
+            const int K = rem <= 32 ? 4 : rem <= 64 ? 2 : 1;
+            const uint32_t k = threadIdx.x / K;
+            const int part = threadIdx.x % K;
             double ar = 0.0;
-#pragma unroll
-            for (int i = 0; i < W; ++i) {
-                double rr = 0.0;
-#pragma unroll
-                for (int j = 0; j < W; ++j) rr = fma(base[i * PE + j], wy[j], rr);
-                ar = fma(rr, wx[i], ar);
+            if (k < rem) {
+                const double2 sv = pos[a0 + full + k - out_lo];
+                const int ix = (int)ceil(sv.x - g.half), iy = (int)ceil(sv.y - g.half);
+                const double* base = S + (ix - X0) * PE + (iy - Y0);
+                const double ux = (ix - sv.x) + g.half, uy = (iy - sv.y) + g.half;
+                if (K == 1)
+                    ar = interp_rows_real<W, PE>(base, ux, uy, P);
+                else if (K == 2)
+                    ar = interp_rows_part<W, PE, 2>(base, ux, uy, P, part);
+                else
+                    ar = interp_rows_part<W, PE, 4>(base, ux, uy, P, part);
             }
-            out[dst] = make_double2(ar * ph.x + ad.x, ad.y);
+            if (K > 1) ar += __shfl_xor_sync(0xffffffffu, ar, 1);
+            if (K > 2) ar += __shfl_xor_sync(0xffffffffu, ar, 2);
+            if (k < rem && part == 0) emit(a0 + full + k, ar);
         }
     }
 }
+
 
 // ---- tile-staged tensor-core interpolation -------------------------------
 // Outputs are Z-ordered by stencil cell, so the outputs whose stencil starts
@@ -2333,6 +2466,65 @@ void launch_interp_real(int w, const WindowPoly& win, GridGeom g, uint64_t n, co
     dispatch_w<InterpRealRun>(w, win, g, n, pos, phase, dx, dy, grid, perm, addend, out, st, tiles, variant);
     count_launch();
     ck(cudaGetLastError(), "k_interp_real");
+}
+
+// Within each 32 x 32 block of Z-ordered outputs, deal the outputs round-robin
+// over the 16 shared-memory double-banks their staged-tile reads start on
+// (k_interp_real_tile: lane = output, address (ix - X0) PE + (iy - Y0) + i PE
+// + j), so each warp's 32 outputs spread ~2 per double-bank: the tap loads of
+// the staged target interpolation need ~2 wavefronts instead of ~4.6 for
+// random positions. The order inside a block is otherwise free.
+// map[new sorted position] = old sorted position.
+__global__ void __launch_bounds__(128) k_bank_interleave(const uint32_t* __restrict__ tstart, uint32_t ntiles,
+                                                         const double2* __restrict__ pos, double half, int shift,
+                                                         int pe, uint32_t* __restrict__ map) {
+    constexpr int kMax = 1024;
+    __shared__ uint8_t sb[kMax];
+    __shared__ uint16_t srank[kMax];
+    __shared__ int cntb[16];
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint32_t t0 = tstart[t], t1 = tstart[t + 1];
+        const uint32_t c = t1 - t0;
+        if (c > kMax) {  // (dense block: keep the Z order)
+            for (uint32_t k = threadIdx.x; k < c; k += blockDim.x) map[t0 + k] = t0 + k;
+            continue;
+        }
+        const double2 s0 = pos[t0];
+        const int X0 = (((int)ceil(s0.x - half) + shift) & ~31) - shift;
+        const int Y0 = (((int)ceil(s0.y - half) + shift) & ~31) - shift;
+        __syncthreads();
+        if (threadIdx.x < 16) cntb[threadIdx.x] = 0;
+        for (uint32_t k = threadIdx.x; k < c; k += blockDim.x) {
+            const double2 sv = pos[t0 + k];
+            const int ix = (int)ceil(sv.x - half), iy = (int)ceil(sv.y - half);
+            sb[k] = (uint8_t)((((ix - X0) * pe + (iy - Y0)) % 16 + 16) % 16);
+        }
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < c; k += blockDim.x) {
+            int r = 0;
+            for (uint32_t q = 0; q < k; ++q) r += sb[q] == sb[k];
+            srank[k] = (uint16_t)r;
+            atomicAdd(&cntb[sb[k]], 1);
+        }
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < c; k += blockDim.x) {
+            const int r = srank[k], b = sb[k];
+            int p = 0;
+            for (int q = 0; q < 16; ++q) p += min(cntb[q], r) + (q < b && cntb[q] > r ? 1 : 0);
+            map[t0 + p] = t0 + k;
+        }
+    }
+}
+
+void bank_interleave_outputs(const uint32_t* tile_start, uint32_t ntiles, const double2* pos, uint64_t n, int w,
+                             int shift, DevBuf<uint32_t>& map, cudaStream_t st) {
+    map.alloc(std::max<uint64_t>(n, 1));
+    if (!ntiles) return;
+    const int pe = (32 + w - 1) | 1;  // k_interp_real_tile's staged-tile pitch
+    k_bank_interleave<<<std::min<uint32_t>(ntiles, 148 * 16), 128, 0, st>>>(tile_start, ntiles, pos, 0.5 * w, shift,
+                                                                          pe, map.p);
+    count_launch();
+    ck(cudaGetLastError(), "k_bank_interleave");
 }
 
 void build_tile_starts(const uint32_t* sorted_keys, uint64_t n, int bits, DevBuf<uint32_t>& start,

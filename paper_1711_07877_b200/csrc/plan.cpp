@@ -198,6 +198,22 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
             // 32 x 32 blocks of the Z order (k_interp_tile)
             out_shift = oshift;
             build_tile_starts(keys.p, n, 10, out_tiles, n_out_tiles, st);
+            // sparse outputs (the targets; < 0.25 per band cell) are interpolated
+            // one per thread from a staged real tile: order each block for
+            // conflict-free shared-memory reads (the dense xi side keeps its
+            // Z order for the 8-node tensor-core groups)
+            if ((double)n < 0.25 * ((double)ax.n * (double)ay.n / 4.0) && !tagged_out) {
+                DevBuf<uint32_t> map;
+                bank_interleave_outputs(out_tiles.p, n_out_tiles, pos.p, n, w, oshift, map, st);
+                DevBuf<double2> a(n), b(n);
+                DevBuf<uint32_t> c(n);
+                launch_gather(pos.p, map.p, a.p, n, st);
+                launch_gather(ph.p, map.p, b.p, n, st);
+                launch_gather(perm.p, map.p, c.p, n, st);
+                pos = std::move(a);
+                ph = std::move(b);
+                perm = std::move(c);
+            }
         }
         ck(cudaStreamSynchronize(st), "sort side");
     };
@@ -353,6 +369,7 @@ bool Plan::enable_hfft(int role, cudaStream_t st) {
         } else {
             ckfft(cufftPlanMany(&hp2, 1, nr, nr, 1, n2, nr, 1, n2, CUFFT_Z2Z, K), "hfft Z2Z rows");
         }
+
     } else {
         return false;
     }

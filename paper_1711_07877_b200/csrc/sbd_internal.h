@@ -164,6 +164,8 @@ struct TileGeom {
 // ("s": gather in apply, spread in apply_transpose) are stored in a sorted
 // order chosen for locality; perm_* map sorted position -> caller index (empty
 // when the caller's order is kept).
+
+
 // Plan-time region lists of the CTA spread: for each 32 x 32 region (row-major,
 // ncy regions per row) the entries (point index | 0x80000000 for the second
 // point arrays) of the points whose stencil overlaps it; list 2 is skipped
@@ -395,6 +397,8 @@ void launch_pack_rows(const double2* Y, int n1, int m0, int n2, int b1, int B1, 
 // transform folded in (rows in (j mod R) M + j / R order); tw[m] = e^{+2 pi i m / n2}
 void launch_pack_dif(const double2* Y, int n1, int m0, int n2, int b1, int B1, double2* Z, int R,
                      const double2* tw, cudaStream_t st);
+
+
 // interpolation from a real band grid whose rows are packed in pairs (row r =
 // component r & 1 of complex row r >> 1, complex pitch g.n2):
 // out[perm?perm[k]:k] = Re(sum taps * dx dy * grid * phase[k]) + addend[k]
@@ -449,6 +453,10 @@ void launch_interp(int w, const WindowPoly& win, GridGeom g, uint64_t n, const d
                    int conj_out, cudaStream_t st, const double2* addend = nullptr,
                    bool transposed = false, const InterpTiles* tiles = nullptr,
                    const HermArgs* herm = nullptr, int variant = 0);  // variant: NufftOpts::interp_kernel
+// map[new] = old sorted position: outputs of each Z-order block dealt round-robin
+// over the shared-memory banks of the staged real target interpolation
+void bank_interleave_outputs(const uint32_t* tile_start, uint32_t ntiles, const double2* pos, uint64_t n, int w,
+                             int shift, DevBuf<uint32_t>& map, cudaStream_t st);
 // sorted keys -> starts of the runs of equal key >> bits
 void build_tile_starts(const uint32_t* sorted_keys, uint64_t n, int bits, DevBuf<uint32_t>& start,
                        uint32_t& ntiles, cudaStream_t st);
