@@ -603,13 +603,12 @@ constexpr int kSCS = 18;   // scan segments: 2 point sets x 3 x 3 bins
 
 template <int W>
 struct SCta {
-    static constexpr int L = W + 14;     // padded tap row (y taps)
-    static constexpr int LA = W + 15;    // x-tap row: one more cell for the even-base shift
+    static constexpr int L = W + 14;     // padded tap row
     static constexpr int NP = kSCB + 1;  // staged points + the zero point
     static constexpr int LS = kSCB + 4;  // list stride (room for the padding)
-    static constexpr size_t smem = (size_t)NP * (LA * sizeof(double2) + L * sizeof(double)) +
+    static constexpr size_t smem = (size_t)NP * L * (sizeof(double2) + sizeof(double)) +
                                    (size_t)kSCQ * 2 * sizeof(double2) + (size_t)16 * LS * 4 +
-                                   (size_t)3 * kSCB * 4;
+                                   (size_t)2 * kSCB * 4;
     static constexpr size_t smem_list = smem - (size_t)kSCQ * 2 * sizeof(double2);  // LIST: no ring
 };
 
@@ -625,7 +624,7 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
     constexpr int L = S::L;
     extern __shared__ __align__(16) double smem_sc[];
     double2* sA = reinterpret_cast<double2*>(smem_sc);  // [NP][L]: b * x taps
-    double2* sQt = sA + S::NP * S::LA;                   // queued positions (16-byte aligned)
+    double2* sQt = sA + S::NP * L;                       // queued positions (16-byte aligned)
     double2* sQb = sQt + (LIST ? 0 : kSCQ);              // queued coefficients (scan mode only)
     double* sB = reinterpret_cast<double*>(sQb + (LIST ? 0 : kSCQ));  // [NP][L]: y taps
     uint32_t* sL = reinterpret_cast<uint32_t*>(sB + S::NP * L);  // [4 warps][4 sub-tiles][LS]
@@ -633,12 +632,6 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
     // sub-tile rows (x) / columns (y) its stencil covers
     int* sDX = reinterpret_cast<int*>(sL + 16 * S::LS);
     int* sDY = sDX + kSCB;
-    // A-fragment bank class of each staged point: its x-tap row starts on an
-    // even 16-byte bank group (row shifted by one cell when needed), class =
-    // (start mod 8) / 2. A DMMA group whose 4 points have 4 distinct classes
-    // reads its A fragment (4 points x 8 rows of 16 bytes) without bank
-    // conflicts; the lists below are laid out class by class
-    int* sCls = sDY + kSCB;
     __shared__ int sCnt[4];
     __shared__ uint32_t sSeg[kSCS], sPre[kSCS + 1];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -653,9 +646,9 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
     const int wr = warp >> 1, wc = warp & 1;
     const unsigned lt = (1u << lane) - 1u;
 
-    for (int i = tid; i < S::NP * S::LA; i += 128) {
+    for (int i = tid; i < S::NP * L; i += 128) {
         sA[i] = make_double2(0.0, 0.0);
-        if (i < S::NP * L) sB[i] = 0.0;
+        sB[i] = 0.0;
     }
     // scan segments: (set, bin) -> [first sorted position, size), prefix sums
     if (!LIST && warp == 0) {
@@ -700,19 +693,14 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
                 if (warp < 2) {
                     const int ix0 = (int)ceil(t.x - g.half);
                     const double u = (ix0 - t.x) + g.half;
-                    const int dx = ix0 - X0;  // in [1 - W, 32)
-                    const int sh = (p * S::LA - dx + 7) & 1;  // even fragment base
-                    double2* a = sA + p * S::LA + sh + 7;
+                    double2* a = sA + p * L + 7;
                     auto put = [&](int i, double v) { a[i] = make_double2(b2.x * v, b2.y * v); };
                     if (warp == 0) {
+                        const int dx = ix0 - X0;  // in [1 - W, 32)
                         const int r0 = max(0, ((dx + 64) >> 3) - 8), r1 = min(3, ((dx + W - 1 + 64) >> 3) - 8);
-                        const int base = p * S::LA + sh - dx + 7;
-                        sDX[p] = (base << 4) | (((2 << r1) - 1) & ~((1 << r0) - 1));
-                        sCls[p] = (base & 7) >> 1;
-                        a[-1] = make_double2(0.0, 0.0);  // a previous batch's tap, one cell before
+                        sDX[p] = ((p * L - dx + 7) << 4) | (((2 << r1) - 1) & ~((1 << r0) - 1));
                         kb_taps_slice<W, 0, H, false>(u, P, put);
                     } else {
-                        a[W] = make_double2(0.0, 0.0);   // ... or one cell after
                         kb_taps_slice<W, H, W / 2, true>(u, P, put);
                     }
                 } else {
@@ -732,61 +720,35 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
             }
         }
         __syncthreads();
-        // 2. this warp's four sub-tile lists: fragment row offsets per entry,
-        // laid out as G = ceil(hits / 4) groups x 4 class columns (entry g 4 + c
-        // holds a point of class c when there is one; a class with more than
-        // G hits overflows into the other columns' free slots, in order; the
-        // rest is the zero point at the column's class)
-        static_assert(kSCB == 32, "one point per lane");
+        // 2. this warp's four sub-tile lists: fragment row offsets per entry
         uint32_t* lst = sL + warp * 4 * S::LS;
-        int cnt[4];
-        {
-            const int p = lane;
-            int ex = 0, ey = 0, cls = 0;
+        int cnt[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int h = 0; h < (kSCB + 31) / 32; ++h) {
+            const int p = h * 32 + lane;
+            int ex = 0, ey = 0;
             if (p < n) {
                 ex = sDX[p] >> wr;  // row mask bit 0 = sub-tile row wr
                 ey = sDY[p] >> wc;
                 ex = (ex & 0xf) | ((sDX[p] >> 4) + 8 * wr) << 4;
                 ey = (ey & 0xf) | ((sDY[p] >> 4) + 8 * wc) << 4;
-                cls = sCls[p];
             }
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 const int i = 2 * (t >> 1), j = 2 * (t & 1);  // sub-tile (wr + i, wc + j)
                 const bool hit = (ex >> i) & (ey >> j) & 1;
-                int nc[4], rank = 0, tot = 0;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const unsigned m = __ballot_sync(0xffffffffu, hit && cls == c);
-                    nc[c] = __popc(m);
-                    if (cls == c) rank = __popc(m & lt);
-                    tot += nc[c];
-                }
-                const int G = (tot + 3) >> 2;
-                uint32_t* lt_ = lst + t * S::LS;
-                for (int q = lane; q < 4 * G; q += 32)
-                    lt_[q] = (uint32_t)(kSCB * S::LA + 2 * (q & 3)) | ((uint32_t)(kSCB * L) << 16);
-                __syncwarp();
-                if (hit) {
-                    int pos;
-                    if (rank < G) {
-                        pos = rank * 4 + cls;
-                    } else {
-                        int k = rank - G;
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) k += c < cls ? max(nc[c] - G, 0) : 0;
-                        pos = 0;
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            const int h = max(G - nc[c], 0);
-                            if (k >= 0 && k < h) pos = (nc[c] + k) * 4 + c;
-                            k -= h;
-                        }
-                    }
-                    lt_[pos] = (uint32_t)((ex >> 4) + 8 * i) | ((uint32_t)((ey >> 4) + 8 * j) << 16);
-                }
-                cnt[t] = 4 * G;
+                const unsigned m = __ballot_sync(0xffffffffu, hit);
+                if (hit)
+                    lst[t * S::LS + cnt[t] + __popc(m & lt)] =
+                        (uint32_t)((ex >> 4) + 8 * i) | ((uint32_t)((ey >> 4) + 8 * j) << 16);
+                cnt[t] += __popc(m);
             }
+        }
+        constexpr uint32_t zero = (uint32_t)(kSCB * L) | ((uint32_t)(kSCB * L) << 16);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            if (lane < ((-cnt[t]) & 3)) lst[t * S::LS + cnt[t] + lane] = zero;
+            cnt[t] = (cnt[t] + 3) & ~3;
         }
         __syncwarp();
         // 3. G[8 x 8] += A[8 x 4] B[4 x 8] per sub-tile, 4 listed points at a time
