@@ -381,6 +381,36 @@ def run_b200(args, w):
     ms_step = ms_total / args.steps
     value = n * R / (ms_step / 1e3)  # one apply of N points (x R right-hand sides) per step, whole job
 
+    # multi-GPU, right-hand-side parallel (weak scaling; SURVEY.md 8e "replicas
+    # across RHS"): every rank applies the full operator to its own right-hand
+    # side, no collective -- the batch-throughput mode, beside the sharded
+    # (strong-scaling, north_star) apply timed above
+    rhs_par = None
+    if world > 1:
+        f_own = torch.from_numpy(rhs(w, n, np.random.default_rng(SEED + 100 + rank)).view(np.float64).copy()).cuda()
+        q_own = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+
+        def own_step():
+            op.apply_device(f_own.data_ptr(), q_own.data_ptr(), 1, sh, f_is_real=f_real)
+        for _ in range(args.warmup):
+            own_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        for _ in range(args.steps):
+            own_step()
+        r1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([r0.elapsed_time(r1)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_rp = float(t.item()) / args.steps
+        rhs_par = {"value": n * world / (ms_rp / 1e3), "unit": "points/s", "ms_per_step": round(ms_rp, 3),
+                   "scaling": "weak",
+                   "note": f"{world} ranks, each one apply of its own N-point right-hand side per step, no collective"}
+        del f_own, q_own
+
     # per-stage averages over the timed region (CUDA events on the launch stream)
     agg = {}
     for name, ms in stages:
@@ -569,6 +599,7 @@ def run_b200(args, w):
             "clocks": clk,
             "batched_rhs": batched,
             "adjoint": adjoint,
+            "rhs_parallel": rhs_par,
             "contract": contract,
             "parity": parity,
         }

@@ -1744,7 +1744,7 @@ __global__ void __launch_bounds__(256) k_spmv_vec(uint64_t rows, const uint64_t*
                                                   const uint32_t* __restrict__ cols,
                                                   const double2* __restrict__ vals,
                                                   const double2* __restrict__ f,
-                                                  double2* __restrict__ qs) {
+                                                  double2* __restrict__ qs, int acc) {
     const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     const uint64_t r = g >> 3;
     const int sub = (int)(g & 7);
@@ -1765,7 +1765,70 @@ __global__ void __launch_bounds__(256) k_spmv_vec(uint64_t rows, const uint64_t*
         ar += __shfl_xor_sync(0xffffffffu, ar, o);
         ai += __shfl_xor_sync(0xffffffffu, ai, o);
     }
-    if (r < rows && sub == 0) qs[r] = make_double2(ar, ai);
+    if (r < rows && sub == 0) {
+        if (acc) {
+            const double2 o = qs[r];
+            ar += o.x;
+            ai += o.y;
+        }
+        qs[r] = make_double2(ar, ai);
+    }
+}
+
+// b[k] = conj?(in[perm[k]]) phase[k]: the transposed NUFFT's input times its
+// postphase (nufft.cpp:313-314)
+__global__ void k_gather_conj_mul(const double2* __restrict__ in, const uint32_t* __restrict__ perm,
+                                  const double2* __restrict__ phase, int conj_in, double2* __restrict__ b,
+                                  uint64_t n) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double2 c = in[perm ? perm[k] : k];
+    if (conj_in) c.y = -c.y;
+    b[k] = cmul(c, phase[k]);
+}
+
+// Deconvolution of the transposed spread (nufft.cpp:325-335) restricted to the
+// band (the factors are zero outside it), folded from the compact spread region
+// into the transposed band layout of the column transforms.
+__global__ void k_band_fold(const double2* __restrict__ Z, int pz, int rlo, int rhi, int clo, int chi, int b1,
+                            int n1, int b2, int B, int n2, const double* __restrict__ dx,
+                            const double* __restrict__ dy, double2* __restrict__ V) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const int R = 2 * b1 + 1;
+    if (k >= (uint64_t)R * B) return;
+    const int c = (int)(k / R), jx = (int)(k - (uint64_t)c * R) - b1;
+    const int jy = c <= b2 ? c : c - B;
+    const int mx = jx < 0 ? jx + n1 : jx, my = jy < 0 ? jy + n2 : jy;
+    double2 v = make_double2(0.0, 0.0);
+    if (jx >= rlo && jx < rhi && jy >= clo && jy < chi) {
+        const double2 z = Z[(size_t)(jx - rlo) * pz + (jy - clo)];
+        const double f = dx[mx] * dy[my];
+        v = make_double2(z.x * f, z.y * f);
+    }
+    V[(size_t)c * n1 + mx] = v;
+}
+
+// Tz[(r - r0) n2 + m(c)] = Wt[c n1 + r]: the transposed band back into rows
+// (32 x 32 tiles through shared memory, both sides coalesced)
+__global__ void __launch_bounds__(256) k_band_untranspose(const double2* __restrict__ Wt, int n1, int r0, int r1,
+                                                          int b, int B, double2* __restrict__ Tz, int n2) {
+    __shared__ double2 tile[32][33];
+    const int cb = blockIdx.x * 32, rb = r0 + blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+#pragma unroll
+    for (int q = 0; q < 32; q += 8) {
+        const int c = cb + ty + q, r = rb + tx;
+        if (r < r1 && c < B) tile[ty + q][tx] = Wt[(size_t)c * n1 + r];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 32; q += 8) {
+        const int r = rb + ty + q, c = cb + tx;
+        if (r < r1 && c < B) {
+            const int m = c <= b ? c : n2 - B + c;
+            Tz[(size_t)(r - r0) * n2 + m] = tile[tx][ty + q];
+        }
+    }
 }
 
 // Tt[c'][r] = T[r][m(c')] for r in [r0, r1) and the band columns c' in [0, B)
@@ -2528,9 +2591,9 @@ void launch_gather_mul(const double2* in, const uint32_t* perm, const double2* p
 }
 
 void launch_spmv_vec(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double2* vals,
-                     const double2* f, double2* qs, cudaStream_t st) {
+                     const double2* f, double2* qs, cudaStream_t st, bool accumulate) {
     if (!rows) return;
-    k_spmv_vec<<<blocks(rows * 8, 256), 256, 0, st>>>(rows, ro, cols, vals, f, qs);
+    k_spmv_vec<<<blocks(rows * 8, 256), 256, 0, st>>>(rows, ro, cols, vals, f, qs, accumulate ? 1 : 0);
     count_launch();
     ck(cudaGetLastError(), "k_spmv_vec");
 }
@@ -2622,6 +2685,31 @@ void launch_spmv_vec_real(uint64_t rows, const uint64_t* ro, const uint32_t* col
     k_spmv_vec_real<<<blocks(rows * 8, 256), 256, 0, st>>>(rows, ro, cols, vals, f, qs);
     count_launch();
     ck(cudaGetLastError(), "k_spmv_vec_real");
+}
+
+void launch_gather_conj_mul(const double2* in, const uint32_t* perm, const double2* phase, int conj_in,
+                            double2* b, uint64_t n, cudaStream_t st) {
+    if (!n) return;
+    k_gather_conj_mul<<<blocks(n, 256), 256, 0, st>>>(in, perm, phase, conj_in, b, n);
+    count_launch();
+    ck(cudaGetLastError(), "k_gather_conj_mul");
+}
+
+void launch_band_fold(const double2* Z, int pz, int rlo, int rhi, int clo, int chi, int b1, int n1, int b2,
+                      int B, int n2, const double* dx, const double* dy, double2* V, cudaStream_t st) {
+    const uint64_t n = (uint64_t)(2 * b1 + 1) * (uint64_t)B;
+    k_band_fold<<<blocks(n, 256), 256, 0, st>>>(Z, pz, rlo, rhi, clo, chi, b1, n1, b2, B, n2, dx, dy, V);
+    count_launch();
+    ck(cudaGetLastError(), "k_band_fold");
+}
+
+void launch_band_untranspose(const double2* Wt, int n1, int r0, int r1, int b, int B, double2* Tz, int n2,
+                             cudaStream_t st) {
+    if (r1 <= r0) return;
+    dim3 grid((unsigned)((B + 31) / 32), (unsigned)((r1 - r0 + 31) / 32));
+    k_band_untranspose<<<grid, 256, 0, st>>>(Wt, n1, r0, r1, b, B, Tz, n2);
+    count_launch();
+    ck(cudaGetLastError(), "k_band_untranspose");
 }
 
 void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int B, double2* Tt,

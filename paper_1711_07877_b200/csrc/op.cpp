@@ -700,12 +700,43 @@ struct sbd_op {
                               "fft_out", "interp_tgt", 0, ~0ull, lo, hi, shard_real ? &h : nullptr);
     }
 
-    // conv_operator.cpp:311-324
+    // D^H as its own CSR (rows = sources, entries in target order, values
+    // conjugated), built on the first adjoint: the near-field part of the
+    // adjoint becomes the same gather SpMV as the forward one instead of a
+    // scatter with fp64 atomics (point_cloud.cpp:125-132)
+    DevBuf<uint64_t> roT;
+    DevBuf<uint32_t> colsT;
+    DevBuf<double2> valsT;
+    bool dT_ready = false;
+    void build_adjoint_csr(cudaStream_t st) {
+        const uint64_t ns = d.n_src(), nt = d.n_tgt(), nnz = d.nnz();
+        std::vector<uint64_t> r(ns + 1, 0);
+        for (uint64_t i = 0; i < nnz; ++i) ++r[d.cols[i] + 1];
+        for (uint64_t c = 0; c < ns; ++c) r[c + 1] += r[c];
+        std::vector<uint64_t> pos(r.begin(), r.end() - 1);
+        std::vector<uint32_t> c2(nnz);
+        std::vector<double> v2(2 * nnz);
+        for (uint64_t t = 0; t < nt; ++t)
+            for (uint64_t i = d.row_offsets[t]; i < d.row_offsets[t + 1]; ++i) {
+                const uint64_t o = pos[d.cols[i]]++;
+                c2[o] = (uint32_t)t;
+                v2[2 * o] = d.values[2 * i];
+                v2[2 * o + 1] = -d.values[2 * i + 1];
+            }
+        roT.upload(r.data(), ns + 1, st);
+        colsT.upload(c2.data(), nnz, st);
+        valsT.upload(reinterpret_cast<const double2*>(v2.data()), nnz, st);
+        ck(cudaStreamSynchronize(st), "adjoint CSR");
+        dT_ready = true;
+    }
+
+    // conv_operator.cpp:311-324: A^H u = conj(fwd_in^T (w . fwd_out^T conj(u))) + D^H u
     void apply_adjoint_one(const double2* u, double2* q, cudaStream_t st) {
+        if (!dT_ready) build_adjoint_csr(st);
         fwd_out->apply_transpose(u, spec.p, work, st, &tm, w_sorted.p, /*conj_in=*/1, 0);
         fwd_in->apply_transpose(spec.p, q, work, st, &tm, nullptr, 0, /*conj_out=*/1);
         if (tm.on) tm.start("spmv_adjoint");
-        launch_spmv_adjoint(d.n_tgt(), ro.p, cols.p, vals.p, u, q, st);
+        launch_spmv_vec(d.n_src(), roT.p, colsT.p, valsT.p, u, q, st, /*accumulate=*/true);
         if (tm.on) tm.stop();
     }
 
@@ -714,7 +745,8 @@ struct sbd_op {
                ro_s.bytes() + cols_s.bytes() + vals_s.bytes() + vals_sr.bytes() + fs_all.bytes() + qs_all.bytes() + kappa.bytes() + f_sorted.bytes() +
                qs.bytes() + work.bbuf.bytes() +
                cols.bytes() + vals.bytes() + work.grid.bytes() + work.T.bytes() + work.band.bytes() +
-               spec.bytes() + hf.bytes() + hq.bytes() + kappa_h.bytes();
+               spec.bytes() + hf.bytes() + hq.bytes() + kappa_h.bytes() + roT.bytes() + colsT.bytes() +
+               valsT.bytes();
     }
 
     // conv_operator.cpp:338-353

@@ -441,7 +441,8 @@ void Plan::full_transform(double2* grid, cudaStream_t st) const {
 
 size_t Plan::device_bytes() const {
     return pts.bytes() + frq.bytes() + perm_t.bytes() + perm_s.bytes() + t.bytes() + pre.bytes() +
-           s.bytes() + post.bytes() + dx.bytes() + dy.bytes();
+           s.bytes() + post.bytes() + dx.bytes() + dy.bytes() + tpw.b.bytes() + tpw.Z.bytes() + tpw.V.bytes() +
+           tpw.Wt.bytes() + tpw.Tz.bytes() + tpw.G.bytes() + tpw.rl_s.bytes() + tpw.rl_e.bytes();
 }
 
 // nufft.cpp:218-290
@@ -676,10 +677,96 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
     }
 }
 
+// nufft.cpp:295-367 on the pruned plan. Every stage is the exact transpose of
+// the corresponding forward stage restricted to the cells that are nonzero or
+// read: the deconvolution factors vanish outside the band (|j| <= n/4), so the
+// transposed spread only matters there; the DFT is symmetric; the gather at
+// the points reads only the populated rows/columns.
+void Plan::apply_transpose_pruned(const double2* in, double2* out, cudaStream_t st, StageTimer* tm,
+                                  const double2* mult, int conj_in, int conj_out) const {
+    TransposeWork& T = tpw;
+    const int n1 = ax.n, n2 = ay.n;
+    const int b1 = n1 / 4;
+    const GridGeom g{n1, n2, 0.5 * w};
+    if (!T.ready) {
+        // tile geometry of the output side at its mode coordinates (stencil
+        // starts ceil(s - w/2), negative modes included) and its region lists
+        DevBuf<int> ext(4);
+        const int init[4] = {INT_MAX, INT_MIN, INT_MAX, INT_MIN};
+        ck(cudaMemcpyAsync(ext.p, init, sizeof(init), cudaMemcpyHostToDevice, st), "extent init");
+        launch_stencil_extent(s.p, nf, g.half, ext.p, st);
+        int he[4];
+        ck(cudaMemcpyAsync(he, ext.p, sizeof(he), cudaMemcpyDeviceToHost, st), "extent D2H");
+        ck(cudaStreamSynchronize(st), "extent");
+        TileGeom tg{};
+        tg.tr = 16;
+        tg.rlo = he[0];
+        tg.clo = he[2];
+        tg.nbx = (he[1] + w - he[0] + 15) / 16;
+        tg.nby = (he[3] + w - he[2] + kTileC - 1) / kTileC;
+        tg.rhi = tg.rlo + tg.nbx * 16;
+        tg.chi = tg.clo + tg.nby * kTileC;
+        tg.pitch = tg.chi - tg.clo;
+        T.tg = tg;
+        build_region_lists(s.p, nf, w, tg, 0u, 0u, T.rl_s, T.rl_e, st);
+        T.b.alloc(std::max<uint64_t>(nf, 1));
+        T.Z.alloc((size_t)(tg.rhi - tg.rlo) * tg.pitch);
+        T.V.alloc((size_t)bc * n1);
+        ck(cudaMemsetAsync(T.V.p, 0, T.V.bytes(), st), "V zero");  // rows outside the band stay zero
+        T.Wt.alloc((size_t)bc * n1);
+        T.Tz.alloc((size_t)(rhi - rlo) * n2);
+        ck(cudaMemsetAsync(T.Tz.p, 0, T.Tz.bytes(), st), "Tz zero");  // columns outside the band stay zero
+        T.G.alloc((size_t)(rhi - rlo) * n2);
+        ck(cudaStreamSynchronize(st), "transpose setup");
+        T.ready = true;
+    }
+    const TileGeom& tg = T.tg;
+    if (tm) tm->start("spread_T");
+    // postphase multiply, then the tile-owned spread at the mode stencils
+    launch_gather_conj_mul(in, perm_s.n ? perm_s.p : nullptr, post.p, conj_in, T.b.p, nf, st);
+    SpreadOut so;
+    so.mode = 0;
+    so.pitch = (size_t)tg.pitch;
+    so.r0 = tg.rlo;
+    so.c0 = tg.clo;
+    so.rend = tg.rhi;
+    so.cend = tg.chi;
+    so.nby_run = tg.nby;
+    so.lists.s1 = T.rl_s.p;
+    so.lists.e1 = T.rl_e.p;
+    so.lists.ncy = (tg.nby + 1) / 2;
+    launch_spread_tiles(w, win, g, tg, nullptr, T.b.p, s.p, T.Z.p, st, nullptr, nullptr, &so, &so.lists, 0);
+    // deconvolution (zero outside the band) into the transposed band
+    launch_band_fold(T.Z.p, tg.pitch, tg.rlo, tg.rhi, tg.clo, tg.chi, b1, n1, band2, bc, n2, dx.p, dy.p, T.V.p, st);
+    if (tm) tm->stop();
+    if (tm) tm->start("fft_T");
+    auto* V = reinterpret_cast<cufftDoubleComplex*>(T.V.p);
+    auto* Wt = reinterpret_cast<cufftDoubleComplex*>(T.Wt.p);
+    ckfft(cufftSetStream(fft_colT, st), "cufftSetStream");
+    ckfft(cufftExecZ2Z(fft_colT, V, Wt, CUFFT_INVERSE), "fft cols T");
+    launch_band_untranspose(T.Wt.p, n1, rlo, rhi, band2, bc, T.Tz.p, n2, st);
+    ckfft(cufftSetStream(fft_row, st), "cufftSetStream");
+    ckfft(cufftExecZ2Z(fft_row, reinterpret_cast<cufftDoubleComplex*>(T.Tz.p),
+                       reinterpret_cast<cufftDoubleComplex*>(T.G.p), CUFFT_INVERSE),
+          "fft rows T");
+    count_launch(2);
+    if (tm) tm->stop();
+    if (tm) tm->start("interp_T");
+    // gather at the point stencils (rows [rlo, rhi) of the transformed grid) x prephase
+    const double2* gbase = T.G.p - (ptrdiff_t)rlo * n2;
+    launch_interp(w, win, g, np, t.p, pre.p, mult, nullptr, nullptr, gbase, perm_t.n ? perm_t.p : nullptr, out, 0,
+                  conj_out, st, nullptr, false, nullptr, nullptr, opts.interp_kernel);
+    if (tm) tm->stop();
+}
+
 // nufft.cpp:295-367
 void Plan::apply_transpose(const double2* in, double2* out, FftWork& wk, cudaStream_t st,
                            StageTimer* tm, const double2* mult, int conj_in,
                            int conj_out) const {
+    if (fast && pruned) {
+        apply_transpose_pruned(in, out, st, tm, mult, conj_in, conj_out);
+        return;
+    }
     if (!fast) {
         if (tm) tm->start("ndft_T");
         const double2* src = in;

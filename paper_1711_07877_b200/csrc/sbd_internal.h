@@ -285,6 +285,20 @@ class Plan {
     void apply_transpose(const double2* in, double2* out, FftWork& wk, cudaStream_t st,
                          StageTimer* tm, const double2* mult = nullptr, int conj_in = 0,
                          int conj_out = 0) const;
+    // Pruned transposed path (nufft.cpp:295-367 restricted to what is nonzero
+    // and read), built on first use: tile-owned spread of the output side at
+    // its mode coordinates into a compact region, fold with the deconvolution
+    // into the transposed band, column transforms, untranspose into the
+    // populated rows, row transforms, gather at the point side.
+    struct TransposeWork {
+        bool ready = false;
+        TileGeom tg{};
+        DevBuf<uint32_t> rl_s, rl_e;
+        DevBuf<double2> b, Z, V, Wt, Tz, G;
+    };
+    mutable TransposeWork tpw;
+    void apply_transpose_pruned(const double2* in, double2* out, cudaStream_t st, StageTimer* tm,
+                                const double2* mult, int conj_in, int conj_out) const;
     void ensure_work(FftWork& wk, cudaStream_t st) const;
     // In-place unnormalised e^{+2 pi i} 2D transform of a full n1 x n2 grid
     // (FFTW_BACKWARD, nufft.cpp:207-213, 252).
@@ -380,6 +394,16 @@ void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int 
                            int n1, cudaStream_t st, int rin0 = 0, int conj_out = 0);
 void launch_mirror_points(const double2* t, uint64_t n, int n1, int n2, int w, double2* out,
                           cudaStream_t st);
+// b[k] = (conj_in ? conj : id)(in[perm ? perm[k] : k]) * phase[k]
+void launch_gather_conj_mul(const double2* in, const uint32_t* perm, const double2* phase, int conj_in,
+                            double2* b, uint64_t n, cudaStream_t st);
+// V[c n1 + (jx mod n1)] = Z[(jx - rlo) pz + (jy - clo)] dx[jx mod n1] dy[jy mod n2] for the band
+// modes |jx| <= b1, jy = c (c <= b2) or c - B (else), zero where Z has no cell
+void launch_band_fold(const double2* Z, int pz, int rlo, int rhi, int clo, int chi, int b1, int n1, int b2,
+                      int B, int n2, const double* dx, const double* dy, double2* V, cudaStream_t st);
+// Tz[(r - r0) n2 + m(c)] = Wt[c n1 + r] for r in [r0, r1), c < B (inverse of launch_band_transpose)
+void launch_band_untranspose(const double2* Wt, int n1, int r0, int r1, int b, int B, double2* Tz, int n2,
+                             cudaStream_t st);
 // out[idx[k]] = conj(in[k]) for k < n
 void launch_conj_scatter(const double2* in, uint64_t n, const uint32_t* idx, double2* out, cudaStream_t st);
 // *flag = 1 if some x[k] has a nonzero imaginary part, else 0
@@ -412,7 +436,7 @@ void launch_gather_mul(const double2* in, const uint32_t* perm, const double2* p
                        double2* raw, uint64_t n, cudaStream_t st, uint64_t lo = 0,
                        uint64_t hi = ~0ull, int* clear = nullptr);
 void launch_spmv_vec(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double2* vals,
-                     const double2* f, double2* qs, cudaStream_t st);
+                     const double2* f, double2* qs, cudaStream_t st, bool accumulate = false);
 void launch_spmv_vec_real(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double* vals,
                           const double2* f, double2* qs, cudaStream_t st);
 // D' times up to kSpmmMax right-hand sides in one pass over D': column j of
