@@ -700,13 +700,16 @@ struct sbd_op {
                               "fft_out", "interp_tgt", 0, ~0ull, lo, hi, shard_real ? &h : nullptr);
     }
 
-    // D^H as its own CSR (rows = sources, entries in target order, values
-    // conjugated), built on the first adjoint: the near-field part of the
-    // adjoint becomes the same gather SpMV as the forward one instead of a
-    // scatter with fp64 atomics (point_cloud.cpp:125-132)
+    // D^H as its own CSR (values conjugated), built on the first adjoint: the
+    // near-field part of the adjoint becomes a gather SpMV like the forward
+    // one instead of a scatter with fp64 atomics (point_cloud.cpp:125-132).
+    // On the fused path it is renumbered like D': rows = sources in fwd_in's
+    // sorted order, columns = targets in fwd_out's sorted order (entries
+    // sorted), so its u gathers are spatially local, and D^H u enters the
+    // source-side gather as its addend.
     DevBuf<uint64_t> roT;
     DevBuf<uint32_t> colsT;
-    DevBuf<double2> valsT;
+    DevBuf<double2> valsT, u_sorted, qsT;
     bool dT_ready = false;
     void build_adjoint_csr(cudaStream_t st) {
         const uint64_t ns = d.n_src(), nt = d.n_tgt(), nnz = d.nnz();
@@ -723,6 +726,35 @@ struct sbd_op {
                 v2[2 * o] = d.values[2 * i];
                 v2[2 * o + 1] = -d.values[2 * i + 1];
             }
+        if (fused) {
+            std::vector<uint32_t> ps(ns), pt(nt), inv_t(nt);
+            ck(cudaMemcpyAsync(ps.data(), fwd_in->perm_t.p, ns * 4, cudaMemcpyDeviceToHost, st), "perm");
+            ck(cudaMemcpyAsync(pt.data(), fwd_out->perm_s.p, nt * 4, cudaMemcpyDeviceToHost, st), "perm");
+            ck(cudaStreamSynchronize(st), "perm");
+            for (uint64_t j = 0; j < nt; ++j) inv_t[pt[j]] = (uint32_t)j;
+            std::vector<uint64_t> r2(ns + 1, 0);
+            for (uint64_t k = 0; k < ns; ++k) r2[k + 1] = r2[k] + (r[ps[k] + 1] - r[ps[k]]);
+            std::vector<uint32_t> c3(nnz);
+            std::vector<double> v3(2 * nnz);
+#pragma omp parallel for schedule(dynamic, 4096)
+            for (int64_t k = 0; k < (int64_t)ns; ++k) {
+                const uint64_t a = r[ps[k]], e = r[ps[k] + 1], o = r2[k];
+                std::vector<std::pair<uint32_t, uint64_t>> row;
+                row.reserve(e - a);
+                for (uint64_t i = a; i < e; ++i) row.emplace_back(inv_t[c2[i]], i);
+                std::sort(row.begin(), row.end());
+                for (uint64_t q = 0; q < row.size(); ++q) {
+                    c3[o + q] = row[q].first;
+                    v3[2 * (o + q)] = v2[2 * row[q].second];
+                    v3[2 * (o + q) + 1] = v2[2 * row[q].second + 1];
+                }
+            }
+            r.swap(r2);
+            c2.swap(c3);
+            v2.swap(v3);
+            u_sorted.alloc(std::max<uint64_t>(nt, 1));
+            qsT.alloc(std::max<uint64_t>(ns, 1));
+        }
         roT.upload(r.data(), ns + 1, st);
         colsT.upload(c2.data(), nnz, st);
         valsT.upload(reinterpret_cast<const double2*>(v2.data()), nnz, st);
@@ -733,6 +765,15 @@ struct sbd_op {
     // conv_operator.cpp:311-324: A^H u = conj(fwd_in^T (w . fwd_out^T conj(u))) + D^H u
     void apply_adjoint_one(const double2* u, double2* q, cudaStream_t st) {
         if (!dT_ready) build_adjoint_csr(st);
+        if (fused) {
+            if (tm.on) tm.start("spmv_adjoint");
+            launch_gather(u, fwd_out->perm_s.p, u_sorted.p, d.n_tgt(), st);
+            launch_spmv_vec(d.n_src(), roT.p, colsT.p, valsT.p, u_sorted.p, qsT.p, st);
+            if (tm.on) tm.stop();
+            fwd_out->apply_transpose(u, spec.p, work, st, &tm, w_sorted.p, /*conj_in=*/1, 0);
+            fwd_in->apply_transpose(spec.p, q, work, st, &tm, nullptr, 0, /*conj_out=*/1, qsT.p);
+            return;
+        }
         fwd_out->apply_transpose(u, spec.p, work, st, &tm, w_sorted.p, /*conj_in=*/1, 0);
         fwd_in->apply_transpose(spec.p, q, work, st, &tm, nullptr, 0, /*conj_out=*/1);
         if (tm.on) tm.start("spmv_adjoint");
@@ -746,7 +787,7 @@ struct sbd_op {
                qs.bytes() + work.bbuf.bytes() +
                cols.bytes() + vals.bytes() + work.grid.bytes() + work.T.bytes() + work.band.bytes() +
                spec.bytes() + hf.bytes() + hq.bytes() + kappa_h.bytes() + roT.bytes() + colsT.bytes() +
-               valsT.bytes();
+               valsT.bytes() + u_sorted.bytes() + qsT.bytes();
     }
 
     // conv_operator.cpp:338-353

@@ -442,7 +442,8 @@ void Plan::full_transform(double2* grid, cudaStream_t st) const {
 size_t Plan::device_bytes() const {
     return pts.bytes() + frq.bytes() + perm_t.bytes() + perm_s.bytes() + t.bytes() + pre.bytes() +
            s.bytes() + post.bytes() + dx.bytes() + dy.bytes() + tpw.b.bytes() + tpw.Z.bytes() + tpw.V.bytes() +
-           tpw.Wt.bytes() + tpw.Tz.bytes() + tpw.G.bytes() + tpw.rl_s.bytes() + tpw.rl_e.bytes();
+           tpw.Wt.bytes() + tpw.Tz.bytes() + tpw.G.bytes() + tpw.rl_s.bytes() + tpw.rl_e.bytes() +
+           tpw.m_tiles.bytes() + tpw.m_src.bytes() + tpw.m_dst.bytes() + tpw.m_t.bytes() + tpw.m_phase.bytes();
 }
 
 // nufft.cpp:218-290
@@ -683,7 +684,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
 // transposed spread only matters there; the DFT is symmetric; the gather at
 // the points reads only the populated rows/columns.
 void Plan::apply_transpose_pruned(const double2* in, double2* out, cudaStream_t st, StageTimer* tm,
-                                  const double2* mult, int conj_in, int conj_out) const {
+                                  const double2* mult, int conj_in, int conj_out, const double2* addend) const {
     TransposeWork& T = tpw;
     const int n1 = ax.n, n2 = ay.n;
     const int b1 = n1 / 4;
@@ -716,7 +717,27 @@ void Plan::apply_transpose_pruned(const double2* in, double2* out, cudaStream_t 
         T.Wt.alloc((size_t)bc * n1);
         T.Tz.alloc((size_t)(rhi - rlo) * n2);
         ck(cudaMemsetAsync(T.Tz.p, 0, T.Tz.bytes(), st), "Tz zero");  // columns outside the band stay zero
-        T.G.alloc((size_t)(rhi - rlo) * n2);
+        T.G.alloc((size_t)n1 * n2);
+        ck(cudaMemsetAsync(T.G.p, 0, T.G.bytes(), st), "G zero");
+        // a dense point side gets a Z order for the staged gather (32 x 32 blocks)
+        T.morton = (double)np >= 0.25 * ((double)n1 * (double)n2 / 4.0) && n1 < 32768 && n2 < 32768;
+        if (T.morton) {
+            DevBuf<uint32_t> keys(np);
+            T.m_shift = 0;
+            launch_morton_keys(t.p, np, g.half, T.m_shift, keys.p, st);
+            T.m_src.alloc(np);
+            launch_iota(T.m_src.p, np, st);
+            sort_by_key(keys.p, T.m_src.p, np, st);
+            build_tile_starts(keys.p, np, 10, T.m_tiles, T.m_ntiles, st);
+            T.m_t.alloc(np);
+            launch_gather(t.p, T.m_src.p, T.m_t.p, np, st);
+            T.m_dst.alloc(np);
+            if (perm_t.n)
+                launch_gather(perm_t.p, T.m_src.p, T.m_dst.p, np, st);
+            else
+                ck(cudaMemcpyAsync(T.m_dst.p, T.m_src.p, np * 4, cudaMemcpyDeviceToDevice, st), "m_dst");
+            T.m_phase.alloc(np);
+        }
         ck(cudaStreamSynchronize(st), "transpose setup");
         T.ready = true;
     }
@@ -747,26 +768,46 @@ void Plan::apply_transpose_pruned(const double2* in, double2* out, cudaStream_t 
     launch_band_untranspose(T.Wt.p, n1, rlo, rhi, band2, bc, T.Tz.p, n2, st);
     ckfft(cufftSetStream(fft_row, st), "cufftSetStream");
     ckfft(cufftExecZ2Z(fft_row, reinterpret_cast<cufftDoubleComplex*>(T.Tz.p),
-                       reinterpret_cast<cufftDoubleComplex*>(T.G.p), CUFFT_INVERSE),
+                       reinterpret_cast<cufftDoubleComplex*>(T.G.p + (size_t)rlo * n2), CUFFT_INVERSE),
           "fft rows T");
     count_launch(2);
     if (tm) tm->stop();
     if (tm) tm->start("interp_T");
-    // gather at the point stencils (rows [rlo, rhi) of the transformed grid) x prephase
-    const double2* gbase = T.G.p - (ptrdiff_t)rlo * n2;
-    launch_interp(w, win, g, np, t.p, pre.p, mult, nullptr, nullptr, gbase, perm_t.n ? perm_t.p : nullptr, out, 0,
-                  conj_out, st, nullptr, false, nullptr, nullptr, opts.interp_kernel);
+    // gather at the point stencils x prephase (x mult)
+    if (T.morton && !addend && !conj_out && opts.interp_kernel == 0) {
+        if (T.m_mult_of != mult || !mult) {
+            launch_gather(pre.p, T.m_src.p, T.m_phase.p, np, st);
+            if (mult) {
+                DevBuf<double2> mm(np);
+                launch_gather(mult, T.m_src.p, mm.p, np, st);
+                launch_mul(T.m_phase.p, mm.p, np, st);
+                ck(cudaStreamSynchronize(st), "m_phase");
+            }
+            T.m_mult_of = mult;
+        }
+        InterpTiles it;
+        it.start = T.m_tiles.p;
+        it.n = T.m_ntiles;
+        it.shift = T.m_shift;
+        it.out_lo = 0;
+        launch_interp(w, win, g, np, T.m_t.p, T.m_phase.p, nullptr, nullptr, nullptr, T.G.p, T.m_dst.p, out, 0, 0,
+                      st, nullptr, false, &it, nullptr, 1);
+    } else {
+        launch_interp(w, win, g, np, t.p, pre.p, mult, nullptr, nullptr, T.G.p, perm_t.n ? perm_t.p : nullptr, out,
+                      0, conj_out, st, addend, false, nullptr, nullptr, opts.interp_kernel);
+    }
     if (tm) tm->stop();
 }
 
 // nufft.cpp:295-367
 void Plan::apply_transpose(const double2* in, double2* out, FftWork& wk, cudaStream_t st,
                            StageTimer* tm, const double2* mult, int conj_in,
-                           int conj_out) const {
+                           int conj_out, const double2* addend) const {
     if (fast && pruned) {
-        apply_transpose_pruned(in, out, st, tm, mult, conj_in, conj_out);
+        apply_transpose_pruned(in, out, st, tm, mult, conj_in, conj_out, addend);
         return;
     }
+    if (addend) throw Error(3, "apply_transpose: addend needs the pruned path");
     if (!fast) {
         if (tm) tm->start("ndft_T");
         const double2* src = in;

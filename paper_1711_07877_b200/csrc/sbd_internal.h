@@ -282,9 +282,10 @@ class Plan {
                       const char* tag_interp, uint64_t in_lo = 0, uint64_t in_hi = ~0ull,
                       uint64_t out_lo = 0, uint64_t out_hi = ~0ull,
                       const HermArgs* herm = nullptr, cudaEvent_t before_interp = nullptr) const;
+    // addend (optional, pruned path): added per SORTED point after conj_out
     void apply_transpose(const double2* in, double2* out, FftWork& wk, cudaStream_t st,
                          StageTimer* tm, const double2* mult = nullptr, int conj_in = 0,
-                         int conj_out = 0) const;
+                         int conj_out = 0, const double2* addend = nullptr) const;
     // Pruned transposed path (nufft.cpp:295-367 restricted to what is nonzero
     // and read), built on first use: tile-owned spread of the output side at
     // its mode coordinates into a compact region, fold with the deconvolution
@@ -294,11 +295,19 @@ class Plan {
         bool ready = false;
         TileGeom tg{};
         DevBuf<uint32_t> rl_s, rl_e;
-        DevBuf<double2> b, Z, V, Wt, Tz, G;
+        DevBuf<double2> b, Z, V, Wt, Tz, G;  // G: full n1 x n2, zero outside the populated rows
+        // dense point side (>= 0.25 per band cell): the gather runs the staged
+        // tensor-core interpolation over a Z order of the points
+        bool morton = false;
+        uint32_t m_ntiles = 0;
+        int m_shift = 0;
+        DevBuf<uint32_t> m_tiles, m_src, m_dst;  // Z position -> sorted point / output index
+        DevBuf<double2> m_t, m_phase;            // positions, prephase x mult in Z order
+        const double2* m_mult_of = nullptr;      // the mult m_phase was formed with
     };
     mutable TransposeWork tpw;
     void apply_transpose_pruned(const double2* in, double2* out, cudaStream_t st, StageTimer* tm,
-                                const double2* mult, int conj_in, int conj_out) const;
+                                const double2* mult, int conj_in, int conj_out, const double2* addend) const;
     void ensure_work(FftWork& wk, cudaStream_t st) const;
     // In-place unnormalised e^{+2 pi i} 2D transform of a full n1 x n2 grid
     // (FFTW_BACKWARD, nufft.cpp:207-213, 252).
