@@ -340,13 +340,22 @@ def run_b200(args, w):
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
 
+    alt_step = None
     if world > 1:
-        # north_star partition: source shards -> all-reduce(xi spectrum) -> target shards
-        from paper_1711_07877_b200.parallel import DeviceBackend, ShardedApply
+        # slab decomposition (no replicated stage, two all-to-alls)
+        # and the north_star partition (source shards -> all-reduce of the xi
+        # spectrum -> target shards); --scheme picks the headline one, the
+        # other is timed beside it
+        from paper_1711_07877_b200.parallel import DeviceBackend, ShardedApply, SlabApply
         sharded = ShardedApply(DeviceBackend(op), rank, world)
+        slab = SlabApply(op, rank, world)
 
-        def step():
+        def step_shard():
             sharded.apply(f_dev, q_dev)
+
+        def step_slab():
+            slab.apply(f_dev, q_dev)
+        step, alt_step = (step_slab, step_shard) if args.scheme == "slab" else (step_shard, step_slab)
     else:
         def step():  # the caller knows its f is real (sbd_op_apply_device_ex)
             op.apply_device(f_dev.data_ptr(), q_dev.data_ptr(), R, sh, f_is_real=f_real)
@@ -385,6 +394,25 @@ def run_b200(args, w):
     # across RHS"): every rank applies the full operator to its own right-hand
     # side, no collective -- the batch-throughput mode, beside the sharded
     # (strong-scaling, north_star) apply timed above
+    alt = None
+    if alt_step is not None:
+        for _ in range(args.warmup):
+            alt_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.steps):
+            alt_step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_alt = float(t.item()) / args.steps
+        alt = {"scheme": "shard" if args.scheme == "slab" else "slab", "value": n / (ms_alt / 1e3),
+               "unit": "points/s", "ms_per_step": round(ms_alt, 3), "scaling": "strong"}
+
     rhs_par = None
     if world > 1:
         f_own = torch.from_numpy(rhs(w, n, np.random.default_rng(SEED + 100 + rank)).view(np.float64).copy()).cuda()
@@ -586,7 +614,9 @@ def run_b200(args, w):
                        "nufft_tol": info["nufft_tol"],
                        "l2": "inputs larger than L2 (grid + xi + D >> 126 MB)",
                        "parallelism": "single" if world == 1 else
-                       (f"sharded x{world}: sources/targets/D rows split, all-reduce of the xi spectrum" +
+                       ((f"slab x{world}: grids, xi nodes and targets split by position, two all-to-alls"
+                         if args.scheme == "slab" else
+                         f"sharded x{world}: sources/targets/D rows split, all-reduce of the xi spectrum") +
                         (f" (gloo; {world} ranks share {ndev} GPU(s): functional run, not a scaling number)"
                          if shared else " (NCCL)")),
                        "offline_s": round(t_offline, 2)},
@@ -600,6 +630,7 @@ def run_b200(args, w):
             "batched_rhs": batched,
             "adjoint": adjoint,
             "rhs_parallel": rhs_par,
+            "other_scheme": alt,
             "contract": contract,
             "parity": parity,
         }
@@ -622,6 +653,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nrhs", type=int, default=8, help="also time one batched apply of this many RHS (1: off)")
     ap.add_argument("--adjoint", type=int, default=1, help="1: also time apply_adjoint")
+    ap.add_argument("--scheme", default="slab", choices=["slab", "shard"],
+                    help="multi-GPU apply for N > 1: slab decomposition or the north_star source/target sharding")
     ap.add_argument("--ref-full", type=int, default=1,
                     help="1: one reference apply of the full config on one core after the timed region "
                          "(parity + same-config cpu_baseline; ~5 min at config 4); 0: the N=5e4 sample only")

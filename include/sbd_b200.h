@@ -177,6 +177,26 @@ int sbd_op_forward_spectrum(sbd_op* op, const double* d_f, uint64_t src_lo, uint
 int sbd_op_backward_targets(sbd_op* op, const double* d_spec, const double* d_f, uint64_t tgt_lo,
                             uint64_t tgt_hi, double* d_q, void* stream);
 
+/* ---- slab decomposition of one apply over `world` devices ----
+ * No stage is replicated: rank r spreads the sources into its row slab of the
+ * first grid, exchanges band columns (all-to-all 0), interpolates the xi
+ * nodes of its slab of the second grid and spreads them, exchanges band rows
+ * (all-to-all 1), and evaluates its targets. Per apply:
+ *   stage 0: d_f (all sources, caller order)    -> d_out = send buffer of exchange 0
+ *   (all-to-all 0: send counts/offsets from sbd_slab_counts(s, 0, ...))
+ *   stage 1: d_in = receive buffer of exchange 0 -> d_out = send buffer of exchange 1
+ *   (all-to-all 1)
+ *   stage 2: d_in = receive buffer of exchange 1, d_f -> d_out = q (caller order; only
+ *            this rank's targets are written)
+ * Counts are complex elements per peer (send[k]: to rank k; recv[k]: from rank k);
+ * buffers hold them back to back in rank order. Complex pipeline (every xi node).
+ * Requires both NUFFTs on the gridded path. */
+typedef struct sbd_slab sbd_slab;
+int sbd_slab_create(sbd_op* op, int rank, int world, sbd_slab** out);
+int sbd_slab_destroy(sbd_slab* s);
+int sbd_slab_counts(const sbd_slab* s, int exchange, uint64_t* send_counts, uint64_t* recv_counts);
+int sbd_slab_stage(sbd_slab* s, int stage, const double* d_in, const double* d_f, double* d_out, void* stream);
+
 /* Per-stage CUDA-event timing of every apply since profiling was enabled (or
  * since the last reset). names: "spread_src", "fft_in", "interp_xi",
  * "spread_xi", "fft_out", "interp_tgt", "spmv", ... ms[i] in milliseconds.

@@ -81,6 +81,10 @@ _sig("sbd_op_forward_spectrum", _int, _vp, _vp, _u64, _u64, _vp, _vp)
 _sig("sbd_op_backward_targets", _int, _vp, _vp, _vp, _u64, _u64, _vp, _vp)
 _sig("sbd_op_spectrum_length", _int, _vp, _vp, _vp, ctypes.POINTER(_u64))
 _sig("sbd_op_stage_times", _int, _vp, _dp, ctypes.POINTER(ctypes.c_char_p), _int)
+_sig("sbd_slab_create", _int, _vp, _int, _int, ctypes.POINTER(_vp))
+_sig("sbd_slab_destroy", _int, _vp)
+_sig("sbd_slab_counts", _int, _vp, _int, ctypes.POINTER(_u64), ctypes.POINTER(_u64))
+_sig("sbd_slab_stage", _int, _vp, _int, _vp, _vp, _vp, _vp)
 _sig("sbd_op_stage_times_reset", _int, _vp)
 _sig("sbd_cloud_diameter", ctypes.c_double, _dp, _u64)
 _sig("sbd_nufft_create", _int, _dp, _u64, _dp, _u64, _int, ctypes.c_double, _int, _u64, _u64,
@@ -108,6 +112,7 @@ EXPORTED = [
     "sbd_nufft_destroy", "sbd_ndft_direct", "sbd_choose_parameters", "sbd_kernel_launch_count",
     "sbd_window_fit_error", "sbd_bessel", "sbd_op_shard_bounds", "sbd_op_forward_spectrum",
     "sbd_op_backward_targets", "sbd_op_spectrum_length",
+    "sbd_slab_create", "sbd_slab_destroy", "sbd_slab_counts", "sbd_slab_stage",
 ]
 
 

@@ -22,7 +22,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["kernels.cu", "assemble_kernels.cu"]
-CPP_SOURCES = ["window.cpp", "plan.cpp", "op.cpp", "assemble.cpp", "bessel_host.cpp", "sbd_fit.cpp"]
+CPP_SOURCES = ["window.cpp", "plan.cpp", "op.cpp", "slab.cpp", "assemble.cpp", "bessel_host.cpp", "sbd_fit.cpp"]
 
 
 def _run(cmd, verbose):

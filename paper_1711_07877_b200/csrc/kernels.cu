@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
     const int gid = lane >> 2, kq = lane & 3;
     const int nrun = so.nby_run;
     const int ncy = (nrun + 1) >> 1;
-    const int cx = blockIdx.x / ncy, cy = blockIdx.x - (blockIdx.x / ncy) * ncy;
+    const int cx = blockIdx.x / ncy + so.cx0, cy = blockIdx.x - (blockIdx.x / ncy) * ncy;
     const int X0 = tg.rlo + cx * 32, Y0 = tg.clo + cy * kTileC * 2;
     // warp w owns the 8 x 8 sub-tiles (wr + 2p, wc + 2q), p, q in {0, 1}, of the
     // region's 4 x 4: every stencil (>= 2 sub-tiles wide) feeds all four warps,
@@ -2231,7 +2231,8 @@ struct SpreadTilesRun {
         if (out && !(use_mma && tg.tr == 16)) throw Error(3, "spread output modes need the DMMA spread");
         if (lists) so.lists = *lists;
         if (use_cta && tg.tr == 16) {
-            const int nblk = ((tg.nbx + 1) / 2) * ((so.nby_run + 1) / 2);
+            const int nblk = (so.ncx_run > 0 ? so.ncx_run : (tg.nbx + 1) / 2) * ((so.nby_run + 1) / 2);
+            if (nblk <= 0) return;
             const bool cplx = so.mode == 0 || so.mode == 2, list = so.lists.s1 && use_cta == 1;
 #define SBD_SPREAD_CTA(C, LI) \
     k_spread_cta<W, C, LI><<<nblk, 128, LI ? SCta<W>::smem_list : SCta<W>::smem, st>>>(P, g, tg, bs, b, pos, \
@@ -2710,6 +2711,38 @@ void launch_band_untranspose(const double2* Wt, int n1, int r0, int r1, int b, i
     k_band_untranspose<<<grid, 256, 0, st>>>(Wt, n1, r0, r1, b, B, Tz, n2);
     count_launch();
     ck(cudaGetLastError(), "k_band_untranspose");
+}
+
+__global__ void __launch_bounds__(256) k_wrap_transpose(const double2* __restrict__ in, size_t ipitch, int nin,
+                                                        int j0, int L, int Q, double2* __restrict__ out,
+                                                        size_t opitch) {
+    __shared__ double2 tile[32][33];
+    const int lb = blockIdx.x * 32, qb = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+        const int q = qb + ty + k, l = lb + tx;
+        if (q < Q && l < L) {
+            int c = (j0 + l) % nin;
+            if (c < 0) c += nin;
+            tile[ty + k][tx] = in[(size_t)q * ipitch + c];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 32; k += 8) {
+        const int l = lb + ty + k, q = qb + tx;
+        if (q < Q && l < L) out[(size_t)l * opitch + q] = tile[tx][ty + k];
+    }
+}
+
+void launch_wrap_transpose(const double2* in, size_t ipitch, int nin, int j0, int L, int Q, double2* out,
+                           size_t opitch, cudaStream_t st) {
+    if (L <= 0 || Q <= 0) return;
+    dim3 grid((unsigned)((L + 31) / 32), (unsigned)((Q + 31) / 32));
+    k_wrap_transpose<<<grid, 256, 0, st>>>(in, ipitch, nin, j0, L, Q, out, opitch);
+    count_launch();
+    ck(cudaGetLastError(), "k_wrap_transpose");
 }
 
 void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int B, double2* Tt,

@@ -354,6 +354,7 @@ struct SpreadOut {
     const double2* b2 = nullptr;
     const uint32_t* src2 = nullptr;  // mirror image -> tag-0 partner (b2 = conj(b[src2]))
     SpreadLists lists;
+    int cx0 = 0, ncx_run = 0;  // CTA spread: run region rows [cx0, cx0 + ncx_run) only (0: all)
 };
 
 // ---------------------------------------------------------------- kernels
@@ -413,6 +414,10 @@ void launch_band_fold(const double2* Z, int pz, int rlo, int rhi, int clo, int c
 // Tz[(r - r0) n2 + m(c)] = Wt[c n1 + r] for r in [r0, r1), c < B (inverse of launch_band_transpose)
 void launch_band_untranspose(const double2* Wt, int n1, int r0, int r1, int b, int B, double2* Tz, int n2,
                              cudaStream_t st);
+// out[l opitch + q] = in[q ipitch + ((j0 + l) mod nin)] for l < L, q < Q (a
+// transposing gather with a wrapped column window; the slab exchanges' packing)
+void launch_wrap_transpose(const double2* in, size_t ipitch, int nin, int j0, int L, int Q, double2* out,
+                           size_t opitch, cudaStream_t st);
 // out[idx[k]] = conj(in[k]) for k < n
 void launch_conj_scatter(const double2* in, uint64_t n, const uint32_t* idx, double2* out, cudaStream_t st);
 // *flag = 1 if some x[k] has a nonzero imaginary part, else 0

@@ -95,3 +95,65 @@ class ShardedApply:
         self.allreduce(self.spec[: 2 * n])
         self.b.backward_targets(self.spec, f, self.tgt[r], self.tgt[r + 1], q)
         return self.target_range()
+
+
+def dist_alltoall(recv, send, recv_splits, send_splits):
+    """The slab exchanges over torch.distributed: NCCL moves device buffers
+    directly; gloo (CPU tests, ranks sharing one GPU) goes through host copies."""
+    import torch.distributed as dist
+    n_r, n_s = sum(recv_splits), sum(send_splits)
+    if dist.get_backend() == "nccl" or not send.is_cuda:
+        dist.all_to_all_single(recv[:n_r], send[:n_s], recv_splits, send_splits)
+        return
+    r = recv[:n_r].cpu()
+    dist.all_to_all_single(r, send[:n_s].cpu(), recv_splits, send_splits)
+    recv[:n_r].copy_(r)
+
+
+class SlabApply:
+    """q = A f over `world` ranks with no replicated stage: the slab
+    decomposition of csrc/slab.cpp. Each rank holds the
+    operator; `alltoall(recv, send, recv_splits, send_splits)` moves the two
+    exchanges (torch.distributed.all_to_all_single over NCCL by default; the
+    single-GPU emulation in tests/ passes its own). `f` (2 n_src float64,
+    interleaved complex, device) is replicated; `q` receives this rank's
+    targets at their caller indices."""
+
+    def __init__(self, op, rank: int, world: int, alltoall=None):
+        import torch
+        self.torch = torch
+        self.op, self.rank, self.world = op, rank, world
+        h = ctypes.c_void_p()
+        check(lib.sbd_slab_create(op._h, rank, world, ctypes.byref(h)))
+        self._h = h
+        self.splits = []
+        for e in (0, 1):
+            snd = (ctypes.c_uint64 * world)()
+            rcv = (ctypes.c_uint64 * world)()
+            check(lib.sbd_slab_counts(h, e, snd, rcv))
+            self.splits.append(([2 * int(x) for x in snd], [2 * int(x) for x in rcv]))
+        self.bufs = [(torch.empty(max(sum(s), 2), dtype=torch.float64, device="cuda"),
+                      torch.empty(max(sum(r), 2), dtype=torch.float64, device="cuda")) for s, r in self.splits]
+        self.alltoall = alltoall or dist_alltoall
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.sbd_slab_destroy(self._h)
+            self._h = None
+
+    def stage(self, k, d_in, d_f, d_out):
+        s = self.torch.cuda.current_stream().cuda_stream
+        ptr = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        check(lib.sbd_slab_stage(self._h, k, ptr(d_in), ptr(d_f), ptr(d_out), ctypes.c_void_p(s)))
+
+    def exchange(self, e):
+        send, recv = self.bufs[e]
+        ssp, rsp = self.splits[e]
+        self.alltoall(recv, send, rsp, ssp)
+
+    def apply(self, f, q):
+        self.stage(0, None, f, self.bufs[0][0])
+        self.exchange(0)
+        self.stage(1, self.bufs[0][1], None, self.bufs[1][0])
+        self.exchange(1)
+        self.stage(2, self.bufs[1][1], f, q)

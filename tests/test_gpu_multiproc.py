@@ -70,4 +70,5 @@ def test_bench_gpus_2_runs_two_ranks():
     line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 2
     assert line["contract"]["ok"]
-    assert "sharded x2" in line["config"]["parallelism"]
+    assert "slab x2" in line["config"]["parallelism"]
+    assert line["other_scheme"]["scheme"] == "shard" and line["rhs_parallel"]["scaling"] == "weak"

@@ -87,3 +87,29 @@ def test_shard_bounds_partition():
         sa = ShardedApply(Dummy(), 0, world, allreduce=lambda t: None)
         assert sa.src[0] == 0 and sa.src[-1] == 10 and sa.tgt[-1] == 7
         assert all(a <= b for a, b in zip(sa.src, sa.src[1:]))
+
+
+def _a2a_worker(rank, world, port, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1711_07877_b200.parallel import dist_alltoall
+    # rank r sends (r + 1) * (k + 1) values "r.k" to rank k, back to back
+    ssp = [(rank + 1) * (k + 1) for k in range(world)]
+    send = torch.cat([torch.full((n,), 10.0 * rank + k, dtype=torch.float64) for k, n in enumerate(ssp)])
+    rsp = [(k + 1) * (rank + 1) for k in range(world)]
+    recv = torch.zeros(sum(rsp) + 3, dtype=torch.float64)  # (oversized, as SlabApply allocates)
+    dist_alltoall(recv, send, rsp, ssp)
+    np.save(os.path.join(outdir, f"a2a_{rank}.npy"), recv.numpy())
+    dist.destroy_process_group()
+
+
+def test_slab_exchange_over_gloo(tmp_path):
+    # the slab decomposition's two all-to-alls (parallel.dist_alltoall) route
+    # each rank's block for rank k to rank k, in rank order
+    world = 2
+    mp.spawn(_a2a_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        got = np.load(tmp_path / f"a2a_{r}.npy")
+        want = np.concatenate([np.full((k + 1) * (r + 1), 10.0 * k + r) for k in range(world)])
+        assert np.array_equal(got[:len(want)], want)
