@@ -603,10 +603,11 @@ constexpr int kSCS = 18;   // scan segments: 2 point sets x 3 x 3 bins
 
 template <int W>
 struct SCta {
-    static constexpr int L = W + 14;     // padded tap row
+    static constexpr int L = W + 14;     // padded tap row (y taps)
+    static constexpr int LA = W + 15;    // x-tap row: one more cell for the even-start shift
     static constexpr int NP = kSCB + 1;  // staged points + the zero point
     static constexpr int LS = kSCB + 4;  // list stride (room for the padding)
-    static constexpr size_t smem = (size_t)NP * L * (sizeof(double2) + sizeof(double)) +
+    static constexpr size_t smem = (size_t)NP * (LA * sizeof(double2) + L * sizeof(double)) +
                                    (size_t)kSCQ * 2 * sizeof(double2) + (size_t)16 * LS * 4 +
                                    (size_t)2 * kSCB * 4;
     static constexpr size_t smem_list = smem - (size_t)kSCQ * 2 * sizeof(double2);  // LIST: no ring
@@ -624,7 +625,7 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
     constexpr int L = S::L;
     extern __shared__ __align__(16) double smem_sc[];
     double2* sA = reinterpret_cast<double2*>(smem_sc);  // [NP][L]: b * x taps
-    double2* sQt = sA + S::NP * L;                       // queued positions (16-byte aligned)
+    double2* sQt = sA + S::NP * S::LA;                   // queued positions (16-byte aligned)
     double2* sQb = sQt + (LIST ? 0 : kSCQ);              // queued coefficients (scan mode only)
     double* sB = reinterpret_cast<double*>(sQb + (LIST ? 0 : kSCQ));  // [NP][L]: y taps
     uint32_t* sL = reinterpret_cast<uint32_t*>(sB + S::NP * L);  // [4 warps][4 sub-tiles][LS]
@@ -646,9 +647,9 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
     const int wr = warp >> 1, wc = warp & 1;
     const unsigned lt = (1u << lane) - 1u;
 
-    for (int i = tid; i < S::NP * L; i += 128) {
+    for (int i = tid; i < S::NP * S::LA; i += 128) {
         sA[i] = make_double2(0.0, 0.0);
-        sB[i] = 0.0;
+        if (i < S::NP * L) sB[i] = 0.0;
     }
     // scan segments: (set, bin) -> [first sorted position, size), prefix sums
     if (!LIST && warp == 0) {
@@ -693,14 +694,21 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
                 if (warp < 2) {
                     const int ix0 = (int)ceil(t.x - g.half);
                     const double u = (ix0 - t.x) + g.half;
-                    double2* a = sA + p * L + 7;
+                    // every A-fragment read of this point starts on an even
+                    // 16-byte bank group (the row shifted by one cell when
+                    // needed): a quarter-warp's 4 points x 2 rows then fall in
+                    // aligned bank-group pairs (fewer conflicts)
+                    const int dx = ix0 - X0;  // in [1 - W, 32)
+                    const int sh = (p * S::LA - dx + 7) & 1;
+                    double2* a = sA + p * S::LA + sh + 7;
                     auto put = [&](int i, double v) { a[i] = make_double2(b2.x * v, b2.y * v); };
                     if (warp == 0) {
-                        const int dx = ix0 - X0;  // in [1 - W, 32)
                         const int r0 = max(0, ((dx + 64) >> 3) - 8), r1 = min(3, ((dx + W - 1 + 64) >> 3) - 8);
-                        sDX[p] = ((p * L - dx + 7) << 4) | (((2 << r1) - 1) & ~((1 << r0) - 1));
+                        sDX[p] = ((p * S::LA + sh - dx + 7) << 4) | (((2 << r1) - 1) & ~((1 << r0) - 1));
+                        a[-1] = make_double2(0.0, 0.0);  // a previous batch's tap one cell before ...
                         kb_taps_slice<W, 0, H, false>(u, P, put);
                     } else {
+                        a[W] = make_double2(0.0, 0.0);   // ... or one cell after
                         kb_taps_slice<W, H, W / 2, true>(u, P, put);
                     }
                 } else {
@@ -744,7 +752,7 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
                 cnt[t] += __popc(m);
             }
         }
-        constexpr uint32_t zero = (uint32_t)(kSCB * L) | ((uint32_t)(kSCB * L) << 16);
+        constexpr uint32_t zero = (uint32_t)(kSCB * S::LA) | ((uint32_t)(kSCB * L) << 16);
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
             if (lane < ((-cnt[t]) & 3)) lst[t * S::LS + cnt[t] + lane] = zero;

@@ -137,8 +137,11 @@ class SlabApply:
         self.alltoall = alltoall or dist_alltoall
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            lib.sbd_slab_destroy(self._h)
+        if getattr(self, "_h", None) and lib is not None:
+            try:
+                lib.sbd_slab_destroy(self._h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
     def stage(self, k, d_in, d_f, d_out):
