@@ -158,6 +158,18 @@ def stage_bytes(info, name):
     }.get(name)
 
 
+def ncu_pipes(stage):
+    """fp64 / DMMA pipe, issue and L1 utilisation of the stage's kernel from the
+    committed ncu --set full capture (profiles/ncu_pipes.json)."""
+    p = os.path.join(ROOT, "profiles", "ncu_pipes.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as fh:
+        d = json.load(fh)
+    v = d.get("pipes", {}).get(stage)
+    return dict(v, source=d.get("source")) if v else None
+
+
 def ncu_traffic(stage):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
@@ -466,6 +478,8 @@ def run_b200(args, w):
                 "stages_ms": {k: round(v, 4) for k, v in avg.items()},
                 "stages_frac": {k: round(stage_bytes(info, k) / (avg[k] / 1e3) / 1e9 / peak, 4)
                                 for k in cand}}
+    roofline["pipes"] = ncu_pipes(dom)  # what actually binds it (fp64 pipes beside HBM)
+    roofline["traffic_source"] = "profiles/ncu_traffic.json (ncu --set full capture of this kernel, per launch)"
     if roof_note:
         roofline["note"] = roof_note
 

@@ -12,6 +12,7 @@
 #include <cub/cub.cuh>
 
 #include <climits>
+#include <type_traits>
 #include <cstdlib>
 
 #include "device_common.cuh"
@@ -623,9 +624,13 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
                                                      const int* __restrict__ herm, SpreadOut so) {
     using S = SCta<W>;
     constexpr int L = S::L;
+    // b * x taps: complex for a complex grid, one double for a real one (half
+    // the A-fragment shared-memory traffic of the real spread)
+    using AT = typename std::conditional<CPLX, double2, double>::type;
     extern __shared__ __align__(16) double smem_sc[];
-    double2* sA = reinterpret_cast<double2*>(smem_sc);  // [NP][L]: b * x taps
-    double2* sQt = sA + S::NP * S::LA;                   // queued positions (16-byte aligned)
+    AT* sA = reinterpret_cast<AT*>(smem_sc);            // [NP][LA]: b * x taps
+    constexpr size_t kABytes = ((size_t)S::NP * S::LA * sizeof(AT) + 15) & ~(size_t)15;
+    double2* sQt = reinterpret_cast<double2*>(reinterpret_cast<char*>(smem_sc) + kABytes);  // queued positions
     double2* sQb = sQt + (LIST ? 0 : kSCQ);              // queued coefficients (scan mode only)
     double* sB = reinterpret_cast<double*>(sQb + (LIST ? 0 : kSCQ));  // [NP][L]: y taps
     uint32_t* sL = reinterpret_cast<uint32_t*>(sB + S::NP * L);  // [4 warps][4 sub-tiles][LS]
@@ -648,7 +653,7 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
     const unsigned lt = (1u << lane) - 1u;
 
     for (int i = tid; i < S::NP * S::LA; i += 128) {
-        sA[i] = make_double2(0.0, 0.0);
+        sA[i] = AT{};
         if (i < S::NP * L) sB[i] = 0.0;
     }
     // scan segments: (set, bin) -> [first sorted position, size), prefix sums
@@ -700,15 +705,20 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
                     // aligned bank-group pairs (fewer conflicts)
                     const int dx = ix0 - X0;  // in [1 - W, 32)
                     const int sh = (p * S::LA - dx + 7) & 1;
-                    double2* a = sA + p * S::LA + sh + 7;
-                    auto put = [&](int i, double v) { a[i] = make_double2(b2.x * v, b2.y * v); };
+                    AT* a = sA + p * S::LA + sh + 7;
+                    auto put = [&](int i, double v) {
+                        if constexpr (CPLX)
+                            a[i] = make_double2(b2.x * v, b2.y * v);
+                        else
+                            a[i] = b2.x * v;
+                    };
                     if (warp == 0) {
                         const int r0 = max(0, ((dx + 64) >> 3) - 8), r1 = min(3, ((dx + W - 1 + 64) >> 3) - 8);
                         sDX[p] = ((p * S::LA + sh - dx + 7) << 4) | (((2 << r1) - 1) & ~((1 << r0) - 1));
-                        a[-1] = make_double2(0.0, 0.0);  // a previous batch's tap one cell before ...
+                        a[-1] = AT{};  // a previous batch's tap one cell before ...
                         kb_taps_slice<W, 0, H, false>(u, P, put);
                     } else {
-                        a[W] = make_double2(0.0, 0.0);   // ... or one cell after
+                        a[W] = AT{};   // ... or one cell after
                         kb_taps_slice<W, H, W / 2, true>(u, P, put);
                     }
                 } else {
@@ -766,10 +776,14 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
             const uint32_t* lt4 = lst + t * S::LS + kq;
             for (int grp = 0; grp < cnt[t]; grp += 4) {
                 const uint32_t e = lt4[grp];
-                const double2 a = sA[(e & 0xffffu) + gid];
+                const AT a = sA[(e & 0xffffu) + gid];
                 const double bv = sB[(e >> 16) + gid];
-                dmma(cr[i][j][0], cr[i][j][1], a.x, bv);
-                if (CPLX) dmma(ci[i][j][0], ci[i][j][1], a.y, bv);
+                if constexpr (CPLX) {
+                    dmma(cr[i][j][0], cr[i][j][1], a.x, bv);
+                    dmma(ci[i][j][0], ci[i][j][1], a.y, bv);
+                } else {
+                    dmma(cr[i][j][0], cr[i][j][1], a, bv);
+                }
             }
         }
         __syncthreads();  // staged rows, starts and lists are rewritten next batch

@@ -91,5 +91,24 @@ for row in r[2:]:
             vals.append(v)
     out.append(f"| `{d.get('Kernel Name', '')[:48]}` | " + " | ".join(vals) + " |")
 open(os.path.join(ROOT, "profiles", f"{tag}_kernels.md"), "w").write("\n".join(out) + "\n")
+# per-stage pipe utilisation of the --set full capture (in apply order: the
+# capture's launches are spread_src, interp_xi, spmv, spread_xi, interp_tgt),
+# read by bench.py beside the HBM fraction
+pipes = {}
+for st_name, row in zip(stage_names, r[2:]):
+    d = dict(zip(h, row))
+
+    def num(k):
+        try:
+            return round(float(d.get(k, "").replace(",", "")), 1)
+        except ValueError:
+            return None
+    pipes[st_name] = {"dmma_pct": num("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active"),
+                      "fp64_pct": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                      "issue_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                      "l1_pct": num("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                      "dram_pct": num("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")}
+json.dump({"source": f"profiles/{tag}_kernels.md (ncu --set full, config 4)", "pipes": pipes},
+          open(os.path.join(ROOT, "profiles", "ncu_pipes.json"), "w"), indent=1)
 print("\n".join(lines[-12:]))
 print("\n".join(out))
