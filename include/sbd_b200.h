@@ -66,6 +66,14 @@ typedef struct sbd_op_options {
     int fused;             /* 1: fused forward path (renumbered D, omega-hat folded into the
                               xi interpolation). Default 1 */
     int verbose;           /* 1: setup diagnostics on stderr. Default 0 */
+    int procedural_rings;  /* 1: the xi nodes are regenerated inside the xi-side kernels from
+                              (rho_p, M_p, weight_p, j) (ring_quadrature.cpp:24-69) and their
+                              per-node arrays (coordinates, phases, omega-hat: ~170 B per node)
+                              are not kept in HBM; needs ring-generated nodes (else stays off,
+                              see sbd_op_info_t.procedural_rings) and the fused path. The other
+                              paths (adjoint, sharded, slab) rebuild the arrays on first use.
+                              Default 0: the kernels are issue-bound, not HBM-bound, so the
+                              regeneration costs time; the mode trades it for capacity */
 } sbd_op_options;
 
 void sbd_op_options_default(sbd_op_options* o);
@@ -94,6 +102,7 @@ typedef struct sbd_op_info_t {
     int fast_in, fast_out;           /* fast (gridded) vs direct path per plan */
     uint64_t bytes;                  /* CompressedOperator::bytes() (conv_operator.cpp:338-353) */
     uint64_t device_bytes;           /* HBM actually held by this operator */
+    int procedural_rings;            /* 1: the xi-side kernels regenerate the ring nodes */
 } sbd_op_info_t;
 
 const char* sbd_last_error(void);

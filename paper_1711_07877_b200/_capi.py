@@ -26,7 +26,8 @@ _int = ctypes.c_int
 
 class OpOptionsC(ctypes.Structure):
     _fields_ = [("real_input_split", _int), ("hermitian_fft", _int), ("radix_first_pass", _int),
-                ("spread_kernel", _int), ("interp_kernel", _int), ("fused", _int), ("verbose", _int)]
+                ("spread_kernel", _int), ("interp_kernel", _int), ("fused", _int), ("verbose", _int),
+                ("procedural_rings", _int)]
 
 
 class AssembleOptionsC(ctypes.Structure):
@@ -45,7 +46,7 @@ class OpInfoC(ctypes.Structure):
                 ("P", _int), ("w", _int), ("beta", ctypes.c_double),
                 ("n1_in", _int), ("n2_in", _int), ("n1_out", _int), ("n2_out", _int),
                 ("fast_in", _int), ("fast_out", _int),
-                ("bytes", _u64), ("device_bytes", _u64)]
+                ("bytes", _u64), ("device_bytes", _u64), ("procedural_rings", _int)]
 
 
 def _sig(name, res, *args):

@@ -12,6 +12,7 @@
 #include <cub/cub.cuh>
 
 #include <climits>
+#include <cstring>
 #include <type_traits>
 #include <cstdlib>
 
@@ -25,41 +26,130 @@ namespace {
 using namespace dev;
 constexpr double kPi = 3.14159265358979323846;
 
-// Per-point plan arrays (nufft.cpp:163-177).
-__global__ void k_plan_points(const double2* __restrict__ pts, uint64_t n, Axis ax, Axis ay,
-                              double beta, double2* __restrict__ t, double2* __restrict__ pre) {
-    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    const double2 p = pts[k];
+// Per-point plan arrays (nufft.cpp:163-177), as device functions so the
+// procedural xi-side kernels regenerate bitwise the values the plan was built
+// from (explicitly rounded operations: no FMA contraction in either place).
+__device__ __forceinline__ double2 plan_point_pos(double2 p, const Axis& ax, const Axis& ay) {
     const double px = __dsub_rn(p.x, ax.center);
     const double py = __dsub_rn(p.y, ay.center);
     const double ux = __ddiv_rn(px, ax.gamma);
     const double uy = __ddiv_rn(py, ay.gamma);
     const double two_pi = 2.0 * kPi;
-    t[k] = make_double2(__ddiv_rn(__dmul_rn(__dadd_rn(ux, kPi), (double)ax.n), two_pi),
+    return make_double2(__ddiv_rn(__dmul_rn(__dadd_rn(ux, kPi), (double)ax.n), two_pi),
                         __ddiv_rn(__dmul_rn(__dadd_rn(uy, kPi), (double)ay.n), two_pi));
+}
+
+__device__ __forceinline__ double2 plan_point_pre(double2 p, const Axis& ax, const Axis& ay, double beta) {
+    const double px = __dsub_rn(p.x, ax.center);
+    const double py = __dsub_rn(p.y, ay.center);
     const double phase = __dadd_rn(__dmul_rn(px, ax.fcenter), __dmul_rn(py, ay.fcenter));
     const double dec = __dmul_rn(__dmul_rn(ax.alpha2, kb_hat(beta, __dmul_rn(ax.alpha2, px))),
                                  __dmul_rn(ay.alpha2, kb_hat(beta, __dmul_rn(ay.alpha2, py))));
     double sn, cs;
     sincos(phase, &sn, &cs);
-    pre[k] = make_double2(__ddiv_rn(cs, dec), __ddiv_rn(sn, dec));
+    return make_double2(__ddiv_rn(cs, dec), __ddiv_rn(sn, dec));
+}
+
+__global__ void k_plan_points(const double2* __restrict__ pts, uint64_t n, Axis ax, Axis ay,
+                              double beta, double2* __restrict__ t, double2* __restrict__ pre) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double2 p = pts[k];
+    t[k] = plan_point_pos(p, ax, ay);
+    pre[k] = plan_point_pre(p, ax, ay, beta);
 }
 
 // Per-output plan arrays (nufft.cpp:179-192). sgn = sign of the plan.
+__device__ __forceinline__ double2 plan_output_pos(double2 f, const Axis& ax, const Axis& ay, double sgn) {
+    const double fx = __dmul_rn(sgn, f.x), fy = __dmul_rn(sgn, f.y);
+    return make_double2(__dmul_rn(ax.gamma, __dsub_rn(fx, ax.fcenter)),
+                        __dmul_rn(ay.gamma, __dsub_rn(fy, ay.fcenter)));
+}
+
+__device__ __forceinline__ double2 plan_output_post(double2 f, const Axis& ax, const Axis& ay, double sgn,
+                                                    double cxy) {
+    const double fx = __dmul_rn(sgn, f.x), fy = __dmul_rn(sgn, f.y);
+    const double phase = __dadd_rn(__dmul_rn(ax.center, fx), __dmul_rn(ay.center, fy));
+    double sn, cs;
+    sincos(phase, &sn, &cs);
+    return make_double2(__dmul_rn(cs, cxy), __dmul_rn(sn, cxy));
+}
+
 __global__ void k_plan_outputs(const double2* __restrict__ frq, uint64_t n, Axis ax, Axis ay,
                                double sgn, double cxy, double2* __restrict__ s,
                                double2* __restrict__ post) {
     const uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (v >= n) return;
     const double2 f = frq[v];
-    const double fx = __dmul_rn(sgn, f.x), fy = __dmul_rn(sgn, f.y);
-    s[v] = make_double2(__dmul_rn(ax.gamma, __dsub_rn(fx, ax.fcenter)),
-                        __dmul_rn(ay.gamma, __dsub_rn(fy, ay.fcenter)));
-    const double phase = __dadd_rn(__dmul_rn(ax.center, fx), __dmul_rn(ay.center, fy));
+    s[v] = plan_output_pos(f, ax, ay, sgn);
+    post[v] = plan_output_post(f, ax, ay, sgn, cxy);
+}
+
+// Ring node `id` (ring_quadrature.cpp:58-63: rho (cos, sin)(2 pi j / m)); the
+// angle is formed as pi * (j * (2 / m)) for sincospi, within 2 ulp of the
+// reference's 2 pi j / m.
+__device__ __forceinline__ double2 ring_node(uint32_t id, const RingRow* __restrict__ rings, double2* w = nullptr) {
+    const RingRow r = rings[(id & ~kRingHalve) >> kRingJBits];
+    const uint32_t j = id & ((1u << kRingJBits) - 1u);
     double sn, cs;
-    sincos(phase, &sn, &cs);
-    post[v] = make_double2(__dmul_rn(cs, cxy), __dmul_rn(sn, cxy));
+    sincospi(__dmul_rn((double)j, r.two_over_m), &sn, &cs);
+    if (w) *w = make_double2(r.wre, r.wim);
+    return make_double2(__dmul_rn(r.rho, cs), __dmul_rn(r.rho, sn));
+}
+
+__global__ void k_ring_nodes(const uint32_t* __restrict__ id, uint64_t n, const RingRow* __restrict__ rings,
+                             double2* __restrict__ xi, double2* __restrict__ w) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    double2 wt;
+    const double2 p = ring_node(id[k], rings, &wt);
+    if (xi) xi[k] = p;
+    if (w) w[k] = wt;
+}
+
+// max over nodes of |a - b| / max(|a|, tiny) as ordered uint64 bits
+__global__ void k_node_deviation(const double2* __restrict__ a, const double2* __restrict__ b, uint64_t n,
+                                 unsigned long long* __restrict__ worst) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    double d = 0.0;
+    if (k < n) {
+        const double2 p = a[k], q = b[k];
+        const double mag = fmax(sqrt(p.x * p.x + p.y * p.y), 1e-300);
+        d = sqrt((p.x - q.x) * (p.x - q.x) + (p.y - q.y) * (p.y - q.y)) / mag;
+        if (!(d == d)) d = 1e300;
+    }
+    for (int o = 16; o; o >>= 1) d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+    if ((threadIdx.x & 31) == 0 && d > 0.0) atomicMax(worst, (unsigned long long)__double_as_longlong(d));
+}
+
+// The materialised plan arrays of procedural nodes in one kernel order:
+// grid coordinates + prephase (point side) or mode coordinates + postphase
+// (output side), and kappa = omega-hat * prephase (halved nodes at 1/2 in kh).
+__global__ void k_ring_point_arrays(NodeGen gen, uint64_t n, double2* __restrict__ t, double2* __restrict__ pre) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const double2 p = ring_node(gen.id[k], gen.rings);
+    if (t) t[k] = plan_point_pos(p, gen.px, gen.py);
+    if (pre) pre[k] = plan_point_pre(p, gen.px, gen.py, gen.pbeta);
+}
+
+__global__ void k_ring_output_arrays(NodeGen gen, uint64_t n, double2* __restrict__ s, double2* __restrict__ post,
+                                     double2* __restrict__ kappa, double2* __restrict__ kappa_h) {
+    const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint32_t id = gen.id[k];
+    double2 w;
+    const double2 p = ring_node(id, gen.rings, &w);
+    if (s) s[k] = plan_output_pos(p, gen.ox, gen.oy, gen.osgn);
+    if (post) post[k] = plan_output_post(p, gen.ox, gen.oy, gen.osgn, gen.ocxy);
+    if (kappa || kappa_h) {
+        const double2 kp = cmul(w, plan_point_pre(p, gen.px, gen.py, gen.pbeta));
+        if (kappa) kappa[k] = kp;
+        if (kappa_h) {
+            const double h = (id & kRingHalve) ? 0.5 : 1.0;
+            kappa_h[k] = make_double2(h * kp.x, h * kp.y);
+        }
+    }
 }
 
 __global__ void k_bin_keys(const double2* __restrict__ pos, uint64_t n, GridGeom g, int tile,
@@ -370,6 +460,19 @@ __global__ void __launch_bounds__(128, TR == 16 ? 4 : 5) k_spread_tiles(WindowPo
     }
 }
 
+// reflection m -> -m (mod n). The image's stencil must be exactly the mirror
+// of the point's (start n - s - w + 1 for start s = ceil(t - w/2)); when
+// rounding puts ceil(t' - w/2) one cell off (t - w/2 within an ulp of an
+// integer), t' is nudged by ulps, which moves the taps by rounding only.
+__device__ __forceinline__ double mirror_coord(double t, int n, int w) {
+    const double h = 0.5 * w;
+    const int want = n - (int)ceil(t - h) - w + 1;
+    double m = (double)n - t;
+    for (int it = 0; it < 8 && (int)ceil(m - h) > want; ++it) m = nextafter(m, -1e300);
+    for (int it = 0; it < 8 && (int)ceil(m - h) < want; ++it) m = nextafter(m, 1e300);
+    return m;
+}
+
 // coefficient of mirror image k (second point set): conj of its tag-0
 // partner's coefficient when the partner map is given, else stored
 __device__ __forceinline__ double2 mirror_coef(const SpreadOut& so, const double2* __restrict__ b,
@@ -614,7 +717,10 @@ struct SCta {
     static constexpr size_t smem_list = smem - (size_t)kSCQ * 2 * sizeof(double2);  // LIST: no ring
 };
 
-template <int W, bool CPLX, bool LIST>
+// PROC (LIST only): the points are procedural ring nodes -- their grid
+// coordinates are regenerated from so.gen.id (a mirror image's from its tag-0
+// partner) instead of read from pos / so.pos2.
+template <int W, bool CPLX, bool LIST, bool PROC = false>
 __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(WindowPoly P, GridGeom g, TileGeom tg,
                                                      const uint32_t* __restrict__ bin_start,
                                                      const double2* __restrict__ bsorted,
@@ -811,7 +917,13 @@ __global__ void __launch_bounds__(128, LIST ? (CPLX ? 8 : 9) : 7) k_spread_cta(W
         auto fetch = [&](uint32_t e, double2& t, double2& b2) {
             if (e != 0xffffffffu) {
                 const uint32_t k = e & 0x7fffffffu;
-                t = (e >> 31) ? so.pos2[k] : pos[k];
+                if constexpr (PROC) {
+                    const uint32_t kp = (e >> 31) ? so.src2[k] : k;
+                    t = plan_point_pos(ring_node(so.gen.id[kp], so.gen.rings), so.gen.px, so.gen.py);
+                    if (e >> 31) t = make_double2(mirror_coord(t.x, g.n1, W), mirror_coord(t.y, g.n2, W));
+                } else {
+                    t = (e >> 31) ? so.pos2[k] : pos[k];
+                }
                 if (warp < 2) b2 = (e >> 31) ? mirror_coef(so, bsorted, k) : bsorted[k];
             }
         };
@@ -1492,13 +1604,16 @@ __device__ __forceinline__ void mma_group_t(const double2* __restrict__ S, int r
     }
 }
 
-template <int W, bool TRANS>
+// PROC: the outputs are procedural ring nodes -- positions, postphase and
+// kappa (omega-hat times the next plan's prephase, `mult` of the fused path)
+// are regenerated from gen.id instead of read from pos / phase / mult.
+template <int W, bool TRANS, bool PROC = false>
 __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
     WindowPoly P, GridGeom g, const uint32_t* __restrict__ tstart, uint32_t ntiles, int shift,
     uint64_t out_lo, uint64_t n, const double2* __restrict__ pos, const double2* __restrict__ phase,
     const double2* __restrict__ mult, const double* __restrict__ dxt, const double* __restrict__ dyt,
     const double2* __restrict__ grid, const uint32_t* __restrict__ perm,
-    const double2* __restrict__ addend, double2* __restrict__ out, HermArgs hh) {
+    const double2* __restrict__ addend, double2* __restrict__ out, HermArgs hh, NodeGen gen) {
     using TT = ITile<W, TRANS>;
     const bool hon = hh.flag && *hh.flag;
     if (hon) {
@@ -1520,7 +1635,8 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
         const uint64_t t0 = tstart[tile], t1 = tstart[tile + 1];
         const uint64_t a0 = t0 > out_lo ? t0 : out_lo, a1 = t1 < out_lo + n ? t1 : out_lo + n;
         if (a0 >= a1) continue;
-        const double2 s0 = pos[a0 - out_lo];
+        const double2 s0 = PROC ? plan_output_pos(ring_node(gen.id[a0 - out_lo], gen.rings), gen.ox, gen.oy, gen.osgn)
+                                : pos[a0 - out_lo];
         const int X0 = (((int)ceil(s0.x - g.half) + shift) & ~(kIT - 1)) - shift;
         const int Y0 = (((int)ceil(s0.y - g.half) + shift) & ~(kIT - 1)) - shift;
         __syncthreads();  // previous tile's readers are done
@@ -1564,10 +1680,18 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
             const uint64_t vr = mine ? vmy - out_lo : 0;
             double2 sv = make_double2(0.0, 0.0), ph = sv, mu = make_double2(1.0, 0.0), ad = sv;
             uint32_t dst = 0;
+            uint32_t nid = 0;
+            double2 xi = sv;
             if (mine) {
-                sv = pos[vr];
-                ph = phase[vr];
-                if (mult) mu = mult[vr];
+                if constexpr (PROC) {
+                    nid = gen.id[vr];
+                    xi = ring_node(nid, gen.rings, &mu);
+                    sv = plan_output_pos(xi, gen.ox, gen.oy, gen.osgn);
+                } else {
+                    sv = pos[vr];
+                    ph = phase[vr];
+                    if (mult) mu = mult[vr];
+                }
                 if (addend) ad = addend[vr];
                 dst = perm ? perm[vr] : (uint32_t)vr;
             }
@@ -1667,8 +1791,14 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
                 }
             }
             if (mine) {
+                if constexpr (PROC) {
+                    // after the group loop: the phases' registers are not live across it
+                    ph = plan_output_post(xi, gen.ox, gen.oy, gen.osgn, gen.ocxy);
+                    mu = cmul(mu, plan_point_pre(xi, gen.px, gen.py, gen.pbeta));
+                    if (hon && (nid & kRingHalve)) mu = make_double2(0.5 * mu.x, 0.5 * mu.y);
+                }
                 double2 o2 = cmul(make_double2(accr, acci), ph);
-                if (mult) o2 = cmul(o2, mu);
+                if (PROC || mult) o2 = cmul(o2, mu);
                 if (hon && hh.two_re) o2 = make_double2(2.0 * o2.x, 0.0);
                 if (hon && hh.out2) hh.out2[hh.perm2[vr]] = make_double2(o2.x, -o2.y);
                 o2.x += ad.x;
@@ -1885,19 +2015,6 @@ __global__ void __launch_bounds__(256) k_band_transpose(const double2* __restric
 }
 
 // Mirrored grid coordinates t' = n - t: the image of a point under the grid
-// reflection m -> -m (mod n). The image's stencil must be exactly the mirror
-// of the point's (start n - s - w + 1 for start s = ceil(t - w/2)); when
-// rounding puts ceil(t' - w/2) one cell off (t - w/2 within an ulp of an
-// integer), t' is nudged by ulps, which moves the taps by rounding only.
-__device__ __forceinline__ double mirror_coord(double t, int n, int w) {
-    const double h = 0.5 * w;
-    const int want = n - (int)ceil(t - h) - w + 1;
-    double m = (double)n - t;
-    for (int it = 0; it < 8 && (int)ceil(m - h) > want; ++it) m = nextafter(m, -1e300);
-    for (int it = 0; it < 8 && (int)ceil(m - h) < want; ++it) m = nextafter(m, 1e300);
-    return m;
-}
-
 __global__ void k_mirror_points(const double2* __restrict__ t, uint64_t n, int n1, int n2, int w,
                                 double2* __restrict__ out) {
     const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -2237,6 +2354,9 @@ struct SpreadTilesRun {
             ck(cudaFuncSetAttribute(k_spread_cta<W, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)SCta<W>::smem_list),
                "smem attr");
+            ck(cudaFuncSetAttribute(k_spread_cta<W, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)SCta<W>::smem_list),
+               "smem attr");
         }
         SpreadOut so;
         if (out) {
@@ -2259,12 +2379,18 @@ struct SpreadTilesRun {
 #define SBD_SPREAD_CTA(C, LI) \
     k_spread_cta<W, C, LI><<<nblk, 128, LI ? SCta<W>::smem_list : SCta<W>::smem, st>>>(P, g, tg, bs, b, pos, \
                                                                                        grid, bs2, herm, so)
-            if (cplx && list) SBD_SPREAD_CTA(true, true);
+            if (so.gen.id && !(cplx && list)) throw Error(3, "procedural nodes need the complex list spread");
+            if (so.gen.id)
+                k_spread_cta<W, true, true, true><<<nblk, 128, SCta<W>::smem_list, st>>>(P, g, tg, bs, b, pos, grid, bs2,
+                                                                                       herm, so);
+            else if (cplx && list) SBD_SPREAD_CTA(true, true);
             else if (cplx) SBD_SPREAD_CTA(true, false);
             else if (list) SBD_SPREAD_CTA(false, true);
             else SBD_SPREAD_CTA(false, false);
 #undef SBD_SPREAD_CTA
-        } else if (use_mma && tg.tr == 16)
+        } else if (so.gen.id)
+            throw Error(3, "procedural nodes need the CTA list spread");
+        else if (use_mma && tg.tr == 16)
             k_spread_mma<W><<<(tg.nbx * so.nby_run + 3) / 4, 128, smem(), st>>>(P, g, tg, bs, b, pos, grid, bs2,
                                                                                herm, so);
         else if (tg.tr == 8)
@@ -2280,8 +2406,9 @@ struct InterpRun {
                     const double2* phase, const double2* mult, const double* dx, const double* dy,
                     const double2* grid, const uint32_t* perm, const double2* addend, double2* out,
                     int acc, int cj, cudaStream_t st, bool trans, const InterpTiles* tiles,
-                    const HermArgs* herm, int variant) {
+                    const HermArgs* herm, int variant, const NodeGen* gen) {
         const HermArgs hh = herm ? *herm : HermArgs{};
+        const NodeGen ng = gen ? *gen : NodeGen{};
         // tensor-core interpolation pays off when outputs are dense on the band
         // (>= 0.25 per cell: the xi side); variant 1 (staged tiles, needs the
         // tile list), 2 (DMMA per warp) or 3 (scalar) forces a choice
@@ -2302,15 +2429,19 @@ struct InterpRun {
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kITW * 32, smem);
                 const unsigned nb = (unsigned)std::min<uint64_t>(tiles->n, (uint64_t)sms * std::max(per, 1) * 8);
                 kern<<<nb, kITW * 32, smem, st>>>(P, g, tiles->start, tiles->n, tiles->shift, tiles->out_lo, n, pos,
-                                            phase, mult, dx, dy, grid, perm, addend, out, hh);
+                                            phase, mult, dx, dy, grid, perm, addend, out, hh, ng);
             };
-            static size_t attr_t = 0, attr_n = 0;  // per W (this template)
-            if (trans)
+            static size_t attr_t = 0, attr_n = 0, attr_p = 0;  // per W (this template)
+            if (ng.id && !trans) throw Error(3, "procedural nodes need the transposed staged interpolation");
+            if (ng.id)
+                go(k_interp_tile<W, true, true>, ITile<W, true>::smem, attr_p);
+            else if (trans)
                 go(k_interp_tile<W, true>, ITile<W, true>::smem, attr_t);
             else
                 go(k_interp_tile<W, false>, ITile<W, false>::smem, attr_n);
             return;
         }
+        if (ng.id) throw Error(3, "procedural nodes need the staged interpolation");
         if (use_mma && !acc && !cj) {
             const uint64_t warps = (n + 31) / 32;
             const unsigned grid_blocks = (unsigned)std::min<uint64_t>((warps + 3) / 4, 148ull * 16);
@@ -2333,6 +2464,44 @@ struct InterpRun {
 };
 
 } // namespace
+
+void launch_ring_nodes(const uint32_t* id, uint64_t n, const RingRow* rings, double2* xi, double2* w,
+                       cudaStream_t st) {
+    if (!n) return;
+    k_ring_nodes<<<blocks(n, 256), 256, 0, st>>>(id, n, rings, xi, w);
+    count_launch();
+    ck(cudaGetLastError(), "k_ring_nodes");
+}
+
+double node_deviation(const double2* a, const double2* b, uint64_t n, cudaStream_t st) {
+    if (!n) return 0.0;
+    DevBuf<unsigned long long> worst(1);
+    ck(cudaMemsetAsync(worst.p, 0, sizeof(unsigned long long), st), "node deviation");
+    k_node_deviation<<<blocks(n, 256), 256, 0, st>>>(a, b, n, worst.p);
+    count_launch();
+    unsigned long long bits = 0;
+    ck(cudaMemcpyAsync(&bits, worst.p, sizeof(bits), cudaMemcpyDeviceToHost, st), "node deviation");
+    ck(cudaStreamSynchronize(st), "node deviation");
+    double d;
+    static_assert(sizeof(d) == sizeof(bits), "double bits");
+    std::memcpy(&d, &bits, sizeof(d));
+    return d;
+}
+
+void launch_ring_point_arrays(const NodeGen& gen, uint64_t n, double2* t, double2* pre, cudaStream_t st) {
+    if (!n) return;
+    k_ring_point_arrays<<<blocks(n, 256), 256, 0, st>>>(gen, n, t, pre);
+    count_launch();
+    ck(cudaGetLastError(), "k_ring_point_arrays");
+}
+
+void launch_ring_output_arrays(const NodeGen& gen, uint64_t n, double2* s, double2* post, double2* kappa,
+                               double2* kappa_h, cudaStream_t st) {
+    if (!n) return;
+    k_ring_output_arrays<<<blocks(n, 256), 256, 0, st>>>(gen, n, s, post, kappa, kappa_h);
+    count_launch();
+    ck(cudaGetLastError(), "k_ring_output_arrays");
+}
 
 void launch_plan_points(const double2* pts, uint64_t n, Axis ax, Axis ay, double beta,
                         double2* t, double2* pre, cudaStream_t st) {
@@ -2477,10 +2646,10 @@ void launch_interp(int w, const WindowPoly& win, GridGeom g, uint64_t n, const d
                    const double2* phase, const double2* mult, const double* dx, const double* dy,
                    const double2* grid, const uint32_t* perm, double2* out, int accumulate,
                    int conj_out, cudaStream_t st, const double2* addend, bool transposed,
-                   const InterpTiles* tiles, const HermArgs* herm, int variant) {
+                   const InterpTiles* tiles, const HermArgs* herm, int variant, const NodeGen* gen) {
     if (!n) return;
     dispatch_w<InterpRun>(w, win, g, n, pos, phase, mult, dx, dy, grid, perm, addend, out,
-                          accumulate, conj_out, st, transposed, tiles, herm, variant);
+                          accumulate, conj_out, st, transposed, tiles, herm, variant, gen);
     count_launch();
     ck(cudaGetLastError(), "k_interp");
 }

@@ -262,6 +262,7 @@ void sbd_op_options_default(sbd_op_options* o) {
     o->interp_kernel = 0;
     o->fused = 1;
     o->verbose = 0;
+    o->procedural_rings = 0;
 }
 
 static void check_options(const sbd_op_options& o) {
@@ -357,6 +358,7 @@ int sbd_op_info(const sbd_op* op, sbd_op_info_t* info) {
         info->n2_out = po.ay.n;
         info->bytes = op->ref_bytes();
         info->device_bytes = op->device_bytes();
+        info->procedural_rings = op->procedural ? 1 : 0;
     });
 }
 

@@ -101,6 +101,140 @@ struct sbd_op {
     cudaStream_t last_stream = nullptr;
     bool have_last = false;
 
+    // Procedural ring nodes (sbd_op_options::procedural_rings; SURVEY 8f item
+    // 3): the ring table and the node ids in the three orders the xi-side
+    // kernels run in; the per-node arrays are then released and rebuilt by
+    // ensure_node_arrays() for the paths that still read them.
+    bool procedural = false;      // the xi-side kernels regenerate the nodes
+    bool nodes_released = false;  // ... and the per-node arrays are not resident
+    DevBuf<RingRow> ring_rows;
+    DevBuf<uint32_t> id_sorted;   // canonical (fwd_out point) order
+    DevBuf<uint32_t> id_z;        // fwd_in output (interpolation) order, bit 31 = halved under the split
+    NodeGen node_gen(const uint32_t* ids) const {
+        NodeGen g;
+        g.id = ids;
+        g.rings = ring_rows.p;
+        g.ox = fwd_in->ax;
+        g.oy = fwd_in->ay;
+        g.osgn = (double)fwd_in->sign;
+        g.ocxy = fwd_in->out_cxy();
+        g.px = fwd_out->ax;
+        g.py = fwd_out->ay;
+        g.pbeta = fwd_out->beta;
+        return g;
+    }
+
+    // Ring table and per-node ids (file order) when every ring of the file is
+    // M equal-weight nodes rho (cos, sin)(2 pi j / M) -- what
+    // build_ring_quadrature (ring_quadrature.cpp:51-66) writes: checked here on
+    // the weights and sizes, and on the device against the file's coordinates.
+    bool ring_table(std::vector<RingRow>& rows, std::vector<uint32_t>& ids) const {
+        const uint64_t nx = d.n_xi();
+        const size_t nr = d.ring_offsets.size() < 2 ? 0 : d.ring_offsets.size() - 1;
+        if (!nx || !nr || nr >= (1u << (31 - kRingJBits)) || d.ring_offsets.front() != 0 ||
+            (uint64_t)d.ring_offsets.back() != nx)
+            return false;
+        rows.resize(nr);
+        ids.resize(nx);
+        for (size_t r = 0; r < nr; ++r) {
+            const uint64_t a = (uint64_t)d.ring_offsets[r], b = (uint64_t)d.ring_offsets[r + 1];
+            if (b <= a || b - a >= (1ull << kRingJBits)) return false;
+            const uint64_t m = b - a;
+            // node 0 sits at angle 0: (rho, 0) exactly
+            if (d.freqs[2 * a + 1] != 0.0 || !(d.freqs[2 * a] >= 0.0)) return false;
+            rows[r].rho = d.freqs[2 * a];
+            rows[r].two_over_m = 2.0 / (double)m;
+            rows[r].wre = d.weights[2 * a];
+            rows[r].wim = d.weights[2 * a + 1];
+            for (uint64_t j = 0; j < m; ++j) {
+                if (d.weights[2 * (a + j)] != rows[r].wre || d.weights[2 * (a + j) + 1] != rows[r].wim) return false;
+                ids[a + j] = (uint32_t)(r << kRingJBits) | (uint32_t)j;
+            }
+        }
+        return true;
+    }
+
+    // Rebuild the per-node arrays a procedural operator released (adjoint,
+    // slab and unfused paths read them). Same device functions as the kernels.
+    void ensure_node_arrays(cudaStream_t st) {
+        if (!nodes_released) return;
+        const uint64_t nx = d.n_xi();
+        const NodeGen gs = node_gen(id_sorted.p), gz = node_gen(id_z.p);
+        fwd_out->t.alloc(nx);
+        fwd_out->pre.alloc(nx);
+        launch_ring_point_arrays(gs, nx, fwd_out->t.p, fwd_out->pre.p, st);
+        fwd_in->s.alloc(nx);
+        fwd_in->post.alloc(nx);
+        kappa.alloc(nx);
+        if (herm_ok) kappa_h.alloc(nx);
+        launch_ring_output_arrays(gz, nx, fwd_in->s.p, fwd_in->post.p, kappa.p, herm_ok ? kappa_h.p : nullptr, st);
+        w_sorted.alloc(nx);
+        launch_ring_nodes(id_sorted.p, nx, ring_rows.p, nullptr, w_sorted.p, st);
+        w_in.alloc(nx);
+        launch_ring_nodes(id_z.p, nx, ring_rows.p, nullptr, w_in.p, st);
+        if (fwd_out->hrole == 2 && fwd_out->n0_pts) {
+            // mirror images in their tile order: hv_t[k] = mirror(t[hv_src[k]])
+            DevBuf<double2> m(fwd_out->n0_pts);
+            launch_mirror_points(fwd_out->t.p, fwd_out->n0_pts, fwd_out->ax.n, fwd_out->ay.n, fwd_out->w, m.p, st);
+            fwd_out->hv_t.alloc(fwd_out->n0_pts);
+            launch_gather(m.p, fwd_out->hv_src.p, fwd_out->hv_t.p, fwd_out->n0_pts, st);
+            ck(cudaStreamSynchronize(st), "node arrays");
+        }
+        ck(cudaStreamSynchronize(st), "node arrays");
+        nodes_released = false;
+        if (opt.verbose) std::fprintf(stderr, "[sbd] procedural rings: per-node arrays rebuilt\n");
+    }
+
+    // After the plans, the fused arrays and the half split exist: hand the ids
+    // to the plans and drop the per-node arrays the forward path no longer reads.
+    void enable_procedural(const std::vector<uint32_t>& ids_file, const std::vector<uint64_t>& halve) {
+        const uint64_t nx = d.n_xi();
+        if (!fused || !fwd_in->n_out_tiles || fwd_out->opts.spread_kernel != 0 || !fwd_out->rl1_s.n) {
+            if (opt.verbose) std::fprintf(stderr, "[sbd] procedural rings off: needs the fused staged path\n");
+            return;
+        }
+        std::vector<uint32_t> hs(nx);
+        for (uint64_t i = 0; i < nx; ++i) hs[i] = ids_file[perm_xi[i]];
+        id_sorted.upload(hs.data(), nx, stream);
+        // fwd_in's output order: position v holds canonical node perm_s[v]
+        std::vector<uint32_t> ps(nx);
+        if (fwd_in->perm_s.n)
+            ck(cudaMemcpyAsync(ps.data(), fwd_in->perm_s.p, nx * 4, cudaMemcpyDeviceToHost, stream), "perm");
+        else
+            for (uint64_t i = 0; i < nx; ++i) ps[i] = (uint32_t)i;
+        ck(cudaStreamSynchronize(stream), "perm");
+        std::vector<uint32_t> hz(nx);
+        for (uint64_t v = 0; v < nx; ++v) hz[v] = hs[ps[v]];
+        if (herm_ok && !halve.empty()) {
+            std::vector<uint32_t> inv_xi(nx), pos_of(nx);
+            for (uint64_t i = 0; i < nx; ++i) inv_xi[perm_xi[i]] = (uint32_t)i;
+            for (uint64_t v = 0; v < nx; ++v) pos_of[ps[v]] = (uint32_t)v;
+            for (uint64_t f : halve) hz[pos_of[inv_xi[f]]] |= kRingHalve;
+        }
+        id_z.upload(hz.data(), nx, stream);
+        ck(cudaStreamSynchronize(stream), "node ids");
+        fwd_out->gen_pts = node_gen(id_sorted.p);
+        fwd_in->gen_out = node_gen(id_z.p);
+        procedural = true;
+        // release: the nodes as fwd_out's points and fwd_in's outputs, the
+        // mirror images, omega-hat and kappa in both orders
+        fwd_out->t = DevBuf<double2>();
+        fwd_out->pre = DevBuf<double2>();
+        fwd_out->pts = DevBuf<double2>();
+        fwd_out->hv_t = DevBuf<double2>();
+        fwd_in->s = DevBuf<double2>();
+        fwd_in->post = DevBuf<double2>();
+        fwd_in->frq = DevBuf<double2>();
+        kappa = DevBuf<double2>();
+        kappa_h = DevBuf<double2>();
+        w_sorted = DevBuf<double2>();
+        w_in = DevBuf<double2>();
+        nodes_released = true;
+        if (opt.verbose)
+            std::fprintf(stderr, "[sbd] procedural rings on: %zu rings, per-node arrays released\n",
+                         (size_t)ring_rows.n);
+    }
+
     sbd_op() { sbd_op_options_default(&opt); }
     ~sbd_op() {
         for (Slot& sl : slot)
@@ -147,9 +281,34 @@ struct sbd_op {
         std::vector<uint8_t> tag;
         std::vector<uint64_t> halve;
         const bool split = herm_pairs(tag, halve);
+        // procedural rings: the nodes both plans are built from are generated
+        // on the device (file order) and must agree with the file's to rounding
+        std::vector<uint32_t> ids_file;
+        DevBuf<double2> xi_gen;
+        bool proc = false;
+        if (opt.procedural_rings) {
+            std::vector<RingRow> rows;
+            if (ring_table(rows, ids_file)) {
+                const uint64_t nx = d.n_xi();
+                ring_rows.upload(rows.data(), rows.size(), stream);
+                DevBuf<uint32_t> idf;
+                idf.upload(ids_file.data(), nx, stream);
+                DevBuf<double2> xi_file;
+                xi_file.upload(reinterpret_cast<const double2*>(d.freqs.data()), nx, stream);
+                xi_gen.alloc(nx);
+                launch_ring_nodes(idf.p, nx, ring_rows.p, xi_gen.p, nullptr, stream);
+                const double dev = node_deviation(xi_file.p, xi_gen.p, nx, stream);
+                proc = dev <= 1e-13;
+                if (opt.verbose)
+                    std::fprintf(stderr, "[sbd] procedural rings: generated nodes within %.2e of the file's\n", dev);
+            } else if (opt.verbose) {
+                std::fprintf(stderr, "[sbd] procedural rings off: the file's nodes are not equal-weight rings\n");
+            }
+        }
         // fwd_out = Plan(xi, tgt, +): xi take this plan's sorted order.
         fwd_out = std::make_unique<Plan>(d.freqs.data(), d.n_xi(), tgt, d.n_tgt(), +1, o, device,
-                                         true, true, stream, split ? tag.data() : nullptr);
+                                         true, true, stream, split ? tag.data() : nullptr, nullptr,
+                                         proc ? xi_gen.p : nullptr);
         perm_xi = fwd_out->adopt_point_order(stream);
         std::vector<double> xi_sorted(2 * d.n_xi()), w_host(2 * d.n_xi());
         for (uint64_t i = 0; i < d.n_xi(); ++i) {
@@ -167,9 +326,19 @@ struct sbd_op {
             tag_sorted.resize(d.n_xi());
             for (uint64_t i = 0; i < d.n_xi(); ++i) tag_sorted[i] = tag[perm_xi[i]];
         }
+        DevBuf<double2> xi_gen_sorted;
+        if (proc) {
+            // the generated nodes in the canonical order
+            DevBuf<uint32_t> pd;
+            pd.upload(perm_xi.data(), d.n_xi(), stream);
+            xi_gen_sorted.alloc(d.n_xi());
+            launch_gather(xi_gen.p, pd.p, xi_gen_sorted.p, d.n_xi(), stream);
+            ck(cudaStreamSynchronize(stream), "generated nodes");
+        }
         fwd_in = std::make_unique<Plan>(d.src.data(), d.n_src(), xi_sorted.data(), d.n_xi(), -1, o,
                                         device, true, true, stream,
-                                        nullptr, split ? tag_sorted.data() : nullptr);
+                                        nullptr, split ? tag_sorted.data() : nullptr, nullptr,
+                                        proc ? xi_gen_sorted.p : nullptr);
         w_sorted.upload(reinterpret_cast<const double2*>(w_host.data()), d.n_xi(), stream);
         w_in.alloc(std::max<uint64_t>(d.n_xi(), 1));
         if (fwd_in->perm_s.n)
@@ -186,6 +355,7 @@ struct sbd_op {
         build_fused();
         if (split) build_half(halve);
         if (herm_ok) build_hfft();
+        if (proc) enable_procedural(ids_file, halve);
     }
 
     void build_hfft() {
@@ -603,6 +773,7 @@ struct sbd_op {
 
     // conv_operator.cpp:311-324: A^H u = conj(fwd_in^T (w . fwd_out^T conj(u))) + D^H u
     void apply_adjoint_one(const double2* u, double2* q, cudaStream_t st) {
+        ensure_node_arrays(st);
         if (!dT_ready) build_adjoint_csr(st);
         if (fused) {
             if (tm.on) tm.start("spmv_adjoint");
@@ -626,7 +797,7 @@ struct sbd_op {
                qs.bytes() + work.bbuf.bytes() +
                cols.bytes() + vals.bytes() + work.grid.bytes() + work.T.bytes() + work.band.bytes() +
                spec.bytes() + hf.bytes() + hq.bytes() + kappa_h.bytes() + roT.bytes() + colsT.bytes() +
-               valsT.bytes() + u_sorted.bytes() + qsT.bytes();
+               valsT.bytes() + u_sorted.bytes() + qsT.bytes() + id_sorted.bytes() + id_z.bytes() + ring_rows.bytes();
     }
 
     // conv_operator.cpp:338-353

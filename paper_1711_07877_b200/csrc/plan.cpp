@@ -79,12 +79,14 @@ int stencil_start_output(const Axis& a, double f, double sg, int w) {
 
 Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf_, int sign_,
            const NufftOpts& o, int dev, bool sort_points, bool sort_outputs, cudaStream_t st,
-           const uint8_t* pt_tag, const uint8_t* out_tag)
+           const uint8_t* pt_tag, const uint8_t* out_tag, const double2* dev_pts, const double2* dev_frq)
     : sign(sign_ > 0 ? 1 : -1), device(dev), np(np_), nf(nf_), opts(o) {
     const uint64_t work = np * nf;
     const bool direct = o.mode == 1 || (o.mode == 0 && work <= o.direct_threshold);
     pts.upload(reinterpret_cast<const double2*>(pts_xy), np, st);
     frq.upload(reinterpret_cast<const double2*>(frq_xy), nf, st);
+    if (dev_pts && np) ck(cudaMemcpyAsync(pts.p, dev_pts, np * 16, cudaMemcpyDeviceToDevice, st), "device points");
+    if (dev_frq && nf) ck(cudaMemcpyAsync(frq.p, dev_frq, nf * 16, cudaMemcpyDeviceToDevice, st), "device freqs");
     if (direct) {
         fast = false;
         ck(cudaStreamSynchronize(st), "plan upload");
@@ -245,6 +247,11 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
               "cufftPlanMany cols T");
     }
     ck(cudaStreamSynchronize(st), "plan build");
+}
+
+double Plan::out_cxy() const {
+    const double kPi = 3.14159265358979323846;
+    return (2.0 * kPi / (ax.n * ax.gamma)) * (2.0 * kPi / (ay.n * ay.gamma));
 }
 
 Plan::~Plan() {
@@ -519,6 +526,11 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
     ensure_work(wk, st);
     const GridGeom g{ax.n, ay.n, 0.5 * w};
     const int n2 = ay.n;
+    // procedural sides: ids restricted like the arrays they replace
+    NodeGen go = gen_out;
+    if (go.id) go.id += out_lo;
+    const NodeGen* gop = go.id ? &go : nullptr;
+    if (gen_pts.id && !in_is_b) throw Error(3, "procedural points take their coefficients as b");
     if (tm) tm->start(tag_spread);
     const double2* b = in;
     if (!in_is_b) {
@@ -568,7 +580,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         }
         // with the radix pass the column factors are already in the band
         launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx.p, hrad > 1 ? nullptr : dy_band.p, hC.p, perm_p,
-                      out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles, hp, opts.interp_kernel);
+                      out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles, hp, opts.interp_kernel, gop);
         if (tm) tm->stop();
         return;
     }
@@ -588,6 +600,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         // partner's (only images near the m2 = n2/2 line are ever read)
         so.src2 = hv_src.p;
         so.lists = lists(true);
+        so.gen = gen_pts;
         launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, hA.p, st, hv_bins.p, nullptr, &so, nullptr,
                             opts.spread_kernel);
         if (tm) tm->stop();
@@ -627,8 +640,20 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
     else if (wk.g_pitch)  // written by a plan of another grid size: clear all of it
         zero_rect_minus(wk.grid.p, wk.g_pitch, wk.gr0, wk.gr1, wk.gc0, wk.gc1, 0, 0, 0, 0, st);
     const SpreadLists sl = lists(false);
-    launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, wk.grid.p, st, bs2, hflag, nullptr, &sl,
-                        opts.spread_kernel);
+    if (gen_pts.id) {
+        SpreadOut so;  // the default full-grid output with the procedural points
+        so.mode = 0;
+        so.rend = ax.n;
+        so.cend = n2;
+        so.pitch = (size_t)n2;
+        so.nby_run = tg.nby;
+        so.gen = gen_pts;
+        launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, wk.grid.p, st, bs2, hflag, &so, &sl,
+                            opts.spread_kernel);
+    } else {
+        launch_spread_tiles(w, win, g, tg, bin_start.p, b, t.p, wk.grid.p, st, bs2, hflag, nullptr, &sl,
+                            opts.spread_kernel);
+    }
     wk.gr0 = rlo;
     wk.gr1 = rhi;
     wk.gc0 = clo;
@@ -672,7 +697,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         if (tm) tm->start(tag_interp);
         const GridGeom gt{ax.n, bc, 0.5 * w};
         launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx.p, dy_band.p, wk.bandT.p, perm_p,
-                      out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles, hp, opts.interp_kernel);
+                      out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles, hp, opts.interp_kernel, gop);
         if (tm) tm->stop();
         return;
     }

@@ -177,13 +177,39 @@ struct SpreadLists {
 
 struct HermArgs;
 
+// Procedural ring nodes (ring_quadrature.cpp:24-69): node j
+// of ring p is rho_p (cos, sin)(2 pi j / M_p) with weight w_p, so the xi-side
+// kernels can regenerate a node's plan arrays (grid / mode coordinates,
+// prephase, postphase, omega-hat) from a 4-byte id instead of streaming them.
+// id = ring << kRingJBits | j; bit 31: the node enters the real-input half
+// split with weight 1/2 (op_internal.h herm_pairs).
+constexpr int kRingJBits = 17;
+constexpr uint32_t kRingHalve = 0x80000000u;
+struct RingRow {
+    double rho, two_over_m, wre, wim;
+};
+struct NodeGen {
+    const uint32_t* id = nullptr;  // ids in the consuming kernel's node order
+    const RingRow* rings = nullptr;
+    Axis ox, oy;                   // the nodes as a plan's outputs (fwd_in): mode coordinates, postphase
+    double osgn = 1.0, ocxy = 1.0;
+    Axis px, py;                   // the nodes as a plan's points (fwd_out): grid coordinates, prephase
+    double pbeta = 0.0;
+};
+
 class Plan {
   public:
     // pt_tag / out_tag (optional, caller order, 0/1): sort tag-0 entries before
     // tag-1 entries on that side (the real-input half split, op.cpp)
+    // dev_pts / dev_frq (optional, device, caller order): the values the
+    // per-point / per-output arrays are computed from instead of the uploaded
+    // host copies (procedural ring nodes: generated on the device, so that the
+    // xi-side kernels regenerate them bitwise; the geometry still comes from
+    // the host arrays)
     Plan(const double* pts_xy, uint64_t np, const double* frq_xy, uint64_t nf, int sign,
          const NufftOpts& opts, int device, bool sort_points, bool sort_outputs, cudaStream_t st,
-         const uint8_t* pt_tag = nullptr, const uint8_t* out_tag = nullptr);
+         const uint8_t* pt_tag = nullptr, const uint8_t* out_tag = nullptr,
+         const double2* dev_pts = nullptr, const double2* dev_frq = nullptr);
     ~Plan();
     Plan(const Plan&) = delete;
     Plan& operator=(const Plan&) = delete;
@@ -259,6 +285,13 @@ class Plan {
     }
     DevBuf<double> hdx_band;          // role 2: deconvolution of the band rows
     bool enable_hfft(int role, cudaStream_t st);
+
+    // Procedural sides (op_internal.h): with gen_*.id set the pruned forward
+    // path regenerates the side's arrays in its kernels, and t / pre / pts /
+    // hv_t (points) or s / post / frq (outputs) may be released; every other
+    // path needs them materialised again (sbd_op::ensure_node_arrays).
+    NodeGen gen_pts, gen_out;
+    double out_cxy() const;  // postphase scale (nufft.cpp:183-184)
 
     uint64_t cells() const { return fast ? (uint64_t)ax.n * (uint64_t)ay.n : 0; }
     size_t device_bytes() const;
@@ -355,6 +388,7 @@ struct SpreadOut {
     const uint32_t* src2 = nullptr;  // mirror image -> tag-0 partner (b2 = conj(b[src2]))
     SpreadLists lists;
     int cx0 = 0, ncx_run = 0;  // CTA spread: run region rows [cx0, cx0 + ncx_run) only (0: all)
+    NodeGen gen;               // gen.id != nullptr: procedural points (pos / pos2 are not read)
 };
 
 // ---------------------------------------------------------------- kernels
@@ -368,6 +402,14 @@ struct GridGeom {
     unsigned rad_magic = 0;
 };
 
+// procedural ring nodes: xi / w (either may be null) of the ids; the largest
+// |a - b| / |a| over n nodes; the plan arrays of ids in a kernel's order
+void launch_ring_nodes(const uint32_t* id, uint64_t n, const RingRow* rings, double2* xi, double2* w,
+                       cudaStream_t st);
+double node_deviation(const double2* a, const double2* b, uint64_t n, cudaStream_t st);
+void launch_ring_point_arrays(const NodeGen& gen, uint64_t n, double2* t, double2* pre, cudaStream_t st);
+void launch_ring_output_arrays(const NodeGen& gen, uint64_t n, double2* s, double2* post, double2* kappa,
+                               double2* kappa_h, cudaStream_t st);
 void launch_plan_points(const double2* pts, uint64_t n, Axis ax, Axis ay, double beta,
                         double2* t, double2* pre, cudaStream_t st);
 void launch_plan_outputs(const double2* frq, uint64_t n, Axis ax, Axis ay, double sgn,
@@ -490,7 +532,8 @@ void launch_interp(int w, const WindowPoly& win, GridGeom g, uint64_t n, const d
                    const double2* grid, const uint32_t* perm, double2* out, int accumulate,
                    int conj_out, cudaStream_t st, const double2* addend = nullptr,
                    bool transposed = false, const InterpTiles* tiles = nullptr,
-                   const HermArgs* herm = nullptr, int variant = 0);  // variant: NufftOpts::interp_kernel
+                   const HermArgs* herm = nullptr, int variant = 0,  // variant: NufftOpts::interp_kernel
+                   const NodeGen* gen = nullptr);  // procedural outputs (staged transposed path)
 // map[new] = old sorted position: outputs of each Z-order block dealt round-robin
 // over the shared-memory banks of the staged real target interpolation
 void bank_interleave_outputs(const uint32_t* tile_start, uint32_t ntiles, const double2* pos, uint64_t n, int w,

@@ -488,6 +488,7 @@ int sbd_slab_create(sbd_op* op, int rank, int world, sbd_slab** out) {
         if (!op->fused) throw Error(SBD_ERR_RUNTIME, "slab decomposition needs both NUFFTs on the gridded path");
         std::lock_guard<std::recursive_mutex> lk(op->mu);
         DeviceGuard g(op->device);
+        op->ensure_node_arrays(op->stream);  // a procedural operator: the slab plan reads the per-node arrays
         auto s = std::make_unique<sbd_slab>();
         s->op = op;
         s->rank = rank;

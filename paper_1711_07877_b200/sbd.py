@@ -109,12 +109,14 @@ class OpOptions:
     interp_kernel: str = "auto"   # auto | tile | mma | scalar
     fused: bool = True
     verbose: bool = False
+    procedural_rings: bool = False  # regenerate the xi nodes in the kernels instead of storing their arrays
 
     def _c(self) -> _capi.OpOptionsC:
         sk = {"lists": 0, "bins": 1, "warp": 2, "scalar": 3}[self.spread_kernel]
         ik = {"auto": 0, "tile": 1, "mma": 2, "scalar": 3}[self.interp_kernel]
         return _capi.OpOptionsC(int(self.real_input_split), int(self.hermitian_fft),
-                                int(self.radix_first_pass), sk, ik, int(self.fused), int(self.verbose))
+                                int(self.radix_first_pass), sk, ik, int(self.fused), int(self.verbose),
+                                int(self.procedural_rings))
 
 
 @dataclasses.dataclass

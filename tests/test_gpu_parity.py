@@ -353,6 +353,58 @@ def test_spread_variants_agree(spread):
             assert rel_l2(other.apply(x), base.apply(x)) <= 1e-13, (name, spread)
 
 
+@pytest.mark.parametrize("name", CASES)
+def test_procedural_rings_match_reference(ops, name):
+    # SURVEY 8f item 3 (ring_quadrature.cpp:24-69): the xi-side kernels
+    # regenerate every ring node (coordinates, phases, omega-hat) from
+    # (rho_p, M_p, weight_p, j) and the per-node arrays are released. Same
+    # parity bar against the reference goldens (apply for real and complex f,
+    # and the adjoint, which rebuilds the arrays with the same device
+    # functions); against the stored-array operator to rounding of the nodes.
+    path, g = golden(name)
+    proc = sbd.CompressedOperator.load(path, options=sbd.OpOptions(procedural_rings=True))
+    info = proc.info()
+    q = proc.apply(g["f"])
+    assert rel_l2(q, g["q"]) <= PARITY
+    # (a generated coordinate an ulp off the file's can move a stencil that
+    # starts on a cell boundary by one cell: taps of ~1e-11 relative weight)
+    assert rel_l2(q, ops[name].apply(g["f"])) <= 1e-10
+    assert np.array_equal(q, proc.apply(g["f"]))  # reproducible
+    rng = np.random.default_rng(9)
+    fc = rng.standard_normal(len(g["f"])) + 1j * rng.standard_normal(len(g["f"]))
+    assert rel_l2(proc.apply(fc), ops[name].apply(fc)) <= 1e-10
+    if info["fast_in"] and info["fast_out"]:
+        # every golden operator's nodes are the reference's ring quadrature
+        assert info["procedural_rings"] == 1, name
+        assert info["device_bytes"] < ops[name].info()["device_bytes"]
+    else:
+        assert info["procedural_rings"] == 0
+    assert rel_l2(proc.apply_adjoint(g["u"]), g["qa"]) <= PARITY
+    assert rel_l2(proc.apply(g["f"]), g["q"]) <= PARITY  # forward again after the arrays were rebuilt
+
+
+def test_procedural_rings_refuse_foreign_nodes(tmp_path):
+    # a file whose nodes are not ring-generated (one node moved off its ring)
+    # keeps the stored arrays: the option is a request, the info says what runs
+    import struct
+
+    src = os.path.join(GOLDEN, "lap_disk_n1000.sbdop")
+    base = sbd.CompressedOperator.load(src)
+    xi = base.quadrature().freqs.copy()
+    raw = bytearray(open(src, "rb").read())
+    probe = struct.pack("<2d", xi[5, 0], xi[5, 1])
+    at = raw.find(probe)
+    assert at > 0
+    raw[at:at + 16] = struct.pack("<2d", xi[5, 0] * (1 + 1e-9), xi[5, 1])
+    moved = tmp_path / "moved.sbdop"
+    moved.write_bytes(bytes(raw))
+    op = sbd.CompressedOperator.load(str(moved), options=sbd.OpOptions(procedural_rings=True))
+    assert op.info()["procedural_rings"] == 0
+    ref = sbd.CompressedOperator.load(str(moved))
+    f = np.random.default_rng(3).standard_normal(op.n_src()) + 0j
+    assert np.array_equal(op.apply(f), ref.apply(f))
+
+
 @pytest.mark.parametrize("name", HALF_CASES)
 def test_radix_first_pass_agrees(ops, name):
     # Hermitian source side: the radix-r first pass of the column transform

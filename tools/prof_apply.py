@@ -17,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="4")
 ap.add_argument("--scale", type=float, default=1.0)
 ap.add_argument("--applies", type=int, default=3)
+ap.add_argument("--verbose", type=int, default=0)
 a = ap.parse_args()
 w = bench.workload(a.config, a.scale)
 z = w["z"]
@@ -24,7 +25,8 @@ d = sbd.cloud_diameter(z)
 kern = sbd.kernel_helmholtz(w["kappa"] / d) if w["kind"] else sbd.kernel_laplace()
 op = sbd.CompressedOperator.assemble(
     kern, z, opts=sbd.AssembleOptions(eps=w["eps"], a_override=(w["dmin"] / d if w["dmin"] else 0.0),
-                                      max_grid_bytes=96 << 30))
+                                      max_grid_bytes=96 << 30,
+                                      pipeline=sbd.OpOptions(verbose=bool(a.verbose))))
 f = bench.rhs(w, len(z), np.random.default_rng(1))
 fd = torch.from_numpy(f.view(np.float64).copy()).cuda()
 qd = torch.empty_like(fd)
