@@ -2130,19 +2130,67 @@ __device__ __forceinline__ void dft_small(const double2 (&x)[R], double2 (&y)[R]
     }
 }
 
+// Radix-R first pass of contiguous length n = R M transforms (rows of X, row
+// pitch n), as its own streaming kernel: Y[row][s M + k] = w_n^{s k} sum_rho
+// X[row][k + M rho] w_R^{s rho}. A batched contiguous length-M cuFFT pass then
+// leaves mode j at (j mod R) M + j / R, where the consumer reads it -- cuFFT's
+// own second pass of a length-n transform writes with stride R at ~58% of the
+// contiguous pass's bandwidth. Columns outside [c_lo, c_hi) are known zeros
+// (the spread's populated range) and are not read.
+template <int R>
+__global__ void __launch_bounds__(256) k_dif_rows(const double2* __restrict__ X, int n, int M, int c_lo, int c_hi,
+                                                  const double2* __restrict__ tw, double2* __restrict__ Y) {
+    const int k = blockIdx.x * 256 + threadIdx.x;
+    if (k >= M) return;
+    const size_t row = (size_t)blockIdx.y * (size_t)n;
+    double2 x[R], y[R];
+#pragma unroll
+    for (int rho = 0; rho < R; ++rho) {
+        const int c = k + M * rho;
+        x[rho] = (c >= c_lo && c < c_hi) ? X[row + c] : make_double2(0.0, 0.0);
+    }
+    dft_small<R>(x, y, tw, M);
+#pragma unroll
+    for (int sI = 0; sI < R; ++sI) Y[row + (size_t)sI * M + k] = sI ? cmul(y[sI], __ldg(tw + sI * k)) : y[sI];
+}
+
 // k_untangle_transpose with the radix-R first pass of the column transform
 // folded in: the band columns c < B of the untangled real rows x[m1] (rows
 // [r0, r0 + 2 nr), zero elsewhere) leave as y_s[k] (column c at c * n1 +
 // s M + k, n1 = R M) for a batched length-M column transform.
-template <int R>
+// RIN > 1: the rows of T come from a radix-RIN first pass + length n2 / RIN
+// transforms (k_dif_rows), mode j at (j mod RIN) MR + j / RIN; a CTA then takes
+// the 32 columns RIN (l0 + lane) + cls of one residue class, which are
+// contiguous there (and so are their mirrors n2 - c).
+template <int R, int RIN = 1>
 __global__ void __launch_bounds__(256, 5) k_untangle_dif(const double2* __restrict__ T, int n2, int nr, int B,
                                                       double2* __restrict__ Tt, int n1, int r0, int M,
                                                       const double2* __restrict__ tw,
                                                       const double* __restrict__ colf) {
     __shared__ double2 so[R][8][33];
-    const int c0 = blockIdx.x * 32, k0 = blockIdx.y * 8;
+    const int k0 = blockIdx.y * 8;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int c = c0 + lane, k = k0 + w;
+    const int MR = n2 / RIN;
+    // columns of this CTA: c(i) = cbase + cstep i, i < 32
+    int cbase, cstep, pa, pb, pbstep;  // positions of column c and of its mirror in a row of T
+    if (RIN > 1) {
+        const int per = ((B + RIN - 1) / RIN + 31) / 32;  // CTAs per residue class
+        const int cls = blockIdx.x / per, l0 = (blockIdx.x - cls * per) * 32;
+        cbase = RIN * l0 + cls;
+        cstep = RIN;
+        pa = cls * MR + l0 + lane;
+        // n2 - c = RIN (MR - l) (cls 0) or RIN (MR - 1 - l) + (RIN - cls)
+        pb = cls ? (RIN - cls) * MR + MR - 1 - (l0 + lane) : (l0 + lane ? MR - (l0 + lane) : 0);
+        pbstep = 0;
+    } else {
+        cbase = blockIdx.x * 32;
+        cstep = 1;
+        pa = cbase + lane;
+        pb = pa ? n2 - pa : 0;
+        pbstep = 0;
+    }
+    (void)pbstep;
+    const int c = cbase + cstep * lane, k = k0 + w;
     double2 x[R], y[R];
 #pragma unroll
     for (int rho = 0; rho < R; ++rho) {
@@ -2150,7 +2198,7 @@ __global__ void __launch_bounds__(256, 5) k_untangle_dif(const double2* __restri
         x[rho] = make_double2(0.0, 0.0);
         if (c < B && m1 >= r0 && m1 < r0 + 2 * nr) {
             const int kk = (m1 - r0) >> 1;
-            const double2 a = T[(size_t)kk * n2 + c], b = T[(size_t)kk * n2 + (c ? n2 - c : 0)];
+            const double2 a = T[(size_t)kk * n2 + pa], b = T[(size_t)kk * n2 + pb];
             x[rho] = ((m1 - r0) & 1) ? make_double2(0.5 * (a.y + b.y), -0.5 * (a.x - b.x))
                                      : make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
         }
@@ -2169,7 +2217,8 @@ __global__ void __launch_bounds__(256, 5) k_untangle_dif(const double2* __restri
     const int kl = threadIdx.x & 7;
     for (int p = threadIdx.x >> 3; p < 32 * R; p += 32) {
         const int sI = p >> 5, cl = p & 31;
-        if (c0 + cl < B) Tt[(size_t)(c0 + cl) * n1 + (size_t)sI * M + k0 + kl] = so[sI][kl][cl];
+        const int co = cbase + cstep * cl;
+        if (co < B) Tt[(size_t)co * n1 + (size_t)sI * M + k0 + kl] = so[sI][kl][cl];
     }
 }
 
@@ -2945,12 +2994,33 @@ void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int 
     ck(cudaGetLastError(), "k_band_transpose");
 }
 
+void launch_dif_rows(const double2* X, int rows, int n, int R, int c_lo, int c_hi, const double2* tw, double2* Y,
+                     cudaStream_t st) {
+    if (rows <= 0) return;
+    const int M = n / R;
+    dim3 grid((unsigned)((M + 255) / 256), (unsigned)rows);
+    if (R == 9)
+        k_dif_rows<9><<<grid, 256, 0, st>>>(X, n, M, c_lo, c_hi, tw, Y);
+    else if (R == 5)
+        k_dif_rows<5><<<grid, 256, 0, st>>>(X, n, M, c_lo, c_hi, tw, Y);
+    else if (R == 3)
+        k_dif_rows<3><<<grid, 256, 0, st>>>(X, n, M, c_lo, c_hi, tw, Y);
+    else
+        throw Error(3, "dif_rows: unsupported radix");
+    count_launch();
+    ck(cudaGetLastError(), "k_dif_rows");
+}
+
 void launch_untangle_dif(const double2* T, int n2, int nr, int B, double2* Tt, int n1, int r0, int R,
-                        const double2* tw, cudaStream_t st, const double* colf) {
+                        const double2* tw, cudaStream_t st, const double* colf, int rin) {
     if (nr <= 0 || B <= 0) return;
     const int M = n1 / R;
     dim3 grid((unsigned)((B + 31) / 32), (unsigned)(M / 8));
-    if (R == 9)
+    if (rin > 1) {
+        if (R != 9 || rin != 9) throw Error(3, "untangle_dif: the permuted row input needs radix 9 on both sides");
+        grid.x = (unsigned)(9 * (((B + 8) / 9 + 31) / 32));
+        k_untangle_dif<9, 9><<<grid, 256, 0, st>>>(T, n2, nr, B, Tt, n1, r0, M, tw, colf);
+    } else if (R == 9)
         k_untangle_dif<9><<<grid, 256, 0, st>>>(T, n2, nr, B, Tt, n1, r0, M, tw, colf);
     else if (R == 5)
         k_untangle_dif<5><<<grid, 256, 0, st>>>(T, n2, nr, B, Tt, n1, r0, M, tw, colf);

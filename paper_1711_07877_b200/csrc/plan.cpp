@@ -301,8 +301,17 @@ bool Plan::enable_hfft(int role, cudaStream_t st) {
         ck(cudaMemsetAsync(hB.p, 0, hB.bytes(), st), "hfft zero");
         hC.alloc((size_t)hcols * n1);
         int nr[1] = {n2}, nc[1] = {n1};
-        ckfft(cufftPlanMany(&hp1, 1, nr, nr, 1, n2, nr, 1, n2, CUFFT_Z2Z, R / 2), "hfft Z2Z rows");
         hrad = pick_radix(n1, opts.radix);
+        // the row transform's own first pass (k_dif_rows) when both sides split by 9
+        hrad0 = hrad == 9 && pick_radix(n2, opts.radix) == 9 ? 9 : 1;
+        if (hrad0 > 1) {
+            int nm0[1] = {n2 / hrad0};
+            ckfft(cufftPlanMany(&hp1, 1, nm0, nm0, 1, nm0[0], nm0, 1, nm0[0], CUFFT_Z2Z, (R / 2) * hrad0),
+                  "hfft Z2Z rows (M)");
+            upload_twiddles(htw0, n2, st);
+        } else {
+            ckfft(cufftPlanMany(&hp1, 1, nr, nr, 1, n2, nr, 1, n2, CUFFT_Z2Z, R / 2), "hfft Z2Z rows");
+        }
         if (hrad > 1) {
             // the untangle does the radix-hrad first pass; cuFFT one length-M pass
             const int M = n1 / hrad;
@@ -557,11 +566,20 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         if (tm) tm->stop();
         if (tm) tm->start(tag_fft);
         ckfft(cufftSetStream(hp1, st), "cufftSetStream");
-        ckfft(cufftExecZ2Z(hp1, reinterpret_cast<cufftDoubleComplex*>(hA.p),
-                           reinterpret_cast<cufftDoubleComplex*>(hD.p), CUFFT_INVERSE),
-              "hfft Z2Z rows");
+        if (hrad0 > 1) {
+            // rows: our radix pass, then contiguous length-M transforms in place
+            launch_dif_rows(hA.p, (rhi - rlo) / 2, n2, hrad0, clo, chi, htw0.p, hD.p, st);
+            ckfft(cufftExecZ2Z(hp1, reinterpret_cast<cufftDoubleComplex*>(hD.p),
+                               reinterpret_cast<cufftDoubleComplex*>(hD.p), CUFFT_INVERSE),
+                  "hfft Z2Z rows (M)");
+        } else {
+            ckfft(cufftExecZ2Z(hp1, reinterpret_cast<cufftDoubleComplex*>(hA.p),
+                               reinterpret_cast<cufftDoubleComplex*>(hD.p), CUFFT_INVERSE),
+                  "hfft Z2Z rows");
+        }
         if (hrad > 1)
-            launch_untangle_dif(hD.p, n2, (rhi - rlo) / 2, hcols, hB.p, ax.n, rlo, hrad, htw.p, st, dy_band.p);
+            launch_untangle_dif(hD.p, n2, (rhi - rlo) / 2, hcols, hB.p, ax.n, rlo, hrad, htw.p, st, dy_band.p,
+                                hrad0);
         else
             launch_untangle_transpose(hD.p, n2, (rhi - rlo) / 2, hcols, hB.p, ax.n, rlo, st);
         ckfft(cufftSetStream(hp2, st), "cufftSetStream");

@@ -266,6 +266,9 @@ class Plan {
     int hrad = 1;                    // radix of the first pass folded into untangle (role 1, columns)
                                      // or pack (role 2, rows); 1: none
     DevBuf<double2> htw;             // its twiddles e^{+2 pi i m / n}
+    int hrad0 = 1;                   // radix of the first pass of the other (first) transform, as
+                                     // its own kernel (k_dif_rows) before a length n / hrad0 cuFFT pass
+    DevBuf<double2> htw0;
     mutable DevBuf<double2> hA, hB, hC, hD;
     int hnm = 0, hnby = 0, hb1 = 0, hB1 = 0, hcols = 0;
     DevBuf<double2> hv_t;             // role 2: mirrored tag-0 points, sorted by tile
@@ -470,7 +473,12 @@ void launch_untangle_transpose(const double2* T, int n2, int nr, int B, double2*
 // the same untangle with the radix-R (3, 5, 9) first pass of the length
 // n1 = R M column transform folded in; tw[m] = e^{+2 pi i m / n1}
 void launch_untangle_dif(const double2* T, int n2, int nr, int B, double2* Tt, int n1, int r0, int R,
-                         const double2* tw, cudaStream_t st, const double* colf = nullptr);
+                         const double2* tw, cudaStream_t st, const double* colf = nullptr, int rin = 1);
+// radix-R first pass of `rows` contiguous length-n transforms (X -> Y, mode j
+// then at (j mod R) n/R + j/R after a batched length n/R pass); columns outside
+// [c_lo, c_hi) of X are zero and not read. tw[m] = e^{+2 pi i m / n}
+void launch_dif_rows(const double2* X, int rows, int n, int R, int c_lo, int c_hi, const double2* tw, double2* Y,
+                     cudaStream_t st);
 // Hermitian band rows from half-plane columns -> pairs packed into full rows
 void launch_pack_rows(const double2* Y, int n1, int m0, int n2, int b1, int B1, double2* Z, cudaStream_t st);
 // the same packing with the radix-R first pass of the length n2 = R M row

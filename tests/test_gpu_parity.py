@@ -420,6 +420,39 @@ def test_radix_first_pass_agrees(ops, name):
     assert rel_l2(q, ops[name].apply(f)) <= 1e-13
 
 
+def test_radix_nine_both_transforms(reflib, tmp_path):
+    # grids of 9 * 8k cells on both axes (config 4: 18432 = 9 x 2048): the
+    # Hermitian pipelines then run the radix-9 first pass of both transforms of
+    # each 2-D FFT in our own kernels (k_dif_rows ahead of contiguous length-M
+    # cuFFT passes, the band read in (j mod 9) M + j / 9 order). Found here on a
+    # small cloud by scanning sizes; forced on, against the plain transforms
+    # and against the reference's own apply of the same operator file.
+    from tests.clouds import disk_cloud
+
+    found = None
+    for n in range(2400, 6400, 200):
+        z = disk_cloud(n, np.random.default_rng(n))
+        op = sbd.CompressedOperator.assemble(
+            sbd.kernel_laplace(), z,
+            opts=sbd.AssembleOptions(eps=1e-5, pipeline=sbd.OpOptions(radix_first_pass=1)))
+        i = op.info()
+        if i["fast_in"] and i["fast_out"] and all(i[k] % 72 == 0 for k in ("n1_in", "n2_in", "n1_out", "n2_out")):
+            found = (z, op)
+            break
+    assert found, "no test cloud with 9 * 8k grids"
+    z, rad = found
+    path = str(tmp_path / "nine.sbdop")
+    rad.save(path)
+    plain = sbd.CompressedOperator.load(path, options=sbd.OpOptions(radix_first_pass=0))
+    rng = np.random.default_rng(12)
+    f = rng.standard_normal(len(z)) + 0j
+    q = rad.apply(f)
+    assert rel_l2(q, plain.apply(f)) <= 1e-13
+    assert rel_l2(q, reflib.load(path).apply(f, len(f))) <= PARITY
+    fc = f + 1j * rng.standard_normal(len(z))
+    assert rel_l2(rad.apply(fc), plain.apply(fc)) <= 1e-13
+
+
 def test_concurrent_host_applies_same_operator(ops):
     # reference contract: apply is const and may be called concurrently
     # (conv_operator.hpp:33-36). Two host threads on one operator must each
