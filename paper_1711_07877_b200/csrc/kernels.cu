@@ -2226,17 +2226,36 @@ __global__ void __launch_bounds__(256, 5) k_untangle_dif(const double2* __restri
 // transform folded in: packed row k (band rows 2k, 2k+1 as z = a + i b, the
 // columns above n2/2 their conjugate mirror) leaves as y_s[k1] at
 // k n2 + s M + k1 for a batched length-M row transform.
-template <int R>
+// RIN > 1: the columns of Y (length n1) come from a radix-RIN first pass +
+// length n1 / RIN transforms (k_dif_rows), mode j at (j mod RIN) M1 + j / RIN;
+// a CTA then takes the 32 packed rows RIN (l0 + lane) + cls, whose band rows
+// sit two cells apart there.
+template <int R, int RIN = 1>
 __global__ void __launch_bounds__(256, 5) k_pack_dif(const double2* __restrict__ Y, int n1, int m0, int n2,
                                                   int b1, int B1, double2* __restrict__ Z, int M,
                                                   const double2* __restrict__ tw) {
     __shared__ double2 so[R][8][33];  // [s][k1][packed row]
-    const int kb = blockIdx.x * 32, k10 = blockIdx.y * 8;
+    const int k10 = blockIdx.y * 8;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int k = kb + lane, k1 = k10 + w;
     const int mhi = n2 / 2, K = (B1 + 1) / 2;
+    int kb, kstep;
+    if (RIN > 1) {
+        const int per = ((K + RIN - 1) / RIN + 31) / 32;  // CTAs per residue class
+        const int cls = blockIdx.x / per;
+        kb = RIN * ((blockIdx.x - cls * per) * 32) + cls;
+        kstep = RIN;
+    } else {
+        kb = blockIdx.x * 32;
+        kstep = 1;
+    }
+    const int k = kb + kstep * lane, k1 = k10 + w;
     const int ra = 2 * k, rb = 2 * k + 1;
-    const int ia = ra <= b1 ? ra : n1 - B1 + ra, ib = rb <= b1 ? rb : n1 - B1 + rb;
+    int ia = ra <= b1 ? ra : n1 - B1 + ra, ib = rb <= b1 ? rb : n1 - B1 + rb;
+    if (RIN > 1 && k < K) {
+        const int M1 = n1 / RIN;
+        ia = (ia % RIN) * M1 + ia / RIN;
+        if (rb < B1) ib = (ib % RIN) * M1 + ib / RIN;
+    }
     double2 z[R], y[R];
 #pragma unroll
     for (int rho = 0; rho < R; ++rho) {
@@ -2259,7 +2278,8 @@ __global__ void __launch_bounds__(256, 5) k_pack_dif(const double2* __restrict__
     const int kl = threadIdx.x & 7;
     for (int p = threadIdx.x >> 3; p < 32 * R; p += 32) {
         const int sI = p >> 5, rl = p & 31;
-        if (kb + rl < K) Z[(size_t)(kb + rl) * n2 + (size_t)sI * M + k10 + kl] = so[sI][kl][rl];
+        const int ko = kb + kstep * rl;
+        if (ko < K) Z[(size_t)ko * n2 + (size_t)sI * M + k10 + kl] = so[sI][kl][rl];
     }
 }
 
@@ -3033,11 +3053,15 @@ void launch_untangle_dif(const double2* T, int n2, int nr, int B, double2* Tt, i
 }
 
 void launch_pack_dif(const double2* Y, int n1, int m0, int n2, int b1, int B1, double2* Z, int R,
-                     const double2* tw, cudaStream_t st) {
+                     const double2* tw, cudaStream_t st, int rin) {
     const int K = (B1 + 1) / 2, M = n2 / R;
     if (K <= 0) return;
     dim3 grid((unsigned)((K + 31) / 32), (unsigned)(M / 8));
-    if (R == 9)
+    if (rin > 1) {
+        if (R != 9 || rin != 9) throw Error(3, "pack_dif: the permuted column input needs radix 9 on both sides");
+        grid.x = (unsigned)(9 * (((K + 8) / 9 + 31) / 32));
+        k_pack_dif<9, 9><<<grid, 256, 0, st>>>(Y, n1, m0, n2, b1, B1, Z, M, tw);
+    } else if (R == 9)
         k_pack_dif<9><<<grid, 256, 0, st>>>(Y, n1, m0, n2, b1, B1, Z, M, tw);
     else if (R == 5)
         k_pack_dif<5><<<grid, 256, 0, st>>>(Y, n1, m0, n2, b1, B1, Z, M, tw);

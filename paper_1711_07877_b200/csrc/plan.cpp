@@ -374,8 +374,17 @@ bool Plan::enable_hfft(int role, cudaStream_t st) {
         for (int r = 0; r < hB1; ++r) hb[r] = hx[r <= hb1 ? r : n1 + r - hB1];
         hdx_band.upload(hb.data(), hB1, st);
         int nc[1] = {n1}, nr[1] = {n2};
-        ckfft(cufftPlanMany(&hp1, 1, nc, nc, 1, n1, nc, 1, n1, CUFFT_Z2Z, hnm), "hfft Z2Z cols");
         hrad = pick_radix(n2, opts.radix);
+        // the column transform's own first pass (k_dif_rows) when both sides split by 9
+        hrad0 = hrad == 9 && pick_radix(n1, opts.radix) == 9 ? 9 : 1;
+        if (hrad0 > 1) {
+            int nm0[1] = {n1 / hrad0};
+            ckfft(cufftPlanMany(&hp1, 1, nm0, nm0, 1, nm0[0], nm0, 1, nm0[0], CUFFT_Z2Z, hnm * hrad0),
+                  "hfft Z2Z cols (M)");
+            upload_twiddles(htw0, n1, st);
+        } else {
+            ckfft(cufftPlanMany(&hp1, 1, nc, nc, 1, n1, nc, 1, n1, CUFFT_Z2Z, hnm), "hfft Z2Z cols");
+        }
         if (hrad > 1) {
             // the packing does the radix-hrad first pass; cuFFT one length-M pass
             const int M = n2 / hrad;
@@ -624,13 +633,22 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         if (tm) tm->stop();
         if (tm) tm->start(tag_fft);
         ckfft(cufftSetStream(hp1, st), "cufftSetStream");
-        ckfft(cufftExecZ2Z(hp1, reinterpret_cast<cufftDoubleComplex*>(hA.p),
-                           reinterpret_cast<cufftDoubleComplex*>(hB.p), CUFFT_INVERSE),
-              "hfft Z2Z cols");
+        if (hrad0 > 1) {
+            // columns: our radix pass over the populated rows, then contiguous
+            // length-M transforms in place
+            launch_dif_rows(hA.p, hnm, ax.n, hrad0, rlo, rhi, htw0.p, hB.p, st);
+            ckfft(cufftExecZ2Z(hp1, reinterpret_cast<cufftDoubleComplex*>(hB.p),
+                               reinterpret_cast<cufftDoubleComplex*>(hB.p), CUFFT_INVERSE),
+                  "hfft Z2Z cols (M)");
+        } else {
+            ckfft(cufftExecZ2Z(hp1, reinterpret_cast<cufftDoubleComplex*>(hA.p),
+                               reinterpret_cast<cufftDoubleComplex*>(hB.p), CUFFT_INVERSE),
+                  "hfft Z2Z cols");
+        }
         // two Hermitian band rows per complex row: their transforms are the
         // real and imaginary parts of one e^{+} transform
         if (hrad > 1)
-            launch_pack_dif(hB.p, ax.n, clo, n2, hb1, hB1, hC.p, hrad, htw.p, st);
+            launch_pack_dif(hB.p, ax.n, clo, n2, hb1, hB1, hC.p, hrad, htw.p, st, hrad0);
         else
             launch_pack_rows(hB.p, ax.n, clo, n2, hb1, hB1, hC.p, st);
         ckfft(cufftSetStream(hp2, st), "cufftSetStream");

@@ -484,7 +484,7 @@ void launch_pack_rows(const double2* Y, int n1, int m0, int n2, int b1, int B1, 
 // the same packing with the radix-R first pass of the length n2 = R M row
 // transform folded in (rows in (j mod R) M + j / R order); tw[m] = e^{+2 pi i m / n2}
 void launch_pack_dif(const double2* Y, int n1, int m0, int n2, int b1, int B1, double2* Z, int R,
-                     const double2* tw, cudaStream_t st);
+                     const double2* tw, cudaStream_t st, int rin = 1);
 
 
 // interpolation from a real band grid whose rows are packed in pairs (row r =
