@@ -618,6 +618,49 @@ def run_b200(args, w):
                    "note": "apply_adjoint of a complex u on device buffers"}
         del u_dev, p_dev
 
+    # procedural ring nodes (sbd_op_options.procedural_rings):
+    # the same workload with the xi-side kernels regenerating every node and the
+    # per-node arrays released -- apply time, HBM held, agreement with the
+    # stored-array operator's q
+    procedural = None
+    if world == 1 and R == 1 and args.procedural:
+        # (the operator goes through its file: a second GPU assembly beside the
+        # resident operator would not fit its temporaries)
+        ppath = f"/tmp/sbd_bench_proc_{os.getpid()}.sbdop"
+        torch.cuda.empty_cache()  # the direct-sum check above leaves large cached blocks
+        try:
+            stored_bytes = int(info["device_bytes"])  # after assembly, before the adjoint's arrays were built
+            op.save(ppath)
+            pop = sbd.CompressedOperator.load(ppath, device=local, max_grid_bytes=96 << 30,
+                                              options=sbd.OpOptions(procedural_rings=True))
+            pinfo = pop.info()
+            qp_dev = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+            for _ in range(3):
+                pop.apply_device(f_dev.data_ptr(), qp_dev.data_ptr(), 1, sh, f_is_real=f_real)
+            torch.cuda.synchronize()
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            p0.record(stream)
+            for _ in range(5):
+                pop.apply_device(f_dev.data_ptr(), qp_dev.data_ptr(), 1, sh, f_is_real=f_real)
+            p1.record(stream)
+            torch.cuda.synchronize()
+            qp = qp_dev.view(-1, 2).cpu().numpy()
+            qp = qp[:, 0] + 1j * qp[:, 1]
+            procedural = {"on": bool(pinfo["procedural_rings"]),
+                          "ms_per_apply": round(p0.elapsed_time(p1) / 5, 3),
+                          "device_bytes": int(pinfo["device_bytes"]), "stored_device_bytes": stored_bytes,
+                          "rel_l2_vs_stored": float(np.linalg.norm(qp - qv) / np.linalg.norm(qv)),
+                          "note": "xi coordinates, phases and omega-hat regenerated in the kernels from (rho_p, "
+                                  "M_p, weight_p, j); per-node arrays released; device_bytes of both operators "
+                                  "before any adjoint"}
+            del pop, qp_dev
+        except Exception as exc:  # never fatal for the headline line
+            procedural = {"error": str(exc)[:200]}
+        finally:
+            if os.path.exists(ppath):
+                os.unlink(ppath)
+        torch.cuda.empty_cache()
+
     cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         if args.ref_full:
@@ -657,6 +700,7 @@ def run_b200(args, w):
             "clocks": clk,
             "batched_rhs": batched,
             "adjoint": adjoint,
+            "procedural_rings": procedural,
             "rhs_parallel": rhs_par,
             "other_scheme": alt,
             "contract": contract,
@@ -681,6 +725,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nrhs", type=int, default=8, help="also time one batched apply of this many RHS (1: off)")
     ap.add_argument("--adjoint", type=int, default=1, help="1: also time apply_adjoint")
+    ap.add_argument("--procedural", type=int, default=1,
+                    help="1: also time the apply with procedural ring nodes (a second assemble)")
     ap.add_argument("--scheme", default="slab", choices=["slab", "shard"],
                     help="multi-GPU apply for N > 1: slab decomposition or the north_star source/target sharding")
     ap.add_argument("--ref-full", type=int, default=1,

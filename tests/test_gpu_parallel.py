@@ -40,3 +40,29 @@ def test_sharded_halves_reproduce_apply(name, world):
         qh = q.cpu().numpy().view(np.complex128)
         assert rel_l2(qh, op.apply(g["f"])) <= 1e-13
         assert rel_l2(qh, g["q"]) <= 1e-9
+
+
+@pytest.mark.parametrize("name", ["lap_disk_n1000", "helm_disk_n800"])
+def test_sharded_halves_on_procedural_operator(name):
+    # the sharded halves run the same xi-side kernels: with procedural ring
+    # nodes they regenerate the nodes of their output / point ranges from the ids
+    path, g = golden(name)
+    op = sbd.CompressedOperator.load(path, options=sbd.OpOptions(procedural_rings=True))
+    assert op.info()["procedural_rings"] == 1
+    f = torch.from_numpy(np.ascontiguousarray(g["f"], dtype=np.complex128).view(np.float64)).cuda()
+    be = DeviceBackend(op)
+    world = 3
+    ranks = [ShardedApply(be, r, world, allreduce=lambda t: None) for r in range(world)]
+    n = be.spectrum_length(f)
+    total = be.new_spectrum()
+    for r, sa in enumerate(ranks):
+        spec = be.new_spectrum()
+        be.forward_spectrum(f, sa.src[r], sa.src[r + 1], spec)
+        total[: 2 * n] += spec[: 2 * n]
+    q = torch.zeros(2 * be.n_tgt, dtype=torch.float64, device="cuda")
+    for r, sa in enumerate(ranks):
+        be.backward_targets(total, f, sa.tgt[r], sa.tgt[r + 1], q)
+    torch.cuda.synchronize()
+    qh = q.cpu().numpy().view(np.complex128)
+    assert rel_l2(qh, op.apply(g["f"])) <= 1e-13
+    assert rel_l2(qh, g["q"]) <= 1e-9

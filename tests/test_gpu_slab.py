@@ -67,6 +67,18 @@ def test_slab_emulated_matches_apply(name, world):
     assert rel_l2(emulated_apply(op, fc, world), op.apply(fc)) <= 1e-11
 
 
+def test_slab_on_procedural_operator():
+    # an operator loaded with procedural ring nodes has released its per-node
+    # arrays; creating the slab plan rebuilds them (same device functions), and
+    # the forward apply keeps regenerating the nodes in its kernels
+    path, g = golden("lap_star_n1500")
+    op = sbd.CompressedOperator.load(path, options=sbd.OpOptions(real_input_split=False, procedural_rings=True))
+    assert op.info()["procedural_rings"] == 1
+    q = emulated_apply(op, g["f"], 3)
+    assert rel_l2(q, g["q"]) <= 1e-9
+    assert rel_l2(op.apply(g["f"]), g["q"]) <= 1e-9
+
+
 def test_slab_emulated_at_scale():
     # the config-4 distribution at N = 2e5 (grid > 4096, radix passes in the
     # single-device pipeline; the slab path runs plain transforms)
