@@ -1549,6 +1549,12 @@ __global__ void __launch_bounds__(128, 8) k_interp_real_tile(
 // memory once; its warps then run the 8-output MMA groups of k_interp_mma
 // from shared memory. The grid is read from L2 once per tile instead of once
 // per 8-output group.
+__device__ __forceinline__ void cp_async16(double2* smem_dst, const double2* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem_dst)),
+                 "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 constexpr int kIT = 32;  // tile edge (Morton level 5)
 constexpr int kITW = 6;  // warps per CTA sharing one staged block
 
@@ -1607,7 +1613,8 @@ __device__ __forceinline__ void mma_group_t(const double2* __restrict__ S, int r
 // PROC: the outputs are procedural ring nodes -- positions, postphase and
 // kappa (omega-hat times the next plan's prephase, `mult` of the fused path)
 // are regenerated from gen.id instead of read from pos / phase / mult.
-template <int W, bool TRANS, bool PROC = false>
+// ASYNC (TRANS, row factors only): the footprint is staged by cp.async, see below.
+template <int W, bool TRANS, bool PROC = false, bool ASYNC = false>
 __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
     WindowPoly P, GridGeom g, const uint32_t* __restrict__ tstart, uint32_t ntiles, int shift,
     uint64_t out_lo, uint64_t n, const double2* __restrict__ pos, const double2* __restrict__ phase,
@@ -1628,8 +1635,11 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
     double* wxs = sm_it + 2 * TT::cells + warp * 2 * 32 * W;
     double* wys = wxs + 32 * W;
     __shared__ int s_jx[kITW][32], s_jy[kITW][32];
+    __shared__ double s_dx[TT::E];  // row factors of the staged footprint (cp.async staging)
     int* jxs = s_jx[warp];
     int* jys = s_jy[warp];
+    // (the cells of S outside the footprint are never written: zero them once)
+    for (int i = threadIdx.x; i < TT::cells; i += kITW * 32) S[i] = make_double2(0.0, 0.0);
     for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         // tile range in sorted order, clipped to this call's output range
         const uint64_t t0 = tstart[tile], t1 = tstart[tile + 1];
@@ -1640,10 +1650,33 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
         const int X0 = (((int)ceil(s0.x - g.half) + shift) & ~(kIT - 1)) - shift;
         const int Y0 = (((int)ceil(s0.y - g.half) + shift) & ~(kIT - 1)) - shift;
         __syncthreads();  // previous tile's readers are done
+        // Row factors only (the column factors are already in the band: the
+        // Hermitian source side): the footprint is a plain copy, sent straight
+        // to shared memory by 16-byte cp.async (LDGSTS: no staging registers,
+        // every load of a thread in flight at once); the row factors go into
+        // the x taps instead. Cells read by conjugate symmetry take the
+        // register path.
+        constexpr bool async_copy = ASYNC;
+        if constexpr (ASYNC) {
+            if (threadIdx.x < TT::E) s_dx[threadIdx.x] = __ldg(dxt + wrap_near(X0 + (int)threadIdx.x, g.n1));
+            for (int i = threadIdx.x; i < TT::cells; i += kITW * 32) {
+                const int c = i / TT::P, r = i - c * TT::P;
+                if (r < TT::E && c < TT::E) {
+                    const int gr = wrap_near(X0 + r, g.n1), gc = wrap_near(Y0 + c, g.n2);
+                    if (hcols && gc >= hcols) {
+                        const double2 m = __ldg(grid + (size_t)(g.n2 - gc) * g.n1 + rad_pos(g, gr ? g.n1 - gr : 0));
+                        S[i] = make_double2(m.x, -m.y);
+                    } else {
+                        cp_async16(S + i, grid + (size_t)gc * g.n1 + rad_pos(g, gr));
+                    }
+                }
+            }
+            cp_async_wait_all();
+        }
         // footprint -> shared memory times the deconvolution factors of its
         // row and column (L1-resident tables), eight loads in flight per thread
         constexpr int kB = 8;
-        for (int ib = 0; ib < TT::cells; ib += kB * kITW * 32) {
+        for (int ib = 0; !ASYNC && ib < TT::cells; ib += kB * kITW * 32) {
             double2 v[kB];
             double f[kB];
 #pragma unroll
@@ -1701,10 +1734,15 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
                     const int ix = (int)ceil(sv.x - g.half), iy = (int)ceil(sv.y - g.half);
                     double* wxp = wxs + lane * W;
                     double* wyp = wys + lane * W;
-                    kb_taps_each<W>((ix - sv.x) + g.half, P, [&](int i, double w) { wxp[i] = w; });
-                    kb_taps_each<W>((iy - sv.y) + g.half, P, [&](int j, double w) { wyp[j] = w; });
                     jx0 = ix - X0;  // tile-local stencil start, in [0, 32)
                     jy0 = iy - Y0;
+                    if constexpr (async_copy) {
+                        const double* fx = s_dx + jx0;
+                        kb_taps_each<W>((ix - sv.x) + g.half, P, [&](int i, double w) { wxp[i] = w * fx[i]; });
+                    } else {
+                        kb_taps_each<W>((ix - sv.x) + g.half, P, [&](int i, double w) { wxp[i] = w; });
+                    }
+                    kb_taps_each<W>((iy - sv.y) + g.half, P, [&](int j, double w) { wyp[j] = w; });
                 }
                 jxs[lane] = jx0;
                 jys[lane] = jy0;
@@ -2502,8 +2540,15 @@ struct InterpRun {
             };
             static size_t attr_t = 0, attr_n = 0, attr_p = 0;  // per W (this template)
             if (ng.id && !trans) throw Error(3, "procedural nodes need the transposed staged interpolation");
-            if (ng.id)
+            // row factors only (the Hermitian source side): cp.async staging
+            const bool as = trans && dx && !dy;
+            static size_t attr_pa = 0, attr_ta = 0;
+            if (ng.id && as)
+                go(k_interp_tile<W, true, true, true>, ITile<W, true>::smem, attr_pa);
+            else if (ng.id)
                 go(k_interp_tile<W, true, true>, ITile<W, true>::smem, attr_p);
+            else if (as)
+                go(k_interp_tile<W, true, false, true>, ITile<W, true>::smem, attr_ta);
             else if (trans)
                 go(k_interp_tile<W, true>, ITile<W, true>::smem, attr_t);
             else
