@@ -1613,7 +1613,7 @@ __device__ __forceinline__ void mma_group_t(const double2* __restrict__ S, int r
 // PROC: the outputs are procedural ring nodes -- positions, postphase and
 // kappa (omega-hat times the next plan's prephase, `mult` of the fused path)
 // are regenerated from gen.id instead of read from pos / phase / mult.
-// ASYNC (TRANS, row factors only): the footprint is staged by cp.async, see below.
+// ASYNC (TRANS): the footprint is staged by cp.async, see below.
 template <int W, bool TRANS, bool PROC = false, bool ASYNC = false>
 __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
     WindowPoly P, GridGeom g, const uint32_t* __restrict__ tstart, uint32_t ntiles, int shift,
@@ -1635,7 +1635,7 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
     double* wxs = sm_it + 2 * TT::cells + warp * 2 * 32 * W;
     double* wys = wxs + 32 * W;
     __shared__ int s_jx[kITW][32], s_jy[kITW][32];
-    __shared__ double s_dx[TT::E];  // row factors of the staged footprint (cp.async staging)
+    __shared__ double s_dx[TT::E], s_dy[TT::E];  // row / column factors of the staged footprint (cp.async staging)
     int* jxs = s_jx[warp];
     int* jys = s_jy[warp];
     // (the cells of S outside the footprint are never written: zero them once)
@@ -1650,15 +1650,17 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
         const int X0 = (((int)ceil(s0.x - g.half) + shift) & ~(kIT - 1)) - shift;
         const int Y0 = (((int)ceil(s0.y - g.half) + shift) & ~(kIT - 1)) - shift;
         __syncthreads();  // previous tile's readers are done
-        // Row factors only (the column factors are already in the band: the
-        // Hermitian source side): the footprint is a plain copy, sent straight
-        // to shared memory by 16-byte cp.async (LDGSTS: no staging registers,
-        // every load of a thread in flight at once); the row factors go into
-        // the x taps instead. Cells read by conjugate symmetry take the
-        // register path.
+        // The footprint is a plain copy, sent straight to shared memory by
+        // 16-byte cp.async (LDGSTS: no staging registers, every load of a
+        // thread in flight at once); the deconvolution factors of its rows and
+        // columns go into each output's x and y taps instead. Cells read by
+        // conjugate symmetry take the register path.
         constexpr bool async_copy = ASYNC;
         if constexpr (ASYNC) {
-            if (threadIdx.x < TT::E) s_dx[threadIdx.x] = __ldg(dxt + wrap_near(X0 + (int)threadIdx.x, g.n1));
+            if (threadIdx.x < TT::E)
+                s_dx[threadIdx.x] = dxt ? __ldg(dxt + wrap_near(X0 + (int)threadIdx.x, g.n1)) : 1.0;
+            else if (threadIdx.x >= 64 && threadIdx.x < 64 + TT::E)
+                s_dy[threadIdx.x - 64] = dyt ? __ldg(dyt + wrap_near(Y0 + (int)threadIdx.x - 64, g.n2)) : 1.0;
             for (int i = threadIdx.x; i < TT::cells; i += kITW * 32) {
                 const int c = i / TT::P, r = i - c * TT::P;
                 if (r < TT::E && c < TT::E) {
@@ -1738,11 +1740,13 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
                     jy0 = iy - Y0;
                     if constexpr (async_copy) {
                         const double* fx = s_dx + jx0;
+                        const double* fy = s_dy + jy0;
                         kb_taps_each<W>((ix - sv.x) + g.half, P, [&](int i, double w) { wxp[i] = w * fx[i]; });
+                        kb_taps_each<W>((iy - sv.y) + g.half, P, [&](int j, double w) { wyp[j] = w * fy[j]; });
                     } else {
                         kb_taps_each<W>((ix - sv.x) + g.half, P, [&](int i, double w) { wxp[i] = w; });
+                        kb_taps_each<W>((iy - sv.y) + g.half, P, [&](int j, double w) { wyp[j] = w; });
                     }
-                    kb_taps_each<W>((iy - sv.y) + g.half, P, [&](int j, double w) { wyp[j] = w; });
                 }
                 jxs[lane] = jx0;
                 jys[lane] = jy0;
@@ -2540,17 +2544,11 @@ struct InterpRun {
             };
             static size_t attr_t = 0, attr_n = 0, attr_p = 0;  // per W (this template)
             if (ng.id && !trans) throw Error(3, "procedural nodes need the transposed staged interpolation");
-            // row factors only (the Hermitian source side): cp.async staging
-            const bool as = trans && dx && !dy;
-            static size_t attr_pa = 0, attr_ta = 0;
-            if (ng.id && as)
-                go(k_interp_tile<W, true, true, true>, ITile<W, true>::smem, attr_pa);
-            else if (ng.id)
-                go(k_interp_tile<W, true, true>, ITile<W, true>::smem, attr_p);
-            else if (as)
-                go(k_interp_tile<W, true, false, true>, ITile<W, true>::smem, attr_ta);
+            // the transposed (band) layout is staged by cp.async
+            if (ng.id)
+                go(k_interp_tile<W, true, true, true>, ITile<W, true>::smem, attr_p);
             else if (trans)
-                go(k_interp_tile<W, true>, ITile<W, true>::smem, attr_t);
+                go(k_interp_tile<W, true, false, true>, ITile<W, true>::smem, attr_t);
             else
                 go(k_interp_tile<W, false>, ITile<W, false>::smem, attr_n);
             return;
