@@ -1613,7 +1613,7 @@ __device__ __forceinline__ void mma_group_t(const double2* __restrict__ S, int r
 // PROC: the outputs are procedural ring nodes -- positions, postphase and
 // kappa (omega-hat times the next plan's prephase, `mult` of the fused path)
 // are regenerated from gen.id instead of read from pos / phase / mult.
-// ASYNC (TRANS): the footprint is staged by cp.async, see below.
+// ASYNC: the footprint is staged by cp.async, see below.
 template <int W, bool TRANS, bool PROC = false, bool ASYNC = false>
 __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
     WindowPoly P, GridGeom g, const uint32_t* __restrict__ tstart, uint32_t ntiles, int shift,
@@ -1662,14 +1662,16 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
             else if (threadIdx.x >= 64 && threadIdx.x < 64 + TT::E)
                 s_dy[threadIdx.x - 64] = dyt ? __ldg(dyt + wrap_near(Y0 + (int)threadIdx.x - 64, g.n2)) : 1.0;
             for (int i = threadIdx.x; i < TT::cells; i += kITW * 32) {
-                const int c = i / TT::P, r = i - c * TT::P;
+                const int q = i / TT::P, rr = i - q * TT::P;
+                const int r = TRANS ? rr : q, c = TRANS ? q : rr;
                 if (r < TT::E && c < TT::E) {
                     const int gr = wrap_near(X0 + r, g.n1), gc = wrap_near(Y0 + c, g.n2);
-                    if (hcols && gc >= hcols) {
+                    if (TRANS && hcols && gc >= hcols) {
                         const double2 m = __ldg(grid + (size_t)(g.n2 - gc) * g.n1 + rad_pos(g, gr ? g.n1 - gr : 0));
                         S[i] = make_double2(m.x, -m.y);
                     } else {
-                        cp_async16(S + i, grid + (size_t)gc * g.n1 + rad_pos(g, gr));
+                        cp_async16(S + i, TRANS ? grid + (size_t)gc * g.n1 + rad_pos(g, gr)
+                                                : grid + (size_t)gr * g.n2 + gc);
                     }
                 }
             }
@@ -2544,13 +2546,13 @@ struct InterpRun {
             };
             static size_t attr_t = 0, attr_n = 0, attr_p = 0;  // per W (this template)
             if (ng.id && !trans) throw Error(3, "procedural nodes need the transposed staged interpolation");
-            // the transposed (band) layout is staged by cp.async
+            // every staged layout is copied by cp.async
             if (ng.id)
                 go(k_interp_tile<W, true, true, true>, ITile<W, true>::smem, attr_p);
             else if (trans)
                 go(k_interp_tile<W, true, false, true>, ITile<W, true>::smem, attr_t);
             else
-                go(k_interp_tile<W, false>, ITile<W, false>::smem, attr_n);
+                go(k_interp_tile<W, false, false, true>, ITile<W, false>::smem, attr_n);
             return;
         }
         if (ng.id) throw Error(3, "procedural nodes need the staged interpolation");
