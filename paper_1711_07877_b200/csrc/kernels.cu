@@ -1675,8 +1675,21 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
                     }
                 }
             }
-            cp_async_wait_all();
         }
+        // this lane's position (or node id) of the warp's first 32 outputs: in
+        // flight while the footprint lands; later rounds are fetched a round ahead
+        double2 svn = make_double2(0.0, 0.0);
+        uint32_t nidn = 0;
+        {
+            const uint64_t v0 = a0 + 32 * warp + lane;
+            if (v0 < a1) {
+                if constexpr (PROC)
+                    nidn = gen.id[v0 - out_lo];
+                else
+                    svn = pos[v0 - out_lo];
+            }
+        }
+        if constexpr (ASYNC) cp_async_wait_all();
         // footprint -> shared memory times the deconvolution factors of its
         // row and column (L1-resident tables), eight loads in flight per thread
         constexpr int kB = 8;
@@ -1715,17 +1728,24 @@ __global__ void __launch_bounds__(kITW * 32, 3) k_interp_tile(
             const uint64_t vmy = base + lane;
             const bool mine = vmy < a1;
             const uint64_t vr = mine ? vmy - out_lo : 0;
-            double2 sv = make_double2(0.0, 0.0), ph = sv, mu = make_double2(1.0, 0.0), ad = sv;
+            double2 sv = svn, ph = make_double2(0.0, 0.0), mu = make_double2(1.0, 0.0), ad = ph;
             uint32_t dst = 0;
-            uint32_t nid = 0;
-            double2 xi = sv;
+            const uint32_t nid = nidn;
+            double2 xi = ph;
+            {
+                const uint64_t vnx = vmy + 32 * kITW;
+                if (vnx < a1) {
+                    if constexpr (PROC)
+                        nidn = gen.id[vnx - out_lo];
+                    else
+                        svn = pos[vnx - out_lo];
+                }
+            }
             if (mine) {
                 if constexpr (PROC) {
-                    nid = gen.id[vr];
                     xi = ring_node(nid, gen.rings, &mu);
                     sv = plan_output_pos(xi, gen.ox, gen.oy, gen.osgn);
                 } else {
-                    sv = pos[vr];
                     ph = phase[vr];
                     if (mult) mu = mult[vr];
                 }
