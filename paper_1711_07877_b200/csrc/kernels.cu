@@ -1915,13 +1915,14 @@ __global__ void k_ndft(const double2* __restrict__ pts, uint64_t np,
 __global__ void k_gather_mul(const double2* __restrict__ in, const uint32_t* __restrict__ perm,
                              const double2* __restrict__ phase, double2* __restrict__ b,
                              double2* __restrict__ raw, uint64_t n, uint64_t lo, uint64_t hi,
-                             int* __restrict__ clear) {
+                             int* __restrict__ clear, double* __restrict__ raw_re) {
     const uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (k >= n) return;
     const double2 c = in[perm ? perm[k] : k];
     if (clear && c.y != 0.0) *clear = 0;
     b[k] = (k >= lo && k < hi) ? cmul(c, phase[k]) : make_double2(0.0, 0.0);
     if (raw) raw[k] = c;
+    if (raw_re) raw_re[k] = c.x;
 }
 
 // qs[r] = sum_{i in row r} D'_i f'_{col'_i} (point_cloud.cpp:116-123 on the
@@ -1930,6 +1931,25 @@ __global__ void k_gather_mul(const double2* __restrict__ in, const uint32_t* __r
 // omega-hat): the values are stored as 8-byte reals, 12 instead of 20 bytes
 // per nonzero streamed from HBM; the result is bitwise the complex kernel's
 // (the imaginary parts it would multiply are exact zeros).
+// Real D' times a real f (the caller said so): the gathers read 8-byte
+// entries of Re(f) (four per 32-byte sector instead of two), q is exactly real.
+__global__ void __launch_bounds__(256) k_spmv_vec_rr(uint64_t rows, const uint64_t* __restrict__ ro,
+                                                     const uint32_t* __restrict__ cols,
+                                                     const double* __restrict__ vals,
+                                                     const double* __restrict__ fr, double2* __restrict__ qs) {
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t r = g >> 3;
+    const int sub = (int)(g & 7);
+    double ar = 0.0;
+    if (r < rows) {
+        const uint64_t e = ro[r + 1];
+        for (uint64_t i = ro[r] + sub; i < e; i += 8) ar = fma(vals[i], fr[cols[i]], ar);
+    }
+#pragma unroll
+    for (int o = 4; o; o >>= 1) ar += __shfl_xor_sync(0xffffffffu, ar, o);
+    if (r < rows && sub == 0) qs[r] = make_double2(ar, 0.0);
+}
+
 __global__ void __launch_bounds__(256) k_spmv_vec_real(uint64_t rows, const uint64_t* __restrict__ ro,
                                                        const uint32_t* __restrict__ cols,
                                                        const double* __restrict__ vals,
@@ -2909,9 +2929,9 @@ void launch_ndft(const double2* pts, uint64_t np, const double2* frq, uint64_t n
 
 void launch_gather_mul(const double2* in, const uint32_t* perm, const double2* phase, double2* b,
                        double2* raw, uint64_t n, cudaStream_t st, uint64_t lo, uint64_t hi,
-                       int* clear) {
+                       int* clear, double* raw_re) {
     if (!n) return;
-    k_gather_mul<<<blocks(n, 256), 256, 0, st>>>(in, perm, phase, b, raw, n, lo, hi, clear);
+    k_gather_mul<<<blocks(n, 256), 256, 0, st>>>(in, perm, phase, b, raw, n, lo, hi, clear, raw_re);
     count_launch();
     ck(cudaGetLastError(), "k_gather_mul");
 }
@@ -3006,9 +3026,12 @@ void launch_spmm(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const 
 }
 
 void launch_spmv_vec_real(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double* vals,
-                          const double2* f, double2* qs, cudaStream_t st) {
+                          const double2* f, double2* qs, cudaStream_t st, const double* f_re) {
     if (!rows) return;
-    k_spmv_vec_real<<<blocks(rows * 8, 256), 256, 0, st>>>(rows, ro, cols, vals, f, qs);
+    if (f_re)
+        k_spmv_vec_rr<<<blocks(rows * 8, 256), 256, 0, st>>>(rows, ro, cols, vals, f_re, qs);
+    else
+        k_spmv_vec_real<<<blocks(rows * 8, 256), 256, 0, st>>>(rows, ro, cols, vals, f, qs);
     count_launch();
     ck(cudaGetLastError(), "k_spmv_vec_real");
 }

@@ -69,9 +69,12 @@ struct sbd_op {
     DevBuf<double> vals_sr;
 
     // rows [lo, hi) of the renumbered D' times f_sorted into qs
+    // (real_f: the caller vouches for a real f, and f_sorted_re holds Re(f_sorted))
+    DevBuf<double> f_sorted_re;
     void spmv_sorted(uint64_t lo, uint64_t hi, cudaStream_t st, bool real_f = false) {
         if (vals_sr.n && (real_f || !vals_s.n))
-            launch_spmv_vec_real(hi - lo, ro_s.p + lo, cols_s.p, vals_sr.p, f_sorted.p, qs.p + lo, st);
+            launch_spmv_vec_real(hi - lo, ro_s.p + lo, cols_s.p, vals_sr.p, f_sorted.p, qs.p + lo, st,
+                                 real_f && f_sorted_re.n ? f_sorted_re.p : nullptr);
         else
             launch_spmv_vec(hi - lo, ro_s.p + lo, cols_s.p, vals_s.p, f_sorted.p, qs.p + lo, st);
     }
@@ -617,6 +620,10 @@ struct sbd_op {
                 hin.clear = true;
                 hout.n = ~0ull;
                 hout.two_re = true;
+                if (real_f) {
+                    if (!f_sorted_re.n) f_sorted_re.alloc(d.n_src());
+                    hin.raw_re = f_sorted_re.p;
+                }
                 if (hfft_now) {
                     hin.hfft = hout.hfft = true;
                     hin.hcols = fwd_in->hcols;
@@ -697,7 +704,9 @@ struct sbd_op {
         if (!fused) throw Error(SBD_ERR_RUNTIME, "sharded apply needs both NUFFTs on the gridded path");
         hi = std::min<uint64_t>(hi, d.n_tgt());
         lo = std::min(lo, hi);
-        launch_gather_mul(f, fwd_in->perm_t.p, fwd_in->pre.p, work.bbuf.p, f_sorted.p, d.n_src(), st, 0, 0);
+        if (shard_real && !f_sorted_re.n) f_sorted_re.alloc(d.n_src());
+        launch_gather_mul(f, fwd_in->perm_t.p, fwd_in->pre.p, work.bbuf.p, f_sorted.p, d.n_src(), st, 0, 0, nullptr,
+                          shard_real ? f_sorted_re.p : nullptr);
         if (tm.on) tm.start("spmv");
         spmv_sorted(lo, hi, st, shard_real);
         if (tm.on) tm.stop();

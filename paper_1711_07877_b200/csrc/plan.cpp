@@ -554,7 +554,7 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
     if (!in_is_b) {
         if (wk.bbuf.n < np) wk.bbuf.alloc(np);
         launch_gather_mul(in, perm_t.n ? perm_t.p : nullptr, pre.p, wk.bbuf.p, raw_sorted, np, st, in_lo,
-                          in_hi, clear);
+                          in_hi, clear, herm ? herm->raw_re : nullptr);
         b = wk.bbuf.p;
     }
     if (herm && herm->hfft && hrole == 1) {

@@ -373,6 +373,7 @@ struct HermArgs {
     double2* out2 = nullptr;
     const uint32_t* perm2 = nullptr;
     bool hfft = false;  // take the Hermitian-FFT pipelines in apply_pruned
+    double* raw_re = nullptr;  // the input gather also writes Re(sorted input) here (the real CSR pass reads it)
 };
 
 // Output of the tile-owned spread: mode 0 = complex grid[(row-r0)*pitch +
@@ -498,11 +499,12 @@ void launch_interp_real(int w, const WindowPoly& win, GridGeom g, uint64_t n, co
 // clear (optional): set to 0 when some in[k] has a nonzero imaginary part.
 void launch_gather_mul(const double2* in, const uint32_t* perm, const double2* phase, double2* b,
                        double2* raw, uint64_t n, cudaStream_t st, uint64_t lo = 0,
-                       uint64_t hi = ~0ull, int* clear = nullptr);
+                       uint64_t hi = ~0ull, int* clear = nullptr, double* raw_re = nullptr);  // raw_re[k] = Re(in[perm[k]])
 void launch_spmv_vec(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double2* vals,
                      const double2* f, double2* qs, cudaStream_t st, bool accumulate = false);
+// f_re (optional): Re(f) as its own array for an f known to be real (q exactly real)
 void launch_spmv_vec_real(uint64_t rows, const uint64_t* ro, const uint32_t* cols, const double* vals,
-                          const double2* f, double2* qs, cudaStream_t st);
+                          const double2* f, double2* qs, cudaStream_t st, const double* f_re = nullptr);
 // D' times up to kSpmmMax right-hand sides in one pass over D': column j of
 // the set is f + idx[j] * ldf -> qs + idx[j] * ldq. vals_r (Re(D')) replaces
 // vals when given.
