@@ -1060,7 +1060,7 @@ __global__ void __launch_bounds__(256) k_interp(WindowPoly P, GridGeom g, uint64
         for (int i = 0; i < W; ++i) {
             int mx = mx0 + i;
             if (mx >= g.n1) mx -= g.n1;
-            mxi[i] = mx;
+            mxi[i] = rad_pos(g, mx);  // (rows stored in a radix first pass's order)
             if (dxt) wx[i] *= dxt[mx];
         }
 #pragma unroll
@@ -1140,7 +1140,8 @@ __device__ __forceinline__ void mma_group(const double2* __restrict__ grid, Grid
 #pragma unroll
         for (int c = 0; c < NCT; ++c) {
             const int col = wrap_near(cmin + 4 * c + kq, g.n2);
-            a[t][c] = __ldg(TRANS ? grid + (size_t)col * g.n1 + rows[t] : grid + (size_t)rows[t] * g.n2 + col);
+            a[t][c] = __ldg(TRANS ? grid + (size_t)col * g.n1 + rad_pos(g, rows[t])
+                                  : grid + (size_t)rows[t] * g.n2 + col);
         }
     }
     double hr[NRT][2], hi[NRT][2];
@@ -1260,7 +1261,7 @@ __global__ void __launch_bounds__(128) k_interp_mma(WindowPoly P, GridGeom g, ui
                             for (int j = 0; j < W; ++j) {
                                 const int my = wrap_near(jy0 + j, g.n2);
                                 const double wyj = wys[node * W + j] * (dyt ? dyt[my] : 1.0);
-                                const double2 gv = __ldg(TRANS ? grid + (size_t)my * g.n1 + mx
+                                const double2 gv = __ldg(TRANS ? grid + (size_t)my * g.n1 + rad_pos(g, mx)
                                                                : grid + (size_t)mx * g.n2 + my);
                                 rr = fma(gv.x, wyj, rr);
                                 ri = fma(gv.y, wyj, ri);
@@ -2071,32 +2072,58 @@ __global__ void __launch_bounds__(256) k_band_untranspose(const double2* __restr
 // (m = c' for c' <= b, n2 - B + c' otherwise): 32 x 32 tiles through shared
 // memory so both the reads (along rows of T) and writes (along rows of Tt)
 // are coalesced.
+// rin > 1: the rows of T come from a radix-rin first pass + length n2 / rin
+// transforms (k_dif_rows): mode j sits at (j mod rin) MR + j / rin, and a CTA
+// takes 32 consecutive positions of one residue class (the modes rin l + cls),
+// keeping those that are band modes.
+__device__ __forceinline__ int band_col_of_pos(int pos, int n2, int b, int B, int rin, int& at) {
+    at = pos;
+    if (pos >= n2) return -1;
+    int j = pos;
+    if (rin > 1) {
+        const int MR = n2 / rin, cls = pos / MR;
+        j = rin * (pos - cls * MR) + cls;
+    }
+    if (j >= n2) return -1;
+    if (j <= b) return j;
+    return j >= n2 - b ? j - (n2 - B) : -1;
+}
+
 __global__ void __launch_bounds__(256) k_band_transpose(const double2* __restrict__ T, int n2,
                                                         int r0, int r1, int b, int B,
                                                         double2* __restrict__ Tt, int n1, int rin0,
-                                                        int conj_out) {
+                                                        int conj_out, int rin) {
     __shared__ double2 tile[32][33];
     const int cb = blockIdx.x * 32, rb = r0 + blockIdx.y * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    // column handled by lane i of this CTA: band column c_of(i) read at position at_of(i)
+    auto col_of = [&](int i, int& at) -> int {
+        if (rin > 1) return band_col_of_pos(cb + i, n2, b, B, rin, at);
+        const int c = cb + i;
+        at = c <= b ? c : n2 - B + c;
+        return c < B ? c : -1;
+    };
 #pragma unroll
     for (int q = 0; q < 32; q += 8) {
-        const int r = rb + ty + q, c = cb + tx;
-        if (r < r1 && c < B) {
-            const int m = c <= b ? c : n2 - B + c;
-            tile[ty + q][tx] = T[(size_t)(r - rin0) * n2 + m];
-        }
+        const int r = rb + ty + q;
+        int at;
+        const int c = col_of(tx, at);
+        if (r < r1 && c >= 0) tile[ty + q][tx] = T[(size_t)(r - rin0) * n2 + at];
     }
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < 32; q += 8) {
-        const int c = cb + ty + q, r = rb + tx;
-        if (r < r1 && c < B) {
+        const int r = rb + tx;
+        int at;
+        const int c = col_of(ty + q, at);
+        if (r < r1 && c >= 0) {
             double2 v = tile[tx][ty + q];
             if (conj_out) v.y = -v.y;
             Tt[(size_t)c * n1 + r] = v;
         }
     }
 }
+
 
 // Mirrored grid coordinates t' = n - t: the image of a point under the grid
 __global__ void k_mirror_points(const double2* __restrict__ t, uint64_t n, int n1, int n2, int w,
@@ -2211,6 +2238,47 @@ __device__ __forceinline__ void dft_small(const double2 (&x)[R], double2 (&y)[R]
             }
             y[k] = a;
         }
+    }
+}
+
+// The band transpose with the radix-R first pass of the length n1 = R M column
+// transform folded in (the complex pipeline's k_untangle_dif): band column c
+// of the rows [r0, r1) of T (zero elsewhere) leaves as y_s[k] at c n1 + s M + k
+// for a batched length-M column transform. Columns by position as above.
+template <int R>
+__global__ void __launch_bounds__(256, 5) k_band_transpose_dif(const double2* __restrict__ T, int n2, int r0, int r1,
+                                                            int b, int B, double2* __restrict__ Tt, int n1, int M,
+                                                            const double2* __restrict__ tw, int rin) {
+    __shared__ double2 so[R][8][33];
+    __shared__ int s_col[32];
+    const int cb = blockIdx.x * 32, k0 = blockIdx.y * 8;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int at = 0;
+    int c;
+    if (rin > 1) {
+        c = band_col_of_pos(cb + lane, n2, b, B, rin, at);
+    } else {
+        c = cb + lane < B ? cb + lane : -1;
+        at = c <= b ? c : n2 - B + c;
+    }
+    if (w == 0) s_col[lane] = c;
+    if (__syncthreads_and(c < 0)) return;  // no band column among these positions
+    const int k = k0 + w;
+    double2 x[R], y[R];
+#pragma unroll
+    for (int rho = 0; rho < R; ++rho) {
+        const int m1 = k + M * rho;
+        x[rho] = (c >= 0 && m1 >= r0 && m1 < r1) ? T[(size_t)(m1 - r0) * n2 + at] : make_double2(0.0, 0.0);
+    }
+    dft_small<R>(x, y, tw, M);
+#pragma unroll
+    for (int sI = 0; sI < R; ++sI) so[sI][w][lane] = sI ? cmul(y[sI], __ldg(tw + sI * k)) : y[sI];
+    __syncthreads();
+    const int kl = threadIdx.x & 7;
+    for (int p = threadIdx.x >> 3; p < 32 * R; p += 32) {
+        const int sI = p >> 5, cl = p & 31;
+        const int co = s_col[cl];
+        if (co >= 0) Tt[(size_t)co * n1 + (size_t)sI * M + k0 + kl] = so[sI][kl][cl];
     }
 }
 
@@ -3094,12 +3162,30 @@ void launch_wrap_transpose(const double2* in, size_t ipitch, int nin, int j0, in
 }
 
 void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int B, double2* Tt,
-                           int n1, cudaStream_t st, int rin0, int conj_out) {
+                           int n1, cudaStream_t st, int rin0, int conj_out, int rin) {
     if (r1 <= r0) return;
-    dim3 grid((unsigned)((B + 31) / 32), (unsigned)((r1 - r0 + 31) / 32));
-    k_band_transpose<<<grid, 256, 0, st>>>(T, n2, r0, r1, b, B, Tt, n1, rin0, conj_out);
+    // permuted rows: CTAs walk the row positions (about half hold band modes)
+    dim3 grid((unsigned)(((rin > 1 ? n2 : B) + 31) / 32), (unsigned)((r1 - r0 + 31) / 32));
+    k_band_transpose<<<grid, 256, 0, st>>>(T, n2, r0, r1, b, B, Tt, n1, rin0, conj_out, rin);
     count_launch();
     ck(cudaGetLastError(), "k_band_transpose");
+}
+
+void launch_band_transpose_dif(const double2* T, int n2, int r0, int r1, int b, int B, double2* Tt, int n1, int R,
+                               const double2* tw, cudaStream_t st, int rin) {
+    if (r1 <= r0) return;
+    const int M = n1 / R;
+    dim3 grid((unsigned)(((rin > 1 ? n2 : B) + 31) / 32), (unsigned)(M / 8));
+    if (R == 9)
+        k_band_transpose_dif<9><<<grid, 256, 0, st>>>(T, n2, r0, r1, b, B, Tt, n1, M, tw, rin);
+    else if (R == 5)
+        k_band_transpose_dif<5><<<grid, 256, 0, st>>>(T, n2, r0, r1, b, B, Tt, n1, M, tw, rin);
+    else if (R == 3)
+        k_band_transpose_dif<3><<<grid, 256, 0, st>>>(T, n2, r0, r1, b, B, Tt, n1, M, tw, rin);
+    else
+        throw Error(3, "band_transpose_dif: unsupported radix");
+    count_launch();
+    ck(cudaGetLastError(), "k_band_transpose_dif");
 }
 
 void launch_dif_rows(const double2* X, int rows, int n, int R, int c_lo, int c_hi, const double2* tw, double2* Y,

@@ -77,6 +77,9 @@ int stencil_start_output(const Axis& a, double f, double sg, int w) {
     return (int)std::ceil(s - 0.5 * w);
 }
 
+static void upload_twiddles(DevBuf<double2>& tw, int n, cudaStream_t st);
+static int pick_radix(int n, int mode);
+
 Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf_, int sign_,
            const NufftOpts& o, int dev, bool sort_points, bool sort_outputs, cudaStream_t st,
            const uint8_t* pt_tag, const uint8_t* out_tag, const double2* dev_pts, const double2* dev_frq)
@@ -245,6 +248,21 @@ Plan::Plan(const double* pts_xy, uint64_t np_, const double* frq_xy, uint64_t nf
               "cufftPlanMany rows");
         ckfft(cufftPlanMany(&fft_colT, 1, n1, n1, 1, ax.n, n1, 1, ax.n, CUFFT_Z2Z, bc),
               "cufftPlanMany cols T");
+        // radix first passes in our own kernels where the lengths split
+        crad_row = pick_radix(ay.n, opts.radix);
+        crad_col = pick_radix(ax.n, opts.radix);
+        if (crad_row > 1) {
+            int m2[1] = {ay.n / crad_row};
+            ckfft(cufftPlanMany(&fft_row_m, 1, m2, m2, 1, m2[0], m2, 1, m2[0], CUFFT_Z2Z, (rhi - rlo) * crad_row),
+                  "cufftPlanMany rows (M)");
+            upload_twiddles(ctw_row, ay.n, st);
+        }
+        if (crad_col > 1) {
+            int m1[1] = {ax.n / crad_col};
+            ckfft(cufftPlanMany(&fft_colT_m, 1, m1, m1, 1, m1[0], m1, 1, m1[0], CUFFT_Z2Z, bc * crad_col),
+                  "cufftPlanMany cols T (M)");
+            upload_twiddles(ctw_col, ax.n, st);
+        }
     }
     ck(cudaStreamSynchronize(st), "plan build");
 }
@@ -258,6 +276,8 @@ Plan::~Plan() {
     if (fft) cufftDestroy(fft);
     if (fft_row) cufftDestroy(fft_row);
     if (fft_colT) cufftDestroy(fft_colT);
+    if (fft_row_m) cufftDestroy(fft_row_m);
+    if (fft_colT_m) cufftDestroy(fft_colT_m);
     if (hp1) cufftDestroy(hp1);
     if (hp2) cufftDestroy(hp2);
 }
@@ -704,34 +724,61 @@ void Plan::apply_pruned(const double2* in, bool in_is_b, double2* raw_sorted, do
         zero_rect_minus(wk.T.p, wk.t_pitch, wk.tr0, wk.tr1, 0, wk.t_pitch, 0, 0, 0, 0, st);
     auto* G = reinterpret_cast<cufftDoubleComplex*>(wk.grid.p);
     auto* T = reinterpret_cast<cufftDoubleComplex*>(wk.T.p);
-    ckfft(cufftSetStream(fft_row, st), "cufftSetStream");
-    ckfft(cufftExecZ2Z(fft_row, G + (size_t)rlo * n2, T + (size_t)rlo * n2, CUFFT_INVERSE), "fft rows");
+    if (crad_row > 1) {
+        // our radix pass over the written columns, then contiguous length-M
+        // transforms in place: mode j of a row at (j mod r) M + j / r
+        launch_dif_rows(wk.grid.p + (size_t)rlo * n2, rhi - rlo, n2, crad_row, clo, chi, ctw_row.p,
+                        wk.T.p + (size_t)rlo * n2, st);
+        ckfft(cufftSetStream(fft_row_m, st), "cufftSetStream");
+        ckfft(cufftExecZ2Z(fft_row_m, T + (size_t)rlo * n2, T + (size_t)rlo * n2, CUFFT_INVERSE), "fft rows (M)");
+    } else {
+        ckfft(cufftSetStream(fft_row, st), "cufftSetStream");
+        ckfft(cufftExecZ2Z(fft_row, G + (size_t)rlo * n2, T + (size_t)rlo * n2, CUFFT_INVERSE), "fft rows");
+    }
     wk.tr0 = rlo;
     wk.tr1 = rhi;
     wk.t_pitch = n2;
     {
-        // Tt[c'][x] (pitch n1) holds band column c' over the populated rows only;
-        // every other row x of Tt stays zero (strips a previous plan left are cleared).
-        if (wk.tt_r1 > wk.tt_r0) {
-            if (wk.tt_pitch == ax.n && wk.tt_rows == bc)
-                zero_rect_minus(wk.T1.p, ax.n, 0, bc, wk.tt_r0, wk.tt_r1, 0, bc, rlo, rhi, st);
-            else
-                zero_rect_minus(wk.T1.p, wk.tt_pitch, 0, wk.tt_rows, wk.tt_r0, wk.tt_r1, 0, 0, 0, 0, st);
-        }
-        launch_band_transpose(wk.T.p, n2, rlo, rhi, band2, bc, wk.T1.p, ax.n, st);
-        wk.tt_r0 = rlo;
-        wk.tt_r1 = rhi;
-        wk.tt_pitch = ax.n;
-        wk.tt_rows = bc;
         auto* Tt = reinterpret_cast<cufftDoubleComplex*>(wk.T1.p);
         auto* BT = reinterpret_cast<cufftDoubleComplex*>(wk.bandT.p);
-        ckfft(cufftSetStream(fft_colT, st), "cufftSetStream");
-        ckfft(cufftExecZ2Z(fft_colT, Tt, BT, CUFFT_INVERSE), "fft cols T");
+        if (crad_col > 1) {
+            // the transpose does the column transform's radix pass and writes
+            // every row of the band columns (no zero strips to keep)
+            launch_band_transpose_dif(wk.T.p + (size_t)rlo * n2, n2, rlo, rhi, band2, bc, wk.T1.p, ax.n, crad_col,
+                                      ctw_col.p, st, crad_row);
+            wk.tt_r0 = 0;
+            wk.tt_r1 = ax.n;
+            wk.tt_pitch = ax.n;
+            wk.tt_rows = bc;
+            ckfft(cufftSetStream(fft_colT_m, st), "cufftSetStream");
+            ckfft(cufftExecZ2Z(fft_colT_m, Tt, BT, CUFFT_INVERSE), "fft cols T (M)");
+        } else {
+            // Tt[c'][x] (pitch n1) holds band column c' over the populated rows only;
+            // every other row x of Tt stays zero (strips a previous plan left are cleared).
+            if (wk.tt_r1 > wk.tt_r0) {
+                if (wk.tt_pitch == ax.n && wk.tt_rows == bc)
+                    zero_rect_minus(wk.T1.p, ax.n, 0, bc, wk.tt_r0, wk.tt_r1, 0, bc, rlo, rhi, st);
+                else
+                    zero_rect_minus(wk.T1.p, wk.tt_pitch, 0, wk.tt_rows, wk.tt_r0, wk.tt_r1, 0, 0, 0, 0, st);
+            }
+            launch_band_transpose(wk.T.p, n2, rlo, rhi, band2, bc, wk.T1.p, ax.n, st, 0, 0, crad_row);
+            wk.tt_r0 = rlo;
+            wk.tt_r1 = rhi;
+            wk.tt_pitch = ax.n;
+            wk.tt_rows = bc;
+            ckfft(cufftSetStream(fft_colT, st), "cufftSetStream");
+            ckfft(cufftExecZ2Z(fft_colT, Tt, BT, CUFFT_INVERSE), "fft cols T");
+        }
         count_launch(2);
         if (tm) tm->stop();
         if (before_interp) ck(cudaStreamWaitEvent(st, before_interp, 0), "wait");
         if (tm) tm->start(tag_interp);
-        const GridGeom gt{ax.n, bc, 0.5 * w};
+        GridGeom gt{ax.n, bc, 0.5 * w};
+        if (crad_col > 1) {
+            gt.rad = crad_col;
+            gt.rad_m = ax.n / crad_col;
+            gt.rad_magic = (unsigned)((0x100000000ull + crad_col - 1) / crad_col);
+        }
         launch_interp(w, win, gt, nout, s_p, post_p, mult_p, dx.p, dy_band.p, wk.bandT.p, perm_p,
                       out_p, 0, 0, st, add_p, /*transposed=*/true, &otiles, hp, opts.interp_kernel, gop);
         if (tm) tm->stop();

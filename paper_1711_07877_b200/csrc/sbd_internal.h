@@ -252,6 +252,12 @@ class Plan {
     DevBuf<double> dy_band;
     cufftHandle fft_row = 0;
     cufftHandle fft_colT = 0;  // contiguous transforms of the transposed band columns
+    // radix first passes of the complex pipeline's two transforms in our own
+    // kernels (k_dif_rows / k_band_transpose_dif), cuFFT on contiguous
+    // length-n/r passes: 1 = cuFFT's own full-length transform
+    int crad_row = 1, crad_col = 1;
+    cufftHandle fft_row_m = 0, fft_colT_m = 0;
+    DevBuf<double2> ctw_row, ctw_col;
 
     // Hermitian-FFT mode for a real input (op.cpp). Role 1 (fwd_in): the
     // spread grid is real; its rows are packed in pairs into complex rows ->
@@ -446,8 +452,14 @@ void build_region_lists(const double2* pos, uint64_t n, int w, TileGeom tg, uint
                         DevBuf<uint32_t>& start, DevBuf<uint32_t>& ent, cudaStream_t st);
 // Tt[c * n1 + r] = T[(r - rin0) * n2 + m(c)] for r in [r0, r1), c < B,
 // m(c) = c (c <= b) else n2 - B + c
+// rin > 1: the rows of T are in the (j mod rin) n2/rin + j/rin order a radix-rin first
+// pass (launch_dif_rows) + length n2/rin transforms leave
 void launch_band_transpose(const double2* T, int n2, int r0, int r1, int b, int B, double2* Tt,
-                           int n1, cudaStream_t st, int rin0 = 0, int conj_out = 0);
+                           int n1, cudaStream_t st, int rin0 = 0, int conj_out = 0, int rin = 1);
+// the same with the radix-R first pass of the length n1 column transform folded in:
+// Tt[c n1 + s n1/R + k], rows of T counted from r0; tw[m] = e^{+2 pi i m / n1}
+void launch_band_transpose_dif(const double2* T, int n2, int r0, int r1, int b, int B, double2* Tt, int n1, int R,
+                               const double2* tw, cudaStream_t st, int rin = 1);
 void launch_mirror_points(const double2* t, uint64_t n, int n1, int n2, int w, double2* out,
                           cudaStream_t st);
 // b[k] = (conj_in ? conj : id)(in[perm ? perm[k] : k]) * phase[k]

@@ -420,6 +420,25 @@ def test_radix_first_pass_agrees(ops, name):
     assert rel_l2(q, ops[name].apply(f)) <= 1e-13
 
 
+@pytest.mark.parametrize("name", CASES)
+def test_radix_first_pass_complex_pipeline(ops, name):
+    # the complex pipeline (complex f; every Helmholtz apply): the radix first
+    # pass of the row transform as k_dif_rows and of the column transform folded
+    # into the band transpose (k_band_transpose_dif), cuFFT on contiguous
+    # length-M passes, the band read in (j mod r) M + j / r order by the staged,
+    # per-warp and scalar interpolations -- forced on wherever a grid length
+    # splits by 3, 5 or 9, against cuFFT's own full-length transforms
+    path, g = golden(name)
+    rng = np.random.default_rng(43)
+    f = rng.standard_normal(len(g["f"])) + 1j * rng.standard_normal(len(g["f"]))
+    plain = sbd.CompressedOperator.load(path, options=sbd.OpOptions(radix_first_pass=0))
+    want = plain.apply(f)
+    for ik in ("auto", "mma", "scalar"):
+        rad = sbd.CompressedOperator.load(path, options=sbd.OpOptions(radix_first_pass=1, interp_kernel=ik))
+        assert rel_l2(rad.apply(f), want) <= 1e-13, ik
+    assert rel_l2(ops[name].apply(f), want) <= 1e-13
+
+
 def test_radix_nine_both_transforms(reflib, tmp_path):
     # grids of 9 * 8k cells on both axes (config 4: 18432 = 9 x 2048): the
     # Hermitian pipelines then run the radix-9 first pass of both transforms of
