@@ -367,7 +367,8 @@ def run_b200(args, w):
 
         def step_slab():
             slab.apply(f_dev, q_dev)
-        step, alt_step = (step_slab, step_shard) if args.scheme == "slab" else (step_shard, step_slab)
+        scheme = "shard" if args.scheme == "shard" else "slab"  # auto: slab first, the faster one reported
+        step, alt_step = (step_slab, step_shard) if scheme == "slab" else (step_shard, step_slab)
     else:
         def step():  # the caller knows its f is real (sbd_op_apply_device_ex)
             op.apply_device(f_dev.data_ptr(), q_dev.data_ptr(), R, sh, f_is_real=f_real)
@@ -422,8 +423,16 @@ def run_b200(args, w):
         t = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_alt = float(t.item()) / args.steps
-        alt = {"scheme": "shard" if args.scheme == "slab" else "slab", "value": n / (ms_alt / 1e3),
+        alt = {"scheme": "shard" if scheme == "slab" else "slab", "value": n / (ms_alt / 1e3),
                "unit": "points/s", "ms_per_step": round(ms_alt, 3), "scaling": "strong"}
+        if args.scheme == "auto" and ms_alt < ms_step:
+            # both partitions were timed by the same protocol (K steps between
+            # barriers, max over ranks): the headline is the one an application
+            # would keep after this calibration, the other stays beside it
+            alt, scheme, ms_step = ({"scheme": scheme, "value": value, "unit": "points/s",
+                                     "ms_per_step": round(ms_step, 3), "scaling": "strong"},
+                                    alt["scheme"], ms_alt)
+            value = n * R / (ms_step / 1e3)
 
     rhs_par = None
     if world > 1:
@@ -686,7 +695,7 @@ def run_b200(args, w):
                        "l2": "inputs larger than L2 (grid + xi + D >> 126 MB)",
                        "parallelism": "single" if world == 1 else
                        ((f"slab x{world}: grids, xi nodes and targets split by position, two all-to-alls"
-                         if args.scheme == "slab" else
+                         if scheme == "slab" else
                          f"sharded x{world}: sources/targets/D rows split, all-reduce of the xi spectrum") +
                         (f" (gloo; {world} ranks share {ndev} GPU(s): functional run, not a scaling number)"
                          if shared else " (NCCL)")),
@@ -727,7 +736,7 @@ def main():
     ap.add_argument("--adjoint", type=int, default=1, help="1: also time apply_adjoint")
     ap.add_argument("--procedural", type=int, default=1,
                     help="1: also time the apply with procedural ring nodes (a second assemble)")
-    ap.add_argument("--scheme", default="slab", choices=["slab", "shard"],
+    ap.add_argument("--scheme", default="auto", choices=["auto", "slab", "shard"],
                     help="multi-GPU apply for N > 1: slab decomposition or the north_star source/target sharding")
     ap.add_argument("--ref-full", type=int, default=1,
                     help="1: one reference apply of the full config on one core after the timed region "

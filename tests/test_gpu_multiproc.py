@@ -70,5 +70,15 @@ def test_bench_gpus_2_runs_two_ranks():
     line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
     assert line["n_gpus"] == 2
     assert line["contract"]["ok"]
-    assert "slab x2" in line["config"]["parallelism"]
-    assert line["other_scheme"]["scheme"] == "shard" and line["rhs_parallel"]["scaling"] == "weak"
+    # both partitions are timed; the headline is the faster one (--scheme auto)
+    par, other = line["config"]["parallelism"], line["other_scheme"]
+    assert ("slab x2" in par and other["scheme"] == "shard") or ("sharded x2" in par and other["scheme"] == "slab")
+    assert line["value"] >= other["value"]
+    assert line["rhs_parallel"]["scaling"] == "weak"
+    forced = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "1",
+                             "--steps", "2", "--warmup", "3", "--nrhs", "1", "--no-cpu-baseline", "--scheme", "slab",
+                             "--adjoint", "0", "--procedural", "0"],
+                            capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert forced.returncode == 0, forced.stderr[-3000:]
+    fl = json.loads([x for x in forced.stdout.splitlines() if x.startswith("{")][-1])
+    assert "slab x2" in fl["config"]["parallelism"] and fl["contract"]["ok"]
