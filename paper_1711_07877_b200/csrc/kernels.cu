@@ -2048,20 +2048,39 @@ __global__ void k_band_fold(const double2* __restrict__ Z, int pz, int rlo, int 
 // Tz[(r - r0) n2 + m(c)] = Wt[c n1 + r]: the transposed band back into rows
 // (32 x 32 tiles through shared memory, both sides coalesced)
 __global__ void __launch_bounds__(256) k_band_untranspose(const double2* __restrict__ Wt, int n1, int r0, int r1,
-                                                          int b, int B, double2* __restrict__ Tz, int n2) {
+                                                          int b, int B, double2* __restrict__ Tz, int n2, int rin) {
+    // rin > 1: the columns of Wt come from a radix-rin first pass + length
+    // n1 / rin transforms: row r sits at (r mod rin) M + r / rin, and a CTA takes
+    // 32 consecutive positions of one residue class
     __shared__ double2 tile[32][33];
-    const int cb = blockIdx.x * 32, rb = r0 + blockIdx.y * 32;
+    const int cb = blockIdx.x * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    auto row_of = [&](int i, int& at) -> int {
+        if (rin > 1) {
+            const int M = n1 / rin, pos = blockIdx.y * 32 + i;
+            at = pos;
+            if (pos >= n1) return -1;
+            const int cls = pos / M, r = rin * (pos - cls * M) + cls;
+            return (r >= r0 && r < r1) ? r : -1;
+        }
+        const int r = r0 + blockIdx.y * 32 + i;
+        at = r;
+        return r < r1 ? r : -1;
+    };
 #pragma unroll
     for (int q = 0; q < 32; q += 8) {
-        const int c = cb + ty + q, r = rb + tx;
-        if (r < r1 && c < B) tile[ty + q][tx] = Wt[(size_t)c * n1 + r];
+        const int c = cb + ty + q;
+        int at;
+        const int r = row_of(tx, at);
+        if (r >= 0 && c < B) tile[ty + q][tx] = Wt[(size_t)c * n1 + at];
     }
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < 32; q += 8) {
-        const int r = rb + ty + q, c = cb + tx;
-        if (r < r1 && c < B) {
+        const int c = cb + tx;
+        int at;
+        const int r = row_of(ty + q, at);
+        if (r >= 0 && c < B) {
             const int m = c <= b ? c : n2 - B + c;
             Tz[(size_t)(r - r0) * n2 + m] = tile[tx][ty + q];
         }
@@ -3121,10 +3140,10 @@ void launch_band_fold(const double2* Z, int pz, int rlo, int rhi, int clo, int c
 }
 
 void launch_band_untranspose(const double2* Wt, int n1, int r0, int r1, int b, int B, double2* Tz, int n2,
-                             cudaStream_t st) {
+                             cudaStream_t st, int rin) {
     if (r1 <= r0) return;
-    dim3 grid((unsigned)((B + 31) / 32), (unsigned)((r1 - r0 + 31) / 32));
-    k_band_untranspose<<<grid, 256, 0, st>>>(Wt, n1, r0, r1, b, B, Tz, n2);
+    dim3 grid((unsigned)((B + 31) / 32), (unsigned)(((rin > 1 ? n1 : r1 - r0) + 31) / 32));
+    k_band_untranspose<<<grid, 256, 0, st>>>(Wt, n1, r0, r1, b, B, Tz, n2, rin);
     count_launch();
     ck(cudaGetLastError(), "k_band_untranspose");
 }

@@ -871,9 +871,17 @@ void Plan::apply_transpose_pruned(const double2* in, double2* out, cudaStream_t 
     if (tm) tm->start("fft_T");
     auto* V = reinterpret_cast<cufftDoubleComplex*>(T.V.p);
     auto* Wt = reinterpret_cast<cufftDoubleComplex*>(T.Wt.p);
-    ckfft(cufftSetStream(fft_colT, st), "cufftSetStream");
-    ckfft(cufftExecZ2Z(fft_colT, V, Wt, CUFFT_INVERSE), "fft cols T");
-    launch_band_untranspose(T.Wt.p, n1, rlo, rhi, band2, bc, T.Tz.p, n2, st);
+    if (crad_col > 1) {
+        // our radix pass along the contiguous band columns, then length-M
+        // transforms in place; the untranspose reads the permuted rows
+        launch_dif_rows(T.V.p, bc, n1, crad_col, 0, n1, ctw_col.p, T.Wt.p, st);
+        ckfft(cufftSetStream(fft_colT_m, st), "cufftSetStream");
+        ckfft(cufftExecZ2Z(fft_colT_m, Wt, Wt, CUFFT_INVERSE), "fft cols T (M)");
+    } else {
+        ckfft(cufftSetStream(fft_colT, st), "cufftSetStream");
+        ckfft(cufftExecZ2Z(fft_colT, V, Wt, CUFFT_INVERSE), "fft cols T");
+    }
+    launch_band_untranspose(T.Wt.p, n1, rlo, rhi, band2, bc, T.Tz.p, n2, st, crad_col);
     ckfft(cufftSetStream(fft_row, st), "cufftSetStream");
     ckfft(cufftExecZ2Z(fft_row, reinterpret_cast<cufftDoubleComplex*>(T.Tz.p),
                        reinterpret_cast<cufftDoubleComplex*>(T.G.p + (size_t)rlo * n2), CUFFT_INVERSE),

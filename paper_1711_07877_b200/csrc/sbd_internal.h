@@ -471,7 +471,7 @@ void launch_band_fold(const double2* Z, int pz, int rlo, int rhi, int clo, int c
                       int B, int n2, const double* dx, const double* dy, double2* V, cudaStream_t st);
 // Tz[(r - r0) n2 + m(c)] = Wt[c n1 + r] for r in [r0, r1), c < B (inverse of launch_band_transpose)
 void launch_band_untranspose(const double2* Wt, int n1, int r0, int r1, int b, int B, double2* Tz, int n2,
-                             cudaStream_t st);
+                             cudaStream_t st, int rin = 1);  // rin: Wt's columns in a radix first pass's order
 // out[l opitch + q] = in[q ipitch + ((j0 + l) mod nin)] for l < L, q < Q (a
 // transposing gather with a wrapped column window; the slab exchanges' packing)
 void launch_wrap_transpose(const double2* in, size_t ipitch, int nin, int j0, int L, int Q, double2* out,

@@ -433,9 +433,13 @@ def test_radix_first_pass_complex_pipeline(ops, name):
     f = rng.standard_normal(len(g["f"])) + 1j * rng.standard_normal(len(g["f"]))
     plain = sbd.CompressedOperator.load(path, options=sbd.OpOptions(radix_first_pass=0))
     want = plain.apply(f)
+    u = rng.standard_normal(len(g["u"])) + 1j * rng.standard_normal(len(g["u"]))
+    want_adj = plain.apply_adjoint(u)
     for ik in ("auto", "mma", "scalar"):
         rad = sbd.CompressedOperator.load(path, options=sbd.OpOptions(radix_first_pass=1, interp_kernel=ik))
         assert rel_l2(rad.apply(f), want) <= 1e-13, ik
+        # the adjoint's transposed column transforms take the same radix pass
+        assert rel_l2(rad.apply_adjoint(u), want_adj) <= 1e-13, ik
     assert rel_l2(ops[name].apply(f), want) <= 1e-13
 
 
