@@ -14,8 +14,10 @@ import paper_1711_07877_b200 as sbd  # noqa: E402
 w = bench.workload("4", 1.0)
 z = w["z"]
 d = sbd.cloud_diameter(z)
+ik = sys.argv[1] if len(sys.argv) > 1 else "auto"
 op = sbd.CompressedOperator.assemble(
-    sbd.kernel_laplace(), z, opts=sbd.AssembleOptions(eps=w["eps"], a_override=w["dmin"] / d, max_grid_bytes=96 << 30))
+    sbd.kernel_laplace(), z, opts=sbd.AssembleOptions(eps=w["eps"], a_override=w["dmin"] / d, max_grid_bytes=96 << 30,
+                                                      pipeline=sbd.OpOptions(interp_kernel=ik)))
 rng = np.random.default_rng(1)
 n = len(z)
 fc = (rng.standard_normal(n) + 1j * rng.standard_normal(n))
@@ -35,4 +37,4 @@ torch.cuda.synchronize()
 agg = {}
 for nm, ms in op.stage_times():
     agg[nm] = agg.get(nm, 0.0) + ms / 5
-print({"complex_ms_per_apply": e0.elapsed_time(e1) / 5, "stages": {k: round(v, 3) for k, v in agg.items()}})
+print({"interp_kernel": ik, "complex_ms_per_apply": e0.elapsed_time(e1) / 5, "stages": {k: round(v, 3) for k, v in agg.items()}})
