@@ -136,8 +136,9 @@ int sbd_op_get(const sbd_op* op, int which, void* dst, uint64_t* count);
  * (reference conv_operator.hpp:33-36); they are serialised, and device work
  * of successive calls is ordered across streams by an operator event. */
 /* q = A f for nrhs right-hand sides stored back to back (f: nrhs x n_src,
- * q: nrhs x n_tgt, interleaved complex). Host buffers; copies are inside
- * (chunked and overlapped; a real f moves only its real parts). */
+ * q: nrhs x n_tgt, interleaved complex). Host buffers; the H2D of f and the
+ * D2H of q are inside the call (synchronous: use sbd_op_apply_async to overlap
+ * them with neighbouring applies); realness of f is detected on the host. */
 int sbd_op_apply(sbd_op* op, const double* f, double* q, int nrhs);
 int sbd_op_apply_adjoint(sbd_op* op, const double* u, double* q, int nrhs);
 /* Pipelined host-buffer apply (no reference analogue): enqueues the H2D of f,
