@@ -53,7 +53,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         o = os.path.join(OBJ, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            _run([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-split-compile", "0", "-Xcompiler", "-fPIC",
+            _run([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
                   "-Xptxas", "-v" if verbose else "-O3", "-c", s, "-o", o], verbose)
     for src in CPP_SOURCES:
         s = os.path.join(CSRC, src)
